@@ -1,0 +1,332 @@
+#!/usr/bin/env python
+"""Benchmark: batched BOCD series*timesteps/s (R=1024, fp64) on B200 — BASELINE.json metric.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...       (one rank per GPU, NCCL)
+
+Workload (BASELINE.json configs[2], "C3"): 32,768 per-link communication-time
+series per GPU (weak scaling: rank g owns global series [g*32768, (g+1)*32768)),
+R = 1024, constant hazard 1/250, MERGE truncation, prior from the first
+observation (Q2/Q3/Q6), synthetic traces from the counter-based
+generator (tracegen.py recipe), generated in HBM before timing.  One bench
+"step" = one falcon_bocd_update_chunk call absorbing --chunk (default 1,000)
+new observations for every series of the rank: all of §8(a)'s rows.  The timed
+region ends with the change-point drain (falcon_bocd_changepoints) and, for
+N > 1, the NCCL all-gather of the events, then the max over ranks.
+
+Emits ONE JSON line on rank 0 (see DESIGN.md §7 for every field).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "BOCD series·timesteps/sec (R=1024, fp64) at 1/2/4/8 B200; % roofline"
+UNIT = "series*steps/s"
+# Algorithmic FP64-pipe work per cell (one run length, one step): DESIGN.md §6.
+#   12 arithmetic (NIG update 4, predictive 3, joint/growth/normalise 3, max/LSE 2)
+#   + 1 log (30 FP64-pipe instructions in libdevice) + 1 exp (18), both measured
+#   from SASS (cuobjdump) in P0 -> 60 FP64-pipe instructions per cell.
+FP64_INSTR_PER_CELL = 60
+# FP64 pipe peak: 148 SMs x 64 FP64 lanes/clk x 1965 MHz (sm_max_mhz, MEASURED_PEAKS.json);
+# P0 measured 58.9 DFMA/clk/SM sustained at 1965 MHz (profiles/r01_p0_fp64_peaks.json).
+SMS, FP64_PER_CLK_SM = 148, 64
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+           0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+           0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+           0x100: "display_clock_setting"}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,power.draw",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons, pw = [], [], set(), []
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 3:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+                bits = int(parts[2], 16)
+                for b, name in REASONS.items():
+                    if bits & b and name != "gpu_idle":
+                        reasons.add(name)
+                if len(parts) > 3:
+                    pw.append(float(parts[3]))
+            except ValueError:
+                continue
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(pw) if pw else None}
+
+
+def cpu_baseline_run(cfg, spec, n_series, T_s, s_offset=0):
+    """The fp64 oracle as it stands, on this host's cores, over a bounded sample."""
+    import oracle
+    from paper_2410_12588_b200 import tracegen
+    x = tracegen.generate(spec, s_offset, n_series, 0, T_s)
+    t0 = time.perf_counter()
+    oracle.run(x, cfg.R, cfg.hazard, cfg.kappa0, cfg.alpha0, prior_first_obs=True,
+               prior_cov=cfg.prior_cov, n_threads=0)
+    dt = time.perf_counter() - t0
+    return n_series * T_s / dt, dt
+
+
+def run_reference(args):
+    """--impl reference: the oracle (the deliberately slow CPU program) on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    from paper_2410_12588_b200 import tracegen
+    cfg = tracegen.CONFIGS[args.config]
+    spec = tracegen.make_spec(cfg, n_series=cfg.n_series)
+    cores = oracle.max_threads()
+    n_s = max(1, min(cfg.n_series // max(1, args.steps + args.warmup), 4 * cores))
+    T_s = min(cfg.T, args.ref_steps)
+    times = []
+    for k in range(args.warmup + args.steps):
+        _, dt = cpu_baseline_run(cfg, spec, n_s, T_s, s_offset=(k * n_s) % max(1, cfg.n_series - n_s))
+        if k >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    value = n_s * T_s * len(times) / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": _config_block(cfg, args, n_series_rank=cfg.n_series, world=1),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"each step: {n_s} C3 series x first {T_s} steps (R={cfg.R}, "
+                                   f"steps 0..{cfg.R - 1} have < R live run lengths)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _config_block(cfg, args, n_series_rank, world):
+    return {"workload": f"{cfg.name}: {cfg.n_series:,} per-link comm-time series x {cfg.T:,} steps, "
+                        f"R={cfg.R} (BASELINE.json configs[2]); timed: {args.steps} x {args.chunk} steps",
+            "series_per_gpu": n_series_rank, "series_global": n_series_rank * world, "R": cfg.R,
+            "hazard": cfg.hazard, "truncation": "merge", "chunk_steps": args.chunk,
+            "parallelism": f"series-sharded x{world}",
+            "l2": "no flush: every step streams a fresh x chunk and the whole state, both > 126 MB L2"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--chunk", type=int, default=1000, help="timesteps absorbed per bench step")
+    ap.add_argument("--series", type=int, default=0, help="series per GPU (default: the config's)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-steps", type=int, default=2048, help="oracle sample length (reference arm)")
+    ap.add_argument("--cpu-sample-steps", type=int, default=2048)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2410_12588_b200 import bocd, tracegen
+    from paper_2410_12588_b200.distributed import allgather_events, max_over_ranks
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = tracegen.CONFIGS[args.config]
+    S = args.series or cfg.n_series
+    s0 = rank * S
+    total = (args.warmup + args.steps) * args.chunk
+    assert total <= cfg.T, "warmup+steps exceed the workload length"
+    spec = tracegen.make_spec(cfg, n_series=S * world)
+    dtrace = bocd.DeviceTrace(spec, dev)
+    x = torch.empty((S, total), dtype=torch.float64, device=dev)
+    dtrace.generate(x, s0, 0)
+    torch.cuda.synchronize()
+
+    b = bocd.BocdBatch(S, R=cfg.R, hazard=cfg.hazard, kappa0=cfg.kappa0, alpha0=cfg.alpha0,
+                       prior_first_obs=True, prior_cov=cfg.prior_cov, threshold=cfg.threshold,
+                       trunc_mode="merge", event_mask=bocd.N.EV_PROB, event_capacity=256,
+                       device=local, series_base=s0)
+    stream = torch.cuda.current_stream()
+    C = args.chunk
+    for k in range(args.warmup):
+        b.update_chunk(x[:, k * C:(k + 1) * C])
+    b.changepoints()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev_start, ev_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k_start = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    k_end = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        time.sleep(0.3)
+        torch.cuda.synchronize()
+        ev_start.record(stream)
+        for k in range(args.steps):
+            c0 = (args.warmup + k) * C
+            k_start[k].record(stream)
+            b.update_chunk(x[:, c0:c0 + C])
+            k_end[k].record(stream)
+        recs, dropped = b.changepoints(device_out=True)
+        n_events_rank = int(recs.shape[0])
+        if world > 1:
+            gathered = allgather_events(recs)
+        ev_end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_ms = ev_start.elapsed_time(ev_end)
+    t_max = max_over_ranks(t_ms, dev)
+    k_ms = [a.elapsed_time(e) for a, e in zip(k_start, k_end)]
+    k_avg = sum(k_ms) / len(k_ms)
+    k_share = sum(k_ms) / t_ms
+    value = S * world * C * args.steps / (t_max * 1e-3)
+    nt, j, spb = b.kernel_shape()
+    cells_per_launch = S * C * cfg.R
+    achieved = FP64_INSTR_PER_CELL * cells_per_launch / (k_avg * 1e-3)
+    peaks = _peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    peak = SMS * FP64_PER_CLK_SM * sm_max * 1e6
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            tj = json.load(open(tpath))
+            if tj.get("series") and tj.get("chunk"):
+                # DRAM bytes scale with series x chunk for this kernel (x stream + one state pass)
+                traffic = tj["bytes_per_launch"] * (S * C) / (tj["series"] * tj["chunk"])
+        except Exception:
+            traffic = None
+    clocks = clk.summary()
+
+    # ---- e2e: host buffers through falcon_bocd_update_chunk_host + host drain ----------
+    e2e = None
+    if not args.no_e2e:
+        hb = [torch.empty((S, C), dtype=torch.float64).pin_memory() for _ in range(2)]
+        for i in range(2):
+            hb[i].copy_(x[:, (args.warmup + i) * C:(args.warmup + i + 1) * C])
+        b2 = bocd.BocdBatch(S, R=cfg.R, hazard=cfg.hazard, kappa0=cfg.kappa0, alpha0=cfg.alpha0,
+                            prior_first_obs=True, prior_cov=cfg.prior_cov, trunc_mode="merge",
+                            event_mask=bocd.N.EV_PROB, event_capacity=256, device=local,
+                            series_base=s0)
+        b2.update_chunk_host(hb[0])
+        b2.changepoints()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d2h = 0
+        e0.record(stream)
+        for k in range(args.steps):
+            b2.update_chunk_host(hb[k % 2])
+            evs, _ = b2.changepoints()
+            d2h += evs.nbytes + 16 + 4 + 8  # records + scan meta + sticky flag + pending count
+        e1.record(stream)
+        torch.cuda.synchronize()
+        et = max_over_ranks(e0.elapsed_time(e1), dev)
+        b2.close()
+        e2e = {"value": S * world * C * args.steps / (et * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": S * C * 8, "d2h_bytes_per_step": int(d2h / args.steps),
+               "api": "falcon_bocd_update_chunk_host + falcon_bocd_changepoints (pinned host x)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        cores = oracle.max_threads()
+        n_s = 8 * cores
+        v, dt = cpu_baseline_run(cfg, spec, n_s, args.cpu_sample_steps)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{n_s} C3 series x first {args.cpu_sample_steps} steps, R={cfg.R} "
+                         f"({dt:.1f} s; steps 0..{cfg.R - 1} have < R live run lengths)"}
+    b.close()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (counter-based generator, C3 recipe, generated in HBM)",
+            "config": _config_block(cfg, args, S, world),
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak,
+                         "unit": "FP64-pipe instr/s", "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "bocd_update_kernel<128,8,FULL>",
+                         "kernel_ms_avg": k_avg, "kernel_share_of_step": k_share,
+                         "work_per_cell": FP64_INSTR_PER_CELL,
+                         "peak_basis": f"{SMS} SMs x {FP64_PER_CLK_SM} FP64/clk x {sm_max:.0f} MHz (derived)"},
+            "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": args.steps + 3,
+            "clocks": clocks,
+            "events": {"rank0": n_events_rank, "dropped": bool(dropped)},
+            "kernel_shape": {"threads_per_series": nt, "cells_per_thread": j, "series_per_cta": spb},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,181 @@
+/*
+ * falcon_bocd.h — C ABI of the B200 batched Bayesian Online Change-Point
+ * Detection library (libfalcon_bocd.so).
+ *
+ * The operation is the run-length recursion of PAPER.md Appendix A
+ * (P:1316-1348), applied independently to each of n_series observation
+ * series (per-rank iteration times; per-link
+ * communication times), with:
+ *   - UPM predictive Pr(x_t | r_t, x_l): Gaussian with unknown
+ *     mean and variance under a Normal-Inverse-Gamma prior, i.e. a Student-t
+ *     predictive (reading Q1);
+ *   - change-point prior Pr(r_t | r_{t-1}): constant hazard H (Q2);
+ *   - normalisation Pr(r_t | x_{1:t});
+ *   - run lengths truncated at R slots (Q6): MERGE (slot R-1 is the ">= R-1"
+ *     bucket, default) or DROP (growth beyond R-1 discarded);
+ *   - the decision of P:770 ("reports t as a change-point if the likelihood
+ *     exceeds 0.9"), read as p_new_t = R_t(1) / (1 - R_t(0)) > threshold (Q4),
+ *     and the MAP run length r*_t = argmax_{1<=r<=R-1} R_t(r) (Q5).
+ * SPEC.md's bocd_update(state, x) -> (state, probability) is
+ * falcon_bocd_update_chunk with T = 1 for every series.
+ *
+ * Conventions (Q7, Q8): observations are 0-based, x_0 .. x_{T-1}.  After x_t,
+ * run-length slot r >= 1 is the open segment x_{t-r+1..t}; slot 0 is the mass
+ * of a change point right after x_t.  Before x_0 a segment starts with
+ * probability one.  No events are reported at global t = 0.
+ *
+ * All entry points return an int status: 0 = OK, > 0 = warning (results
+ * valid), < 0 = error.  Argument errors return immediately with no side
+ * effects.  All device work is enqueued on the caller's CUDA stream (passed
+ * as `void *stream`, a cudaStream_t; NULL = legacy default stream) and is
+ * asynchronous unless stated.  A handle must not be used from two host
+ * threads at once (no internal locking).  There is no CPU fallback:
+ * every call that computes runs CUDA kernels for sm_100a.
+ */
+#ifndef FALCON_BOCD_H
+#define FALCON_BOCD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FALCON_BOCD_ABI_VERSION 1
+
+enum {
+    FALCON_OK = 0,
+    FALCON_WARN_EVENTS_DROPPED = 1, /* an event buffer overflowed since the last drain        */
+    FALCON_EINVAL = -1,             /* invalid argument (message in falcon_bocd_last_error)    */
+    FALCON_ECUDA = -2,              /* CUDA runtime error (message in falcon_bocd_last_error)  */
+    FALCON_ENOMEM = -3,             /* device or host allocation failed                        */
+    FALCON_ENONFINITE = -4,         /* a NaN/Inf observation was seen (Q13); sticky            */
+    FALCON_ESTATE = -5              /* handle poisoned by an earlier ENONFINITE / ECUDA        */
+};
+
+enum { FALCON_TRUNC_MERGE = 0, FALCON_TRUNC_DROP = 1 };
+enum { FALCON_EV_PROB = 1u, FALCON_EV_MAPRESET = 2u };
+
+typedef struct falcon_bocd_s *falcon_bocd_t; /* opaque; owns all device state */
+
+typedef struct {
+    int64_t n_series;        /* S >= 1                                                        */
+    int32_t R;               /* run-length slots, 2 <= R <= 4096                               */
+    double hazard;           /* H, 0 < H < 1 (Q2)                                      */
+    double kappa0, alpha0;   /* NIG prior, > 0, shared by all series                           */
+    const double *mu0;       /* HOST [n_series] prior means, or NULL -> mu0_scalar              */
+    double mu0_scalar;
+    const double *beta0;     /* HOST [n_series] prior scales (> 0), or NULL -> beta0_scalar     */
+    double beta0_scalar;
+    int32_t prior_first_obs; /* 1: mu0 = x_0 and beta0 = alpha0 * (prior_cov * x_0)^2 per series
+                                (Q3); overrides mu0 / beta0                          */
+    double prior_cov;        /* coefficient of variation for prior_first_obs                   */
+    double threshold;        /* theta of P:770, default 0.9                                     */
+    int32_t trunc_mode;      /* FALCON_TRUNC_MERGE (default) or FALCON_TRUNC_DROP               */
+    uint32_t event_mask;     /* which flags produce events, default FALCON_EV_PROB              */
+    int32_t event_capacity;  /* events kept per series between drains, >= 1, default 64         */
+    int32_t device;          /* CUDA device ordinal; the handle is bound to it                  */
+    int64_t series_base;     /* global id of local series 0, written into event records (sharded
+                                multi-GPU runs); default 0                                      */
+} falcon_bocd_config;
+
+/* One reported change point.  t: global step; cp_index = t - r*_t + 1, the
+ * first index of the MAP segment; flags: FALCON_EV_*; p_new as defined above. */
+typedef struct {
+    int64_t series;
+    int64_t t;
+    int64_t cp_index;
+    uint32_t flags;
+    uint32_t reserved;
+    double p_new;
+} falcon_bocd_event;
+
+/* Optional per-step outputs, each [n_series][ld] (column = step index within
+ * the call, 0..T-1).  Pointers are DEVICE memory for update_chunk and HOST
+ * memory for update_chunk_host; any may be NULL. */
+typedef struct {
+    int32_t *map_rl;  /* r*_t                                   */
+    double *p_new;    /* R_t(1) / (1 - R_t(0))                  */
+    double *log_z;    /* log Pr(x_t | x_{<t})                   */
+    int64_t ld;       /* >= T                                   */
+} falcon_bocd_step_out;
+
+/* Fills *cfg with defaults (R = 1024, H = 1/250, kappa0 = alpha0 = 1,
+ * mu0 = 0, beta0 = 1, threshold 0.9, MERGE, EV_PROB, capacity 64, device 0). */
+int falcon_bocd_config_init(falcon_bocd_config *cfg);
+
+/* Allocates the handle: per-series state (3 x R fp64 per series: mu, beta,
+ * unnormalised log posterior), the per-R predictive constant table and the
+ * event buffers on cfg->device.  The state starts at the prior (no data).
+ * Returns FALCON_EINVAL on a bad config, FALCON_ENOMEM if device memory runs out. */
+int falcon_bocd_create(const falcon_bocd_config *cfg, falcon_bocd_t *out);
+
+/* Absorbs T >= 0 new observations per series: x_dev is DEVICE memory,
+ * row-major [n_series][ld] fp64 (ld >= T; rows 16-byte aligned enables the
+ * TMA bulk-copy path).  Stream-ordered; x_dev and outs must stay valid until
+ * the work completes.  Results are bit-identical for every split of the same
+ * data into calls. */
+int falcon_bocd_update_chunk(falcon_bocd_t h, const double *x_dev, int64_t ld, int64_t T,
+                             const falcon_bocd_step_out *outs, void *stream);
+
+/* Same, with HOST x (pinned memory recommended) and HOST outs: the library
+ * copies the chunk to the device (internal staging buffers, copy overlapped
+ * with the previous call's compute), runs the same kernel, and copies the
+ * requested outputs back.  Synchronous with respect to the host buffers:
+ * returns after outs are written and x may be reused. */
+int falcon_bocd_update_chunk_host(falcon_bocd_t h, const double *x_host, int64_t ld, int64_t T,
+                                  const falcon_bocd_step_out *outs, void *stream);
+
+/* Drains the per-series event buffers into out[capacity] (HOST or DEVICE
+ * memory, detected), in (series, t) order, and resets them.  *n_out receives
+ * the number written.  Synchronises `stream`.  Returns FALCON_WARN_EVENTS_DROPPED
+ * if any series overflowed event_capacity since the last drain (the first
+ * event_capacity events of each series are kept), FALCON_EINVAL if capacity is
+ * smaller than the number of buffered events (nothing is drained; *n_out = the
+ * number needed), FALCON_ENONFINITE if a non-finite observation was seen. */
+int falcon_bocd_changepoints(falcon_bocd_t h, falcon_bocd_event *out, int64_t capacity,
+                             int64_t *n_out, void *stream);
+
+/* Number of buffered events (synchronises `stream`). */
+int falcon_bocd_pending_events(falcon_bocd_t h, int64_t *n_out, void *stream);
+
+/* Copies the normalised log run-length posterior log Pr(r_t = r | x_{1:t}) and
+ * the NIG statistics (mu_r, beta_r) of series [s0, s0+count) in RUN-LENGTH
+ * order into HOST or DEVICE arrays [count][R] (any pointer may be NULL).
+ * Synchronises `stream`. */
+int falcon_bocd_read_posterior(falcon_bocd_t h, int64_t s0, int64_t count, double *logR_out,
+                               double *mu_out, double *beta_out, void *stream);
+
+/* Number of observations absorbed so far (the next global t). */
+int falcon_bocd_steps(falcon_bocd_t h, int64_t *t_out);
+
+/* Threads per series group and cells per thread of the kernel variant bound to
+ * this handle (for the bench / roofline bookkeeping). */
+int falcon_bocd_kernel_shape(falcon_bocd_t h, int32_t *threads_per_series, int32_t *cells_per_thread,
+                             int32_t *series_per_cta);
+
+/* Releases every resource of the handle.  NULL is accepted.  Synchronises the device. */
+int falcon_bocd_destroy(falcon_bocd_t h);
+
+/* Per-handle message of the last error (h may be NULL: the last create error).
+ * Valid until the next call on that handle. */
+const char *falcon_bocd_last_error(falcon_bocd_t h);
+
+int falcon_bocd_abi_version(void);
+
+/* Host-only helper (no device work): the per-run-length predictive constants
+ * the kernels use, for r = 0..R-1 with kappa_r = kappa0 + r, alpha_r = alpha0 + r/2:
+ *   c[r]  = lgamma(alpha_r + 1/2) - lgamma(alpha_r) - 1/2 log(2 pi (kappa_r + 1) / kappa_r)
+ *   a[r]  = alpha_r
+ *   g[r]  = kappa_r / (2 (kappa_r + 1))
+ *   k1[r] = 1 / (kappa_r + 1)
+ * (Student-t normaliser of P:1345's UPM predictive; evaluated in long double
+ * and rounded once.)  Any output pointer may be NULL. */
+int falcon_bocd_predictive_constants(int32_t R, double kappa0, double alpha0, double *c, double *a,
+                                     double *g, double *k1);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FALCON_BOCD_H */

@@ -54,7 +54,8 @@ double oracle_student_t_logpdf(double x, double mu, double kappa, double alpha, 
 {
     double nu = 2.0 * alpha;
     double scale2 = beta * (kappa + 1.0) / (alpha * kappa);
-    long double dl = lgammal(0.5L * ((long double)nu + 1.0L)) - lgammal(0.5L * (long double)nu);
+    int sg1, sg2; /* lgammal_r: the reentrant lgammal (no shared signgam between threads) */
+    long double dl = lgammal_r(0.5L * ((long double)nu + 1.0L), &sg1) - lgammal_r(0.5L * (long double)nu, &sg2);
     double z2 = (x - mu) * (x - mu) / (nu * scale2);
     return (double)dl - 0.5 * log(nu * M_PI * scale2) - 0.5 * (nu + 1.0) * log1p(z2);
 }

@@ -1,0 +1,201 @@
+"""Thin Python binding over the C ABI (same names, argument marshalling only).
+
+Every step of the BOCD hot path runs in the CUDA kernels of libfalcon_bocd.so;
+PyTorch supplies device memory and streams.  Nothing here computes.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native as N
+
+EVENT_DTYPE = np.dtype([("series", np.int64), ("t", np.int64), ("cp_index", np.int64),
+                        ("flags", np.uint32), ("reserved", np.uint32), ("p_new", np.float64)])
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+class BocdBatch:
+    """falcon_bocd_create / _update_chunk / _changepoints / _read_posterior / _destroy."""
+
+    def __init__(self, n_series: int, R: int = 1024, hazard: float = 1.0 / 250.0,
+                 kappa0: float = 1.0, alpha0: float = 1.0, mu0=0.0, beta0=1.0,
+                 prior_first_obs: bool = False, prior_cov: float = 0.05, threshold: float = 0.9,
+                 trunc_mode: str | int = "merge", event_mask: int = N.EV_PROB,
+                 event_capacity: int = 64, device: int | None = None, series_base: int = 0):
+        L = N.lib()
+        cfg = N.Config()
+        N.check(L.falcon_bocd_config_init(ctypes.byref(cfg)))
+        if device is None:
+            device = torch.cuda.current_device()
+        cfg.n_series = int(n_series)
+        cfg.R = int(R)
+        cfg.hazard = float(hazard)
+        cfg.kappa0 = float(kappa0)
+        cfg.alpha0 = float(alpha0)
+        keep = []
+        for name in ("mu0", "beta0"):
+            val = mu0 if name == "mu0" else beta0
+            arr = np.asarray(val, dtype=np.float64)
+            if arr.ndim == 0:
+                setattr(cfg, name, None)
+                setattr(cfg, name + "_scalar", float(arr))
+            else:
+                arr = np.ascontiguousarray(arr.reshape(int(n_series)))
+                keep.append(arr)
+                setattr(cfg, name, arr.ctypes.data)
+        cfg.prior_first_obs = int(bool(prior_first_obs))
+        cfg.prior_cov = float(prior_cov)
+        cfg.threshold = float(threshold)
+        if isinstance(trunc_mode, str):
+            trunc_mode = {"merge": N.TRUNC_MERGE, "drop": N.TRUNC_DROP}[trunc_mode.lower()]
+        cfg.trunc_mode = int(trunc_mode)
+        cfg.event_mask = int(event_mask)
+        cfg.event_capacity = int(event_capacity)
+        cfg.device = int(device)
+        cfg.series_base = int(series_base)
+        h = ctypes.c_void_p()
+        N.check(L.falcon_bocd_create(ctypes.byref(cfg), ctypes.byref(h)), None)
+        self._h = h
+        self.n_series, self.R, self.device = int(n_series), int(R), torch.device("cuda", int(device))
+        self.event_capacity = int(event_capacity)
+
+    # -- hot path ---------------------------------------------------------------
+    def update_chunk(self, x: torch.Tensor, outputs: bool = False, stream=None):
+        """Absorb x[:, :T] (device fp64, row stride x.stride(0)).  With outputs=True returns
+        (map_rl int32, p_new fp64, log_z fp64), each [S][T] on the device."""
+        assert x.is_cuda and x.dtype == torch.float64 and x.dim() == 2 and x.stride(1) == 1
+        assert x.shape[0] == self.n_series
+        T = x.shape[1]
+        outs, res = None, None
+        if outputs:
+            res = (torch.empty((self.n_series, T), dtype=torch.int32, device=x.device),
+                   torch.empty((self.n_series, T), dtype=torch.float64, device=x.device),
+                   torch.empty((self.n_series, T), dtype=torch.float64, device=x.device))
+            outs = N.StepOut(res[0].data_ptr(), res[1].data_ptr(), res[2].data_ptr(), T)
+        N.check(N.lib().falcon_bocd_update_chunk(self._h, _ptr(x), x.stride(0), T,
+                                                 ctypes.byref(outs) if outs else None,
+                                                 _stream_ptr(stream)), self._h)
+        return res
+
+    def update_chunk_host(self, x: np.ndarray | torch.Tensor, outputs: bool = False, stream=None):
+        """Absorb HOST x[S][T] (pinned recommended); copies happen inside the library."""
+        if isinstance(x, torch.Tensor):
+            assert x.device.type == "cpu" and x.dtype == torch.float64 and x.stride(1) == 1
+            ptr, ld, T = x.data_ptr(), x.stride(0), x.shape[1]
+        else:
+            assert x.dtype == np.float64 and x.strides[1] == 8
+            ptr, ld, T = x.ctypes.data, x.strides[0] // 8, x.shape[1]
+        outs, res = None, None
+        if outputs:
+            res = (np.empty((self.n_series, T), np.int32), np.empty((self.n_series, T)),
+                   np.empty((self.n_series, T)))
+            outs = N.StepOut(res[0].ctypes.data, res[1].ctypes.data, res[2].ctypes.data, T)
+        N.check(N.lib().falcon_bocd_update_chunk_host(self._h, ctypes.c_void_p(ptr), ld, T,
+                                                      ctypes.byref(outs) if outs else None,
+                                                      _stream_ptr(stream)), self._h)
+        return res
+
+    def changepoints(self, stream=None, device_out: bool = False):
+        """Drain buffered events in (series, t) order.  Returns (events, dropped) where events
+        is a numpy structured array (host) or a uint8 device tensor of 40-B records."""
+        L = N.lib()
+        n = ctypes.c_int64()
+        N.check(L.falcon_bocd_pending_events(self._h, ctypes.byref(n), _stream_ptr(stream)), self._h)
+        cap = int(n.value)
+        if device_out:
+            buf = torch.empty((max(cap, 1), EVENT_DTYPE.itemsize), dtype=torch.uint8, device=self.device)
+            ptr = ctypes.c_void_p(buf.data_ptr())
+        else:
+            buf = np.empty(max(cap, 1), dtype=EVENT_DTYPE)
+            ptr = ctypes.c_void_p(buf.ctypes.data)
+        rc = N.check(L.falcon_bocd_changepoints(self._h, ptr, cap, ctypes.byref(n),
+                                                _stream_ptr(stream)), self._h)
+        return buf[: int(n.value)], rc == N.FALCON_WARN_EVENTS_DROPPED
+
+    def read_posterior(self, s0: int = 0, count: int | None = None, stream=None):
+        """(logR, mu, beta) as device tensors [count][R] in run-length order."""
+        count = self.n_series - s0 if count is None else count
+        out = [torch.empty((count, self.R), dtype=torch.float64, device=self.device) for _ in range(3)]
+        N.check(N.lib().falcon_bocd_read_posterior(self._h, s0, count, _ptr(out[0]), _ptr(out[1]),
+                                                   _ptr(out[2]), _stream_ptr(stream)), self._h)
+        return tuple(out)
+
+    @property
+    def steps(self) -> int:
+        t = ctypes.c_int64()
+        N.check(N.lib().falcon_bocd_steps(self._h, ctypes.byref(t)), self._h)
+        return int(t.value)
+
+    def kernel_shape(self):
+        a, b, c = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        N.check(N.lib().falcon_bocd_kernel_shape(self._h, ctypes.byref(a), ctypes.byref(b),
+                                                 ctypes.byref(c)), self._h)
+        return int(a.value), int(b.value), int(c.value)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            rc = N.lib().falcon_bocd_destroy(self._h)
+            self._h = None
+            if rc not in (N.FALCON_OK, N.FALCON_ENONFINITE):  # ENONFINITE was reported earlier
+                N.check(rc, None)
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                N.lib().falcon_bocd_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+def predictive_constants(R: int, kappa0: float, alpha0: float):
+    """Host-only table (c_r, alpha_r, g_r, 1/(kappa_r+1)) used by the kernels."""
+    out = [np.empty(R) for _ in range(4)]
+    N.check(N.lib().falcon_bocd_predictive_constants(int(R), float(kappa0), float(alpha0),
+                                                     *[o.ctypes.data for o in out]))
+    return tuple(out)
+
+
+class DeviceTrace:
+    """Device copy of a tracegen.TraceSpec, for falcon_trace_generate."""
+
+    def __init__(self, spec, device):
+        dev = torch.device(device)
+        self.spec = spec
+        t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a), dtype=dt).to(dev)
+        self._b = t(spec.b, torch.float64)
+        self._sigma = t(spec.sigma, torch.float64)
+        self._off = t(spec.ep_off, torch.int64)
+        E = max(1, len(spec.ep_start))
+        pad = lambda a, dt: t(np.resize(a, E) if len(a) else np.zeros(E), dt)
+        self._st = pad(spec.ep_start, torch.int64)
+        self._en = pad(spec.ep_end, torch.int64)
+        self._ls = pad(spec.ep_logsev, torch.float64)
+        self.c = N.TraceSpecC(spec.seed, spec.n_series, spec.gamma, self._b.data_ptr(),
+                              self._sigma.data_ptr(), self._off.data_ptr(), self._st.data_ptr(),
+                              self._en.data_ptr(), self._ls.data_ptr())
+
+    def generate(self, out: torch.Tensor, s0: int, t0: int, stream=None):
+        """out[i, j] = x(s0 + i, t0 + j) (device fp64 [count][T] with row stride out.stride(0))."""
+        assert out.is_cuda and out.dtype == torch.float64 and out.stride(1) == 1
+        N.check(N.lib().falcon_trace_generate(ctypes.byref(self.c), _ptr(out), out.stride(0), s0,
+                                              out.shape[0], t0, out.shape[1], _stream_ptr(stream)))
+        return out

@@ -1,0 +1,479 @@
+// bocd_kernel.cuh — resident batched BOCD kernel for sm_100a (fp64).
+//
+// One series group of NT threads owns one series; each thread owns J run-length
+// cells.  The R cells of a series live in a RING indexed by position
+// p = (segment start time) mod R (p = i + NT*j for thread i, register j): at
+// global step t the cell at position p holds run length r = (t - p) mod R
+// BEFORE x_t is absorbed, so growth r -> r+1 (App. A)
+// moves no data, and the position that truncation at R recycles (r = R-1) is
+// exactly the one that becomes the new change-point cell.  Per-r constants of
+// the Student-t predictive come from a shared-memory table indexed by r.
+//
+// Per step (all fp64, no fast-math):
+//   A1  NIG update           mu' = mu + d/(kappa+1),  beta' = beta + kappa d^2 / (2(kappa+1))
+//   A2  Student-t predictive l_r = c_r + alpha_r (log beta - log beta') - 1/2 log beta'
+//       (= c_r - 1/2 log beta - (alpha_r + 1/2) log1p(kappa d^2 / (2 beta (kappa+1))))
+//   A3/A4  lp_r = v_r + l_r;  group max/argmax (one 64-bit key per cell, REDUX) then
+//       sum_r exp(lp_r - M) (xor-butterfly, fixed order => deterministic)
+//   A5  v'_{r+1} = lp_r - M + log(1-H);  v'_0 = log H + log(sum);  the posterior is kept
+//       UNNORMALISED (log R_t = v' - N_t, N_t = log sum_r e^{v'_r}); only the tail needs N_t
+//   A6  MERGE: v'_{R-1} = log(1-H) + log(e_{R-2} + e_{R-1});  DROP: e_{R-1} discarded
+//   A7  r*, p_new = e_0/sum (MERGE) or e_0/(sum - e_{R-1}) (DROP), flags, events
+// State stays in registers for the whole call; x is staged per series in
+// double-buffered shared-memory tiles by 1-D TMA bulk copies (cp.async.bulk +
+// mbarrier); state is spilled to HBM (coalesced) once per call.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fbocd {
+
+constexpr int kTile = 256;  // x steps per shared-memory tile (2 KB)
+
+struct SeriesScalars {  // per-series state carried between calls (HBM), 48 B
+    double mu0, beta0;  // prior (set from x_0 when prior_first_obs)
+    double n_prev;      // N_{t-1} = log sum_r exp(v_r): the normaliser of the stored v
+    int32_t map_prev;   // r*_{t-1}
+    int32_t ev_count;   // events appended since the last drain (may exceed capacity)
+    int32_t flags;      // bit0: non-finite observation seen; bit1: beta0 <= 0
+    int32_t pad;
+    double pad2;
+};
+
+struct EventRec {  // 32 B, series id implicit
+    int64_t t;
+    int64_t cp_index;
+    uint32_t flags;
+    uint32_t pad;
+    double p_new;
+};
+
+struct KParams {
+    int R;
+    int64_t S;
+    double logH, log1mH, omH, theta, alpha0, prior_cov;
+    int mode;  // 0 MERGE, 1 DROP
+    int prior_first_obs;
+    uint32_t ev_mask;
+    int ev_cap;
+    const double2* tab_ca;  // [R] {c_r, alpha_r}
+    const double2* tab_gk;  // [R] {g_r, 1/(kappa_r+1)}
+    double* st_mu;          // [S][R] position order
+    double* st_beta;
+    double* st_v;
+    SeriesScalars* scal;  // [S]
+    EventRec* ev;         // [S][ev_cap]
+    unsigned* err;        // sticky device error bits
+    const double* x;      // [S][ld] chunk, column 0 = global step t0
+    int64_t ld;
+    int T;
+    int64_t t0;
+    int32_t* out_map;  // [S][ld_o] or null
+    double* out_pnew;
+    double* out_logz;
+    int64_t ld_o;
+    int tma_ok;  // x base 16-B aligned and ld even
+};
+
+template <int NT>
+struct __align__(16) GroupSmem {
+    double xbuf[2][kTile];
+    unsigned long long red1[NT / 32 > 0 ? NT / 32 : 1];
+    double red2[NT / 32 > 0 ? NT / 32 : 1];
+    double spec[2][8];  // [parity][0 lpA,1 lpB,2 e0,3 eA,4 eB,5 eex]
+    double mu0, beta0, L0, n_prev;
+    int map_prev, ev_count, flags, pad;
+    unsigned long long mbar[2];
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        " .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+template <int NT>
+__device__ __forceinline__ void group_sync(int g) {
+    if constexpr (NT == 32) {
+        __syncwarp();
+    } else {
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(NT) : "memory");
+    }
+}
+
+// Order-preserving map of a non-NaN double to a signed 64-bit key.
+__device__ __forceinline__ long long ord_key(double v) {
+    long long b = __double_as_longlong(v);
+    return b >= 0 ? b : (b ^ 0x7FFFFFFFFFFFFFFFLL);
+}
+__device__ __forceinline__ double ord_val(long long k) {
+    long long b = k >= 0 ? k : (k ^ 0x7FFFFFFFFFFFFFFFLL);
+    return __longlong_as_double(b);
+}
+
+// Issues (or performs) the load of x tile k for this group.  TMA path: one
+// elected thread, completion on gs.mbar[k & 1].  Returns true if the tile was
+// loaded synchronously (caller must group_sync before reading).
+template <int NT>
+__device__ __forceinline__ void issue_tile_tma(GroupSmem<NT>& gs, const double* xrow, int k, int T) {
+    const int base = k * kTile;
+    const int n = min(kTile, T - base);
+    fence_proxy_async();
+    mbar_arrive_expect_tx(&gs.mbar[k & 1], unsigned(n) * 8u);
+    tma_load_1d(gs.xbuf[k & 1], xrow + base, unsigned(n) * 8u, &gs.mbar[k & 1]);
+}
+
+template <int NT>
+__device__ __forceinline__ bool tile_tma_ok(const KParams& P, int k) {
+    const int n = min(kTile, P.T - k * kTile);
+    return P.tma_ok && ((n & 1) == 0);
+}
+
+// ---------------------------------------------------------------------------
+// The kernel.  FULL: R == NT*J (power of two) known at compile time.
+// ---------------------------------------------------------------------------
+template <int NT, int J, bool FULL, int SPB, int MINB>
+__global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParams P) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int R = FULL ? NT * J : P.R;
+    double2* s_ca = reinterpret_cast<double2*>(smem_raw);
+    double2* s_gk = s_ca + R;
+    GroupSmem<NT>* groups = reinterpret_cast<GroupSmem<NT>*>(s_gk + R);
+
+    for (int k = threadIdx.x; k < R; k += blockDim.x) {
+        s_ca[k] = P.tab_ca[k];
+        s_gk[k] = P.tab_gk[k];
+    }
+    const int g = threadIdx.x / NT;
+    const int i = threadIdx.x % NT;
+    const int lane = threadIdx.x & 31;
+    const int w = i >> 5;
+    GroupSmem<NT>& gs = groups[g];
+    const int64_t s = int64_t(blockIdx.x) * SPB + g;
+    const bool active = s < P.S;
+    const double* xrow = P.x + (active ? s : 0) * P.ld;
+    const int ntiles = (P.T + kTile - 1) / kTile;
+    if (i == 0) {
+        mbar_init(&gs.mbar[0], 1);
+        mbar_init(&gs.mbar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (!active) return;
+
+    // Prefetch tile 0 (TMA) as early as possible.
+    if (i == 0 && ntiles > 0 && tile_tma_ok<NT>(P, 0)) issue_tile_tma<NT>(gs, xrow, 0, P.T);
+
+    // ---- load or initialise the state ------------------------------------
+    double mu[J], be[J], L[J], v[J];
+    const int64_t sbase = s * int64_t(R);
+    if (i == 0) {
+        SeriesScalars sc = P.scal[s];
+        if (P.t0 == 0) {
+            if (P.prior_first_obs && P.T > 0) {
+                const double x0 = xrow[0];
+                sc.mu0 = x0;
+                sc.beta0 = P.alpha0 * (P.prior_cov * x0) * (P.prior_cov * x0);
+            }
+            sc.n_prev = 0.0;
+            sc.map_prev = 0;
+        }
+        gs.mu0 = sc.mu0;
+        gs.beta0 = sc.beta0;
+        gs.L0 = log(sc.beta0);
+        gs.n_prev = sc.n_prev;
+        gs.map_prev = sc.map_prev;
+        gs.ev_count = sc.ev_count;
+        gs.flags = sc.flags | ((sc.beta0 > 0.0 && isfinite(sc.beta0) && isfinite(sc.mu0)) ? 0 : 2);
+    }
+    group_sync<NT>(g);
+    const double mu0 = gs.mu0, beta0 = gs.beta0, L0 = gs.L0;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+        const int p = i + NT * j;
+        if (FULL || p < R) {
+            if (P.t0 == 0) {
+                mu[j] = mu0;
+                be[j] = beta0;
+                L[j] = L0;
+                v[j] = (p == 0) ? 0.0 : -INFINITY;
+            } else {
+                mu[j] = P.st_mu[sbase + p];
+                be[j] = P.st_beta[sbase + p];
+                v[j] = P.st_v[sbase + p];
+                L[j] = log(be[j]);
+            }
+        } else {
+            mu[j] = mu0;
+            be[j] = beta0;
+            L[j] = L0;
+            v[j] = -INFINITY;
+        }
+    }
+
+    const double logH = P.logH, log1mH = P.log1mH;
+    const bool merge = (P.mode == 0);
+    // argmax-eligible run lengths: MERGE r <= R-3 (slot R-1 is the bucket), DROP r <= R-2
+    const int r_elig = merge ? R - 3 : R - 2;
+    const unsigned long long KEY_NONE = 0ull;  // below every real key (biased order)
+    // ring position bookkeeping: tmod = t mod R
+    int tmod = int(P.t0 % R);
+    bool nonfinite = false;
+
+    for (int k = 0; k < ntiles; ++k) {
+        const int base = k * kTile;
+        const int n = min(kTile, P.T - base);
+        const int buf = k & 1;
+        // prefetch the next tile into the other buffer (its previous readers all
+        // passed at least one group barrier since their last read)
+        if (i == 0 && k + 1 < ntiles && tile_tma_ok<NT>(P, k + 1)) issue_tile_tma<NT>(gs, xrow, k + 1, P.T);
+        if (tile_tma_ok<NT>(P, k)) {
+            mbar_wait(&gs.mbar[buf], unsigned(k >> 1) & 1u);
+        } else {
+            for (int q = i; q < n; q += NT) gs.xbuf[buf][q] = xrow[base + q];
+            group_sync<NT>(g);
+        }
+        for (int q = 0; q < n; ++q) {
+            const int tl = base + q;
+            const int64_t t = P.t0 + tl;
+            const int par = tl & 1;
+            const double x = gs.xbuf[buf][q];
+            // ---- phase 1: A1 + A2 + A3, local argmax key ----------------
+            unsigned long long key = KEY_NONE;
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                const int p = i + NT * j;
+                if (FULL || p < R) {
+                    int r = tmod - p;
+                    if (FULL) {
+                        r &= (R - 1);
+                    } else {
+                        r += (r < 0) ? R : 0;
+                    }
+                    const double2 ca = s_ca[r];
+                    const double2 gk = s_gk[r];
+                    const double d = x - mu[j];
+                    const double gd = gk.x * d;
+                    const double bn = fma(gd, d, be[j]);
+                    mu[j] = fma(d, gk.y, mu[j]);
+                    const double Ln = log(bn);
+                    const double ell = fma(-0.5, Ln, fma(ca.y, L[j] - Ln, ca.x));
+                    be[j] = bn;
+                    L[j] = Ln;
+                    const double lp = v[j] + ell;
+                    v[j] = lp;
+                    if (r <= r_elig) {
+                        const unsigned long long kk =
+                            (static_cast<unsigned long long>((ord_key(lp) & ~0xFFFLL)) | (0xFFFull - r)) ^
+                            0x8000000000000000ull;
+                        key = kk > key ? kk : key;
+                    }
+                    if (r == R - 2) gs.spec[par][0] = lp;
+                    if (r == R - 1) gs.spec[par][1] = lp;
+                }
+            }
+            // ---- group max/argmax --------------------------------------
+            {
+                const unsigned hi = unsigned(key >> 32);
+                const unsigned hmax = __reduce_max_sync(0xffffffffu, hi);
+                const unsigned lmax = __reduce_max_sync(0xffffffffu, hi == hmax ? unsigned(key) : 0u);
+                key = (static_cast<unsigned long long>(hmax) << 32) | lmax;
+            }
+            if constexpr (NT > 32) {
+                if (lane == 0) gs.red1[w] = key;
+                group_sync<NT>(g);
+#pragma unroll
+                for (int ww = 0; ww < NT / 32; ++ww) {
+                    const unsigned long long o = gs.red1[ww];
+                    key = o > key ? o : key;
+                }
+            } else {
+                group_sync<NT>(g);
+            }
+            const double lpA = gs.spec[par][0];
+            const double lpB = gs.spec[par][1];
+            int r_ex = -1;
+            double M = fmax(lpA, lpB);
+            if (key != KEY_NONE) {
+                const long long sk = static_cast<long long>(key ^ 0x8000000000000000ull);
+                r_ex = int(0xFFF - (sk & 0xFFF));
+                M = fmax(M, ord_val(sk & ~0xFFFLL));
+            }
+            // ---- phase 2: exp + sum, growth (A4, A5) --------------------
+            double sum = 0.0;
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                const int p = i + NT * j;
+                if (FULL || p < R) {
+                    int r = tmod - p;
+                    if (FULL) {
+                        r &= (R - 1);
+                    } else {
+                        r += (r < 0) ? R : 0;
+                    }
+                    const double dm = v[j] - M;
+                    const double e = exp(dm);
+                    sum += e;
+                    v[j] = dm + log1mH;
+                    if (r == 0) gs.spec[par][2] = e;
+                    if (r == R - 2) gs.spec[par][3] = e;
+                    if (r == R - 1) gs.spec[par][4] = e;
+                    if (r == r_ex) gs.spec[par][5] = e;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            if constexpr (NT > 32) {
+                if (lane == 0) gs.red2[w] = sum;
+                group_sync<NT>(g);
+                sum = gs.red2[0];
+#pragma unroll
+                for (int ww = 1; ww < NT / 32; ++ww) sum += gs.red2[ww];
+            } else {
+                group_sync<NT>(g);
+            }
+            // ---- cell fix-ups and the scalar tail (A5-A8) -----------------
+            const int pB = (tmod + 1 == R) ? 0 : tmod + 1;  // recycled: r = R-1 -> new r = 0
+            const int pA = (pB + 1 == R) ? 0 : pB + 1;      // r = R-2 -> bucket r = R-1 (MERGE)
+            const bool ownB = (pB % NT) == i;
+            const bool ownA = merge && ((pA % NT) == i);
+            if (ownB || ownA) {
+                const double eA = gs.spec[par][3], eB = gs.spec[par][4];
+                // one shared log for both fix-ups: log(sum) for the new CP cell, log(eA+eB) for the bucket
+                const double lg = log(ownB ? sum : (eA + eB));
+                if (ownA && !ownB) {
+                    const int jA = pA / NT;
+#pragma unroll
+                    for (int j = 0; j < J; ++j)
+                        if (j == jA) v[j] = log1mH + lg;
+                }
+                if (ownB) {
+                    const int jB = pB / NT;
+                    const double vcp = logH + lg;
+#pragma unroll
+                    for (int j = 0; j < J; ++j)
+                        if (j == jB) {
+                            v[j] = vcp;
+                            mu[j] = mu0;
+                            be[j] = beta0;
+                            L[j] = L0;
+                        }
+                    if (merge && ownA) {  // R-1 and R-2 owned by the same thread (tiny R)
+                        const double lb = log(eA + eB);
+                        const int jA = pA / NT;
+#pragma unroll
+                        for (int j = 0; j < J; ++j)
+                            if (j == jA) v[j] = log1mH + lb;
+                    }
+                    // tail: normaliser, log Z, p_new, r*, flags, events
+                    const double e0 = gs.spec[par][2];
+                    double Nt, pnew;
+                    if (merge) {
+                        Nt = lg;
+                        pnew = (R == 2 ? eA + eB : e0) / sum;
+                    } else {
+                        Nt = log(sum - P.omH * eB);
+                        pnew = e0 / (sum - eB);
+                    }
+                    const double logz = M + Nt - gs.n_prev;
+                    int rstar;
+                    if (merge) {
+                        const double eex = gs.spec[par][5];
+                        rstar = (r_ex < 0 || (eA + eB) > eex) ? R - 1 : r_ex + 1;
+                    } else {
+                        rstar = r_ex + 1;
+                    }
+                    uint32_t fl = 0;
+                    if (t > 0) {
+                        if (pnew > P.theta) fl |= 1u;
+                        const int cap = min(gs.map_prev + 1, R - 1);
+                        if (rstar < cap) fl |= 2u;
+                    }
+                    if (fl & P.ev_mask) {
+                        const int idx = gs.ev_count++;
+                        if (idx < P.ev_cap) {
+                            EventRec ev;
+                            ev.t = t;
+                            ev.cp_index = t - rstar + 1;
+                            ev.flags = fl;
+                            ev.pad = 0;
+                            ev.p_new = pnew;
+                            P.ev[s * P.ev_cap + idx] = ev;
+                        }
+                    }
+                    gs.map_prev = rstar;
+                    gs.n_prev = Nt;
+                    if (P.out_map) P.out_map[s * P.ld_o + tl] = rstar;
+                    if (P.out_pnew) P.out_pnew[s * P.ld_o + tl] = pnew;
+                    if (P.out_logz) P.out_logz[s * P.ld_o + tl] = logz;
+                    if (!isfinite(x)) nonfinite = true;
+                }
+            }
+            tmod = (tmod + 1 == R) ? 0 : tmod + 1;
+        }
+    }
+    // ---- spill -------------------------------------------------------------
+    if (nonfinite) gs.flags |= 1;  // benign race: every writer stores the same bit set
+    group_sync<NT>(g);
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+        const int p = i + NT * j;
+        if (FULL || p < R) {
+            P.st_mu[sbase + p] = mu[j];
+            P.st_beta[sbase + p] = be[j];
+            P.st_v[sbase + p] = v[j];
+        }
+    }
+    if (i == 0) {
+        SeriesScalars sc;
+        sc.mu0 = gs.mu0;
+        sc.beta0 = gs.beta0;
+        sc.n_prev = gs.n_prev;
+        sc.map_prev = gs.map_prev;
+        sc.ev_count = gs.ev_count;
+        sc.flags = gs.flags;
+        sc.pad = 0;
+        sc.pad2 = 0.0;
+        P.scal[s] = sc;
+        if (gs.flags) atomicOr(P.err, unsigned(gs.flags));
+    }
+}
+
+}  // namespace fbocd

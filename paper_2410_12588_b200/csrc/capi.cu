@@ -1,0 +1,671 @@
+// capi.cu — host runtime and C ABI of libfalcon_bocd.so (include/falcon_bocd.h).
+//
+// Owns: the per-R predictive constant table (long double on the host, rounded
+// once), the per-series state (mu, beta, unnormalised log posterior v in ring
+// position order, plus SeriesScalars), the per-series event buffers, the
+// host-staging buffers of update_chunk_host, and the drain / posterior-gather
+// kernels.  Every computing entry point launches CUDA kernels; there is no CPU
+// fallback.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/falcon_bocd.h"
+#include "bocd_kernel.cuh"
+#include "bocd_variants.h"
+
+using fbocd::EventRec;
+using fbocd::KParams;
+using fbocd::SeriesScalars;
+
+struct falcon_bocd_s {
+    falcon_bocd_config cfg{};
+    fbocd::Variant var{};
+    size_t smem = 0;
+    int64_t t = 0;  // observations absorbed
+    double2* d_ca = nullptr;
+    double2* d_gk = nullptr;
+    double* d_mu = nullptr;
+    double* d_beta = nullptr;
+    double* d_v = nullptr;
+    SeriesScalars* d_scal = nullptr;
+    EventRec* d_ev = nullptr;
+    unsigned* d_err = nullptr;
+    // drain scratch
+    int64_t* d_off = nullptr;  // [S+1]
+    int64_t* d_meta = nullptr; // [2]: total kept, overflow flag
+    falcon_bocd_event* d_evout = nullptr;
+    int64_t evout_cap = 0;
+    // host staging (update_chunk_host)
+    double* d_stage[2] = {nullptr, nullptr};
+    size_t stage_cap = 0;  // doubles per buffer
+    int stage_idx = 0;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_copied[2] = {nullptr, nullptr};
+    cudaEvent_t ev_free[2] = {nullptr, nullptr};
+    int32_t* d_omap = nullptr;
+    double* d_opnew = nullptr;
+    double* d_ologz = nullptr;
+    size_t out_cap = 0;
+    bool poisoned = false;
+    std::string err;
+};
+
+namespace {
+
+thread_local std::string g_create_err;
+
+int fail(falcon_bocd_t h, int code, const std::string& msg) {
+    if (h)
+        h->err = msg;
+    else
+        g_create_err = msg;
+    return code;
+}
+
+int cuda_fail(falcon_bocd_t h, cudaError_t e, const char* what) {
+    std::string m = std::string(what) + ": " + cudaGetErrorString(e);
+    if (h) h->poisoned = true;
+    return fail(h, e == cudaErrorMemoryAllocation ? FALCON_ENOMEM : FALCON_ECUDA, m);
+}
+
+#define CUDA_TRY(h, expr)                                   \
+    do {                                                    \
+        cudaError_t e_ = (expr);                            \
+        if (e_ != cudaSuccess) return cuda_fail(h, e_, #expr); \
+    } while (0)
+
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// ---------------------------------------------------------------------------
+// helper kernels
+// ---------------------------------------------------------------------------
+__global__ void init_scalars_kernel(SeriesScalars* scal, const double* mu0, const double* beta0, int64_t S) {
+    for (int64_t s = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; s < S; s += int64_t(gridDim.x) * blockDim.x) {
+        SeriesScalars sc;
+        sc.mu0 = mu0[s];
+        sc.beta0 = beta0[s];
+        sc.n_prev = 0.0;
+        sc.map_prev = 0;
+        sc.ev_count = 0;
+        sc.flags = 0;
+        sc.pad = 0;
+        sc.pad2 = 0.0;
+        scal[s] = sc;
+    }
+}
+
+__global__ void init_state_kernel(double* mu, double* beta, double* v, const SeriesScalars* scal, int64_t S,
+                                  int R) {
+    const int64_t n = S * int64_t(R);
+    for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t s = k / R;
+        const int p = int(k - s * R);
+        mu[k] = scal[s].mu0;
+        beta[k] = scal[s].beta0;
+        v[k] = (p == 0) ? 0.0 : -INFINITY;
+    }
+}
+
+// Exclusive scan of min(count, cap) over series (single CTA), total + overflow flag in meta.
+__global__ void drain_scan_kernel(const SeriesScalars* scal, int64_t S, int cap, int64_t* off, int64_t* meta) {
+    __shared__ int64_t part[1024];
+    __shared__ int ovf;
+    if (threadIdx.x == 0) ovf = 0;
+    const int64_t per = (S + blockDim.x - 1) / blockDim.x;
+    const int64_t a = threadIdx.x * per, b = min(S, a + per);
+    int64_t loc = 0;
+    int o = 0;
+    for (int64_t s = a; s < b; ++s) {
+        const int c = scal[s].ev_count;
+        loc += c < cap ? c : cap;
+        o |= c > cap;
+    }
+    part[threadIdx.x] = loc;
+    __syncthreads();
+    if (o) atomicOr(&ovf, 1);
+    for (int d = 1; d < blockDim.x; d <<= 1) {
+        int64_t v = threadIdx.x >= d ? part[threadIdx.x - d] : 0;
+        __syncthreads();
+        part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    int64_t run = part[threadIdx.x] - loc;
+    for (int64_t s = a; s < b; ++s) {
+        off[s] = run;
+        const int c = scal[s].ev_count;
+        run += c < cap ? c : cap;
+    }
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) {
+        off[S] = part[threadIdx.x];
+        meta[0] = part[threadIdx.x];
+        meta[1] = ovf;
+    }
+}
+
+// One warp per series: copy its kept events (time order) to out[off[s] ..] and reset the count.
+__global__ void drain_gather_kernel(SeriesScalars* scal, const EventRec* ev, int64_t S, int cap, const int64_t* off,
+                                    falcon_bocd_event* out, int reset, int64_t series_base) {
+    const int64_t s = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (s >= S) return;
+    const int c = scal[s].ev_count;
+    const int n = c < cap ? c : cap;
+    const int64_t o = off[s];
+    for (int k = lane; k < n; k += 32) {
+        const EventRec r = ev[s * int64_t(cap) + k];
+        falcon_bocd_event e;
+        e.series = series_base + s;
+        e.t = r.t;
+        e.cp_index = r.cp_index;
+        e.flags = r.flags;
+        e.reserved = 0;
+        e.p_new = r.p_new;
+        out[o + k] = e;
+    }
+    __syncwarp();
+    if (reset && lane == 0) scal[s].ev_count = 0;
+}
+
+// Ring position order -> run-length order; log R = v - N_t.
+__global__ void posterior_kernel(const double* mu, const double* beta, const double* v,
+                                 const SeriesScalars* scal, int64_t s0, int64_t count, int R, int64_t t,
+                                 double* logR_out, double* mu_out, double* beta_out) {
+    const int64_t n = count * int64_t(R);
+    const int tm = int(t % R);
+    for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = k / R;
+        const int r = int(k - i * R);
+        int p = tm - r;
+        if (p < 0) p += R;
+        const int64_t src = (s0 + i) * int64_t(R) + p;
+        if (logR_out) logR_out[k] = v[src] - scal[s0 + i].n_prev;
+        if (mu_out) mu_out[k] = mu[src];
+        if (beta_out) beta_out[k] = beta[src];
+    }
+}
+
+int grid_for(int64_t n, int block) {
+    int64_t g = (n + block - 1) / block;
+    if (g > 148 * 32) g = 148 * 32;
+    if (g < 1) g = 1;
+    return int(g);
+}
+
+int check_sticky(falcon_bocd_t h, cudaStream_t st) {
+    unsigned e = 0;
+    CUDA_TRY(h, cudaMemcpyAsync(&e, h->d_err, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(h, cudaStreamSynchronize(st));
+    if (e & 1u) {
+        h->poisoned = true;
+        return fail(h, FALCON_ENONFINITE, "non-finite observation seen (NaN/Inf in x)");
+    }
+    if (e & 2u) {
+        h->poisoned = true;
+        return fail(h, FALCON_ENONFINITE, "non-finite or non-positive prior (beta0 <= 0, or first observation 0)");
+    }
+    return FALCON_OK;
+}
+
+int set_device(falcon_bocd_t h) {
+    CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+    return FALCON_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int falcon_bocd_abi_version(void) { return FALCON_BOCD_ABI_VERSION; }
+
+int falcon_bocd_config_init(falcon_bocd_config* cfg) {
+    if (!cfg) return FALCON_EINVAL;
+    std::memset(cfg, 0, sizeof(*cfg));
+    cfg->n_series = 1;
+    cfg->R = 1024;
+    cfg->hazard = 1.0 / 250.0;
+    cfg->kappa0 = 1.0;
+    cfg->alpha0 = 1.0;
+    cfg->mu0_scalar = 0.0;
+    cfg->beta0_scalar = 1.0;
+    cfg->prior_first_obs = 0;
+    cfg->prior_cov = 0.05;
+    cfg->threshold = 0.9;
+    cfg->trunc_mode = FALCON_TRUNC_MERGE;
+    cfg->event_mask = FALCON_EV_PROB;
+    cfg->event_capacity = 64;
+    cfg->device = 0;
+    cfg->series_base = 0;
+    return FALCON_OK;
+}
+
+int falcon_bocd_predictive_constants(int32_t R, double kappa0, double alpha0, double* c, double* a, double* g,
+                                     double* k1) {
+    if (R < 1 || !(kappa0 > 0.0) || !(alpha0 > 0.0) || !std::isfinite(kappa0) || !std::isfinite(alpha0))
+        return FALCON_EINVAL;
+    // D_r = lgamma(alpha_r + 1/2) - lgamma(alpha_r) by the half-step recurrence
+    // D(alpha + 1/2) = log(alpha) - D(alpha) (from Gamma(alpha + 1) = alpha Gamma(alpha)),
+    // started from lgammal at alpha0: no cancellation between large lgamma values.
+    long double D = lgammal((long double)alpha0 + 0.5L) - lgammal((long double)alpha0);
+    const long double two_pi = 6.283185307179586476925286766559005768L;
+    for (int r = 0; r < R; ++r) {
+        const long double kap = (long double)kappa0 + r;
+        const long double alp = (long double)alpha0 + 0.5L * r;
+        const long double kp1 = kap + 1.0L;
+        if (c) c[r] = (double)(D - 0.5L * logl(two_pi * kp1 / kap));
+        if (a) a[r] = (double)alp;
+        if (g) g[r] = (double)(kap / (2.0L * kp1));
+        if (k1) k1[r] = (double)(1.0L / kp1);
+        D = logl(alp) - D;
+    }
+    return FALCON_OK;
+}
+
+int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
+    g_create_err.clear();
+    if (!cfg || !out) return fail(nullptr, FALCON_EINVAL, "null argument");
+    *out = nullptr;
+    const falcon_bocd_config& c = *cfg;
+    if (c.n_series < 1) return fail(nullptr, FALCON_EINVAL, "n_series must be >= 1");
+    if (c.R < 2 || c.R > 4096) return fail(nullptr, FALCON_EINVAL, "R must be in [2, 4096]");
+    if (!(c.hazard > 0.0 && c.hazard < 1.0)) return fail(nullptr, FALCON_EINVAL, "hazard must be in (0, 1)");
+    if (!(c.kappa0 > 0.0) || !(c.alpha0 > 0.0) || !std::isfinite(c.kappa0) || !std::isfinite(c.alpha0))
+        return fail(nullptr, FALCON_EINVAL, "kappa0 and alpha0 must be finite and > 0");
+    if (c.trunc_mode != FALCON_TRUNC_MERGE && c.trunc_mode != FALCON_TRUNC_DROP)
+        return fail(nullptr, FALCON_EINVAL, "trunc_mode must be MERGE or DROP");
+    if (c.event_capacity < 1) return fail(nullptr, FALCON_EINVAL, "event_capacity must be >= 1");
+    if (c.series_base < 0) return fail(nullptr, FALCON_EINVAL, "series_base must be >= 0");
+    if (!std::isfinite(c.threshold)) return fail(nullptr, FALCON_EINVAL, "threshold must be finite");
+    if (c.prior_first_obs && !(c.prior_cov > 0.0 && std::isfinite(c.prior_cov)))
+        return fail(nullptr, FALCON_EINVAL, "prior_cov must be finite and > 0");
+    if (!c.prior_first_obs && !c.beta0 && !(c.beta0_scalar > 0.0 && std::isfinite(c.beta0_scalar)))
+        return fail(nullptr, FALCON_EINVAL, "beta0 must be finite and > 0");
+    if (!c.prior_first_obs && !c.mu0 && !std::isfinite(c.mu0_scalar))
+        return fail(nullptr, FALCON_EINVAL, "mu0 must be finite");
+    const int64_t S = c.n_series;
+    std::vector<double> mu0(S), beta0(S);
+    for (int64_t s = 0; s < S; ++s) {
+        mu0[s] = c.mu0 ? c.mu0[s] : c.mu0_scalar;
+        beta0[s] = c.beta0 ? c.beta0[s] : c.beta0_scalar;
+        if (!c.prior_first_obs && (!std::isfinite(mu0[s]) || !(beta0[s] > 0.0) || !std::isfinite(beta0[s])))
+            return fail(nullptr, FALCON_EINVAL, "per-series mu0 must be finite and beta0 > 0");
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(nullptr, FALCON_ECUDA, "no CUDA device available (this library has no CPU fallback)");
+    }
+    if (c.device < 0 || c.device >= ndev) return fail(nullptr, FALCON_EINVAL, "device ordinal out of range");
+
+    falcon_bocd_t h = new falcon_bocd_s();
+    h->cfg = c;
+    h->cfg.mu0 = nullptr;
+    h->cfg.beta0 = nullptr;
+    if (fbocd::select_variant(c.R, &h->var) != 0) {
+        delete h;
+        return fail(nullptr, FALCON_EINVAL, "no kernel variant for this R");
+    }
+    h->smem = size_t(c.R) * 2 * sizeof(double2) + size_t(h->var.spb) * h->var.group_smem;
+    auto bail = [&](int code) {
+        g_create_err = h->err;
+        falcon_bocd_destroy(h);
+        return code;
+    };
+    int rc;
+    if ((rc = set_device(h)) != 0) return bail(rc);
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, c.device) != cudaSuccess || prop.major < 10) {
+        cudaGetLastError();
+        h->err = "device is not sm_100 class (this library is built for sm_100a only)";
+        return bail(FALCON_ECUDA);
+    }
+    if (h->smem > 227 * 1024) {
+        h->err = "shared memory footprint too large";
+        return bail(FALCON_EINVAL);
+    }
+    cudaError_t e = cudaFuncSetAttribute(h->var.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(h->smem));
+    if (e != cudaSuccess) return bail(cuda_fail(h, e, "cudaFuncSetAttribute"));
+
+    const int R = c.R;
+    std::vector<double> tc(R), ta(R), tg(R), tk(R);
+    falcon_bocd_predictive_constants(R, c.kappa0, c.alpha0, tc.data(), ta.data(), tg.data(), tk.data());
+    std::vector<double2> ca(R), gk(R);
+    for (int r = 0; r < R; ++r) {
+        ca[r] = make_double2(tc[r], ta[r]);
+        gk[r] = make_double2(tg[r], tk[r]);
+    }
+    const size_t SR = size_t(S) * size_t(R);
+    double *dmu0 = nullptr, *dbeta0 = nullptr;
+#define ALLOC(ptr, bytes)                                                   \
+    do {                                                                    \
+        cudaError_t e2 = cudaMalloc((void**)&(ptr), (bytes));               \
+        if (e2 != cudaSuccess) {                                            \
+            cudaFree(dmu0);                                                 \
+            cudaFree(dbeta0);                                               \
+            return bail(cuda_fail(h, e2, "cudaMalloc " #ptr));              \
+        }                                                                   \
+    } while (0)
+    ALLOC(h->d_ca, R * sizeof(double2));
+    ALLOC(h->d_gk, R * sizeof(double2));
+    ALLOC(h->d_mu, SR * sizeof(double));
+    ALLOC(h->d_beta, SR * sizeof(double));
+    ALLOC(h->d_v, SR * sizeof(double));
+    ALLOC(h->d_scal, S * sizeof(SeriesScalars));
+    ALLOC(h->d_ev, size_t(S) * c.event_capacity * sizeof(EventRec));
+    ALLOC(h->d_err, sizeof(unsigned));
+    ALLOC(h->d_off, (S + 1) * sizeof(int64_t));
+    ALLOC(h->d_meta, 2 * sizeof(int64_t));
+    ALLOC(dmu0, S * sizeof(double));
+    ALLOC(dbeta0, S * sizeof(double));
+#undef ALLOC
+    cudaError_t e3 = cudaSuccess;
+    if (e3 == cudaSuccess) e3 = cudaMemcpy(h->d_ca, ca.data(), R * sizeof(double2), cudaMemcpyHostToDevice);
+    if (e3 == cudaSuccess) e3 = cudaMemcpy(h->d_gk, gk.data(), R * sizeof(double2), cudaMemcpyHostToDevice);
+    if (e3 == cudaSuccess) e3 = cudaMemcpy(dmu0, mu0.data(), S * sizeof(double), cudaMemcpyHostToDevice);
+    if (e3 == cudaSuccess) e3 = cudaMemcpy(dbeta0, beta0.data(), S * sizeof(double), cudaMemcpyHostToDevice);
+    if (e3 == cudaSuccess) e3 = cudaMemset(h->d_err, 0, sizeof(unsigned));
+    if (e3 == cudaSuccess) {
+        init_scalars_kernel<<<grid_for(S, 256), 256>>>(h->d_scal, dmu0, dbeta0, S);
+        init_state_kernel<<<grid_for(int64_t(SR), 256), 256>>>(h->d_mu, h->d_beta, h->d_v, h->d_scal, S, R);
+        e3 = cudaGetLastError();
+    }
+    if (e3 == cudaSuccess) e3 = cudaDeviceSynchronize();
+    cudaFree(dmu0);
+    cudaFree(dbeta0);
+    if (e3 != cudaSuccess) return bail(cuda_fail(h, e3, "create: init"));
+    *out = h;
+    return FALCON_OK;
+}
+
+static int launch_update(falcon_bocd_t h, const double* x_dev, int64_t ld, int64_t T,
+                         int32_t* omap, double* opnew, double* ologz, int64_t ld_o, cudaStream_t st) {
+    const falcon_bocd_config& c = h->cfg;
+    int64_t done = 0;
+    while (done < T) {
+        const int64_t n = (T - done) > (1 << 30) ? (1 << 30) : (T - done);
+        KParams P;
+        std::memset(&P, 0, sizeof(P));
+        P.R = c.R;
+        P.S = c.n_series;
+        P.logH = std::log(c.hazard);
+        P.log1mH = std::log1p(-c.hazard);
+        P.omH = 1.0 - c.hazard;
+        P.theta = c.threshold;
+        P.alpha0 = c.alpha0;
+        P.prior_cov = c.prior_cov;
+        P.mode = c.trunc_mode;
+        P.prior_first_obs = c.prior_first_obs;
+        P.ev_mask = c.event_mask;
+        P.ev_cap = c.event_capacity;
+        P.tab_ca = h->d_ca;
+        P.tab_gk = h->d_gk;
+        P.st_mu = h->d_mu;
+        P.st_beta = h->d_beta;
+        P.st_v = h->d_v;
+        P.scal = h->d_scal;
+        P.ev = h->d_ev;
+        P.err = h->d_err;
+        P.x = x_dev + done;
+        P.ld = ld;
+        P.T = int(n);
+        P.t0 = h->t;
+        P.out_map = omap ? omap + done : nullptr;
+        P.out_pnew = opnew ? opnew + done : nullptr;
+        P.out_logz = ologz ? ologz + done : nullptr;
+        P.ld_o = ld_o;
+        P.tma_ok = ((reinterpret_cast<uintptr_t>(P.x) & 15u) == 0) && ((ld & 1) == 0);
+        const int64_t grid = (c.n_series + h->var.spb - 1) / h->var.spb;
+        void* args[] = {&P};
+        cudaError_t e = cudaLaunchKernel(h->var.fn, dim3(unsigned(grid)), dim3(unsigned(h->var.nt * h->var.spb)),
+                                         args, h->smem, st);
+        if (e != cudaSuccess) return cuda_fail(h, e, "bocd_update_kernel launch");
+        h->t += n;
+        done += n;
+    }
+    return FALCON_OK;
+}
+
+int falcon_bocd_update_chunk(falcon_bocd_t h, const double* x_dev, int64_t ld, int64_t T,
+                             const falcon_bocd_step_out* outs, void* stream) {
+    if (!h) return FALCON_EINVAL;
+    if (h->poisoned) return fail(h, FALCON_ESTATE, "handle poisoned by an earlier error");
+    if (T < 0 || ld < T || (T > 0 && !x_dev)) return fail(h, FALCON_EINVAL, "bad x / ld / T");
+    if (outs && outs->ld < T && (outs->map_rl || outs->p_new || outs->log_z))
+        return fail(h, FALCON_EINVAL, "outs->ld < T");
+    if (T == 0) return FALCON_OK;
+    int rc;
+    if ((rc = set_device(h)) != 0) return rc;
+    return launch_update(h, x_dev, ld, T, outs ? outs->map_rl : nullptr, outs ? outs->p_new : nullptr,
+                         outs ? outs->log_z : nullptr, outs ? outs->ld : 0, (cudaStream_t)stream);
+}
+
+int falcon_bocd_update_chunk_host(falcon_bocd_t h, const double* x_host, int64_t ld, int64_t T,
+                                  const falcon_bocd_step_out* outs, void* stream) {
+    if (!h) return FALCON_EINVAL;
+    if (h->poisoned) return fail(h, FALCON_ESTATE, "handle poisoned by an earlier error");
+    if (T < 0 || ld < T || (T > 0 && !x_host)) return fail(h, FALCON_EINVAL, "bad x / ld / T");
+    const bool want_out = outs && (outs->map_rl || outs->p_new || outs->log_z);
+    if (want_out && outs->ld < T) return fail(h, FALCON_EINVAL, "outs->ld < T");
+    if (T == 0) return FALCON_OK;
+    int rc;
+    if ((rc = set_device(h)) != 0) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t S = h->cfg.n_series;
+    const size_t need = size_t(S) * size_t(T);
+    if (!h->copy_stream) {
+        CUDA_TRY(h, cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+        for (int b = 0; b < 2; ++b) {
+            CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_copied[b], cudaEventDisableTiming));
+            CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_free[b], cudaEventDisableTiming));
+        }
+    }
+    if (need > h->stage_cap) {
+        CUDA_TRY(h, cudaDeviceSynchronize());
+        for (int b = 0; b < 2; ++b) {
+            cudaFree(h->d_stage[b]);
+            h->d_stage[b] = nullptr;
+        }
+        h->stage_cap = 0;
+        for (int b = 0; b < 2; ++b) CUDA_TRY(h, cudaMalloc((void**)&h->d_stage[b], need * sizeof(double)));
+        h->stage_cap = need;
+    }
+    const int b = h->stage_idx;
+    h->stage_idx ^= 1;
+    // copy x (pitched host rows -> dense device rows) on the copy stream once the buffer is free
+    CUDA_TRY(h, cudaStreamWaitEvent(h->copy_stream, h->ev_free[b], 0));
+    CUDA_TRY(h, cudaMemcpy2DAsync(h->d_stage[b], size_t(T) * sizeof(double), x_host, size_t(ld) * sizeof(double),
+                                  size_t(T) * sizeof(double), size_t(S), cudaMemcpyHostToDevice, h->copy_stream));
+    CUDA_TRY(h, cudaEventRecord(h->ev_copied[b], h->copy_stream));
+    CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_copied[b], 0));
+    int32_t* omap = nullptr;
+    double *opnew = nullptr, *ologz = nullptr;
+    if (want_out) {
+        if (need > h->out_cap) {
+            CUDA_TRY(h, cudaStreamSynchronize(st));
+            cudaFree(h->d_omap);
+            cudaFree(h->d_opnew);
+            cudaFree(h->d_ologz);
+            h->d_omap = nullptr;
+            h->d_opnew = h->d_ologz = nullptr;
+            h->out_cap = 0;
+            CUDA_TRY(h, cudaMalloc((void**)&h->d_omap, need * sizeof(int32_t)));
+            CUDA_TRY(h, cudaMalloc((void**)&h->d_opnew, need * sizeof(double)));
+            CUDA_TRY(h, cudaMalloc((void**)&h->d_ologz, need * sizeof(double)));
+            h->out_cap = need;
+        }
+        omap = outs->map_rl ? h->d_omap : nullptr;
+        opnew = outs->p_new ? h->d_opnew : nullptr;
+        ologz = outs->log_z ? h->d_ologz : nullptr;
+    }
+    if ((rc = launch_update(h, h->d_stage[b], T, T, omap, opnew, ologz, T, st)) != 0) return rc;
+    CUDA_TRY(h, cudaEventRecord(h->ev_free[b], st));
+    if (want_out) {
+        const size_t hp = size_t(outs->ld);
+        if (omap)
+            CUDA_TRY(h, cudaMemcpy2DAsync(outs->map_rl, hp * 4, omap, size_t(T) * 4, size_t(T) * 4, size_t(S),
+                                          cudaMemcpyDeviceToHost, st));
+        if (opnew)
+            CUDA_TRY(h, cudaMemcpy2DAsync(outs->p_new, hp * 8, opnew, size_t(T) * 8, size_t(T) * 8, size_t(S),
+                                          cudaMemcpyDeviceToHost, st));
+        if (ologz)
+            CUDA_TRY(h, cudaMemcpy2DAsync(outs->log_z, hp * 8, ologz, size_t(T) * 8, size_t(T) * 8, size_t(S),
+                                          cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(h, cudaStreamSynchronize(st));
+    }
+    // the caller may reuse x_host once the copy has landed
+    CUDA_TRY(h, cudaEventSynchronize(h->ev_copied[b]));
+    return FALCON_OK;
+}
+
+int falcon_bocd_pending_events(falcon_bocd_t h, int64_t* n_out, void* stream) {
+    if (!h || !n_out) return FALCON_EINVAL;
+    int rc;
+    if ((rc = set_device(h)) != 0) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t S = h->cfg.n_series;
+    drain_scan_kernel<<<1, 1024, 0, st>>>(h->d_scal, S, h->cfg.event_capacity, h->d_off, h->d_meta);
+    CUDA_TRY(h, cudaGetLastError());
+    int64_t meta[2];
+    CUDA_TRY(h, cudaMemcpyAsync(meta, h->d_meta, sizeof(meta), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(h, cudaStreamSynchronize(st));
+    *n_out = meta[0];
+    return FALCON_OK;
+}
+
+int falcon_bocd_changepoints(falcon_bocd_t h, falcon_bocd_event* out, int64_t capacity, int64_t* n_out,
+                             void* stream) {
+    if (!h || !n_out || capacity < 0 || (capacity > 0 && !out)) return FALCON_EINVAL;
+    *n_out = 0;
+    int rc;
+    if ((rc = set_device(h)) != 0) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    if ((rc = check_sticky(h, st)) != 0) return rc;
+    const int64_t S = h->cfg.n_series;
+    const int cap = h->cfg.event_capacity;
+    drain_scan_kernel<<<1, 1024, 0, st>>>(h->d_scal, S, cap, h->d_off, h->d_meta);
+    CUDA_TRY(h, cudaGetLastError());
+    int64_t meta[2];
+    CUDA_TRY(h, cudaMemcpyAsync(meta, h->d_meta, sizeof(meta), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(h, cudaStreamSynchronize(st));
+    const int64_t total = meta[0];
+    if (total > capacity) {
+        *n_out = total;
+        return fail(h, FALCON_EINVAL, "output capacity smaller than the number of buffered events");
+    }
+    const bool dev_out = total > 0 && is_device_ptr(out);
+    falcon_bocd_event* dst = out;
+    if (total > 0 && !dev_out) {
+        if (total > h->evout_cap) {
+            cudaFree(h->d_evout);
+            h->d_evout = nullptr;
+            h->evout_cap = 0;
+            CUDA_TRY(h, cudaMalloc((void**)&h->d_evout, size_t(total) * sizeof(falcon_bocd_event)));
+            h->evout_cap = total;
+        }
+        dst = h->d_evout;
+    }
+    const int64_t threads = S * 32;
+    drain_gather_kernel<<<unsigned((threads + 255) / 256), 256, 0, st>>>(h->d_scal, h->d_ev, S, cap, h->d_off,
+                                                                         dst, 1, h->cfg.series_base);
+    CUDA_TRY(h, cudaGetLastError());
+    if (total > 0 && !dev_out)
+        CUDA_TRY(h, cudaMemcpyAsync(out, dst, size_t(total) * sizeof(falcon_bocd_event), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(h, cudaStreamSynchronize(st));
+    *n_out = total;
+    if (meta[1]) {
+        h->err = "event buffer overflow: some events were dropped";
+        return FALCON_WARN_EVENTS_DROPPED;
+    }
+    return FALCON_OK;
+}
+
+int falcon_bocd_read_posterior(falcon_bocd_t h, int64_t s0, int64_t count, double* logR_out, double* mu_out,
+                               double* beta_out, void* stream) {
+    if (!h || s0 < 0 || count < 0 || s0 + count > h->cfg.n_series) return FALCON_EINVAL;
+    if (count == 0 || (!logR_out && !mu_out && !beta_out)) return FALCON_OK;
+    int rc;
+    if ((rc = set_device(h)) != 0) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    if ((rc = check_sticky(h, st)) != 0) return rc;
+    const int R = h->cfg.R;
+    const size_t n = size_t(count) * R;
+    double* outs[3] = {logR_out, mu_out, beta_out};
+    double* dst[3] = {nullptr, nullptr, nullptr};
+    double* tmp = nullptr;
+    bool any_host = false;
+    for (int k = 0; k < 3; ++k)
+        if (outs[k] && !is_device_ptr(outs[k])) any_host = true;
+    if (any_host) CUDA_TRY(h, cudaMalloc((void**)&tmp, 3 * n * sizeof(double)));
+    for (int k = 0; k < 3; ++k) {
+        if (!outs[k]) continue;
+        dst[k] = is_device_ptr(outs[k]) ? outs[k] : tmp + k * n;
+    }
+    posterior_kernel<<<grid_for(int64_t(n), 256), 256, 0, st>>>(h->d_mu, h->d_beta, h->d_v, h->d_scal, s0, count, R,
+                                                                h->t, dst[0], dst[1], dst[2]);
+    cudaError_t e = cudaGetLastError();
+    for (int k = 0; k < 3 && e == cudaSuccess; ++k)
+        if (outs[k] && dst[k] != outs[k])
+            e = cudaMemcpyAsync(outs[k], dst[k], n * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (tmp) cudaFree(tmp);
+    if (e != cudaSuccess) return cuda_fail(h, e, "read_posterior");
+    return FALCON_OK;
+}
+
+int falcon_bocd_steps(falcon_bocd_t h, int64_t* t_out) {
+    if (!h || !t_out) return FALCON_EINVAL;
+    *t_out = h->t;
+    return FALCON_OK;
+}
+
+int falcon_bocd_kernel_shape(falcon_bocd_t h, int32_t* nt, int32_t* j, int32_t* spb) {
+    if (!h) return FALCON_EINVAL;
+    if (nt) *nt = h->var.nt;
+    if (j) *j = h->var.j;
+    if (spb) *spb = h->var.spb;
+    return FALCON_OK;
+}
+
+int falcon_bocd_destroy(falcon_bocd_t h) {
+    if (!h) return FALCON_OK;
+    int rc = FALCON_OK;
+    if (cudaSetDevice(h->cfg.device) == cudaSuccess) {
+        if (cudaDeviceSynchronize() != cudaSuccess) rc = FALCON_ECUDA;
+        if (rc == FALCON_OK && h->d_err) {
+            unsigned e = 0;
+            if (cudaMemcpy(&e, h->d_err, sizeof(unsigned), cudaMemcpyDeviceToHost) == cudaSuccess && (e & 3u))
+                rc = FALCON_ENONFINITE;
+        }
+    }
+    cudaGetLastError();
+    void* ptrs[] = {h->d_ca, h->d_gk, h->d_mu, h->d_beta, h->d_v, h->d_scal, h->d_ev, h->d_err, h->d_off,
+                    h->d_meta, h->d_evout, h->d_stage[0], h->d_stage[1], h->d_omap, h->d_opnew, h->d_ologz};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    for (int b = 0; b < 2; ++b) {
+        if (h->ev_copied[b]) cudaEventDestroy(h->ev_copied[b]);
+        if (h->ev_free[b]) cudaEventDestroy(h->ev_free[b]);
+    }
+    if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+    delete h;
+    return rc;
+}
+
+const char* falcon_bocd_last_error(falcon_bocd_t h) { return h ? h->err.c_str() : g_create_err.c_str(); }
+
+}  // extern "C"

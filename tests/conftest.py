@@ -18,3 +18,13 @@ def oracle_mod():
     import oracle
     oracle.build()
     return oracle
+
+
+def pytest_sessionfinish(session, exitstatus):
+    path = os.environ.get("PARITY_STATS")
+    if path:
+        import json
+        from tests import parity
+        if parity.STATS:
+            with open(path, "w") as f:
+                json.dump(parity.STATS, f, indent=1, sort_keys=True)

@@ -1,0 +1,201 @@
+"""T3/T4 — the CUDA path (through the C ABI) vs the fp64 oracle, on the same seeded inputs.
+
+Tolerances: tests/parity.py (log posteriors and log Z within 1e-9 absolute;
+MAP / events exact outside MAP margins < 1e-6 and |p_new - theta| < 1e-6).
+Metamorphic checks (chunk split, series permutation, host vs device input)
+are bit-exact.
+"""
+import numpy as np
+import pytest
+
+from tests import bruteforce, parity
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - collected on CPU boxes too
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2410_12588_b200 import bocd, tracegen  # noqa: E402
+
+
+def _run_gpu(x, R, H, mode, chunks=None, kappa0=1.0, alpha0=1.0, mu0=None, beta0=None,
+             prior_cov=0.05, ev_mask=1, cap=64):
+    S, T = x.shape
+    first = mu0 is None
+    b = bocd.BocdBatch(S, R=R, hazard=H, kappa0=kappa0, alpha0=alpha0,
+                       mu0=0.0 if first else mu0, beta0=1.0 if first else beta0,
+                       prior_first_obs=first, prior_cov=prior_cov, trunc_mode=mode,
+                       event_mask=ev_mask, event_capacity=cap)
+    xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    chunks = chunks or [T]
+    maps, pn, lz = [], [], []
+    t0 = 0
+    for n in chunks:
+        m, p, z = b.update_chunk(xd[:, t0:t0 + n], outputs=True)
+        maps.append(m.cpu().numpy()); pn.append(p.cpu().numpy()); lz.append(z.cpu().numpy())
+        t0 += n
+    assert t0 == T
+    logR, mu, be = (a.cpu().numpy() for a in b.read_posterior())
+    ev, dropped = b.changepoints()
+    b.close()
+    return dict(map=np.concatenate(maps, 1), pnew=np.concatenate(pn, 1), logz=np.concatenate(lz, 1),
+                logR=logR, mu=mu, beta=be, events=ev, dropped=dropped)
+
+
+def _oracle(oracle_mod, x, R, H, mode, mu0=None, beta0=None, prior_cov=0.05, kappa0=1.0,
+            alpha0=1.0, traj=False):
+    first = mu0 is None
+    return oracle_mod.run(x, R, H, kappa0, alpha0, mu0, beta0, trunc_mode=mode,
+                          prior_first_obs=first, prior_cov=prior_cov, traj=traj, n_threads=0)
+
+
+def _full_check(g, res, theta=0.9, mask=1, name=None):
+    st = parity.compare_steps(g["map"], g["pnew"], g["logz"], res, theta)
+    st["max_dlogR"] = parity.compare_logR(g["logR"], res.logR_final)
+    st["events"] = parity.compare_events(g["events"], res, theta, mask)
+    if name:
+        parity.record(name, st)
+    return st
+
+
+@pytest.mark.parametrize("sigma", [0.0, 0.02])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_c1_parity(oracle_mod, sigma, mode):
+    cfg = tracegen.CONFIGS["C1"]
+    x = tracegen.generate(tracegen.make_spec(cfg, sigma=sigma))
+    g = _run_gpu(x, cfg.R, cfg.hazard, mode, ev_mask=3, cap=4096)
+    res = _oracle(oracle_mod, x, cfg.R, cfg.hazard, mode)
+    _full_check(g, res, mask=3, name=f"C1 sigma={sigma} mode={mode}")
+    assert [(int(e["t"]), int(e["cp_index"])) for e in g["events"] if e["flags"] & 1] == [(600, 600)]
+
+
+@pytest.mark.parametrize("R,mode,variant", [(3, "drop", 0), (3, "merge", 0), (4, "merge", 0),
+                                            (5, "drop", 0), (16, "merge", 0), (16, "drop", 1),
+                                            (4, "drop", 1), (2, "merge", 0), (2, "drop", 0)])
+def test_bruteforce_cases_streaming(R, mode, variant):
+    """T = 1 per call (streaming), posterior read after every step, vs enumeration."""
+    from tests.test_oracle_bruteforce import _data
+    x, pr = _data(variant)
+    b = bocd.BocdBatch(1, R=R, hazard=pr["H"], kappa0=pr["k0"], alpha0=pr["a0"], mu0=pr["mu0"],
+                       beta0=pr["b0"], trunc_mode=mode)
+    xd = torch.from_numpy(x[None, :].copy()).cuda()
+    traj = []
+    for t in range(x.shape[0]):
+        b.update_chunk(xd[:, t:t + 1])
+        traj.append(b.read_posterior()[0].cpu().numpy()[0])
+    b.close()
+    ref, _ = bruteforce.posterior(x, R, pr["H"], pr["mu0"], pr["k0"], pr["a0"], pr["b0"], mode)
+    for t in range(x.shape[0]):
+        r = np.asarray(ref[t])
+        fin = np.isfinite(r)
+        assert np.all(np.abs(traj[t][fin] - r[fin]) < 1e-11), (t, traj[t], r)
+        assert np.all(traj[t][~fin] < -1e300)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_c2_subset_parity(oracle_mod, mode):
+    cfg = tracegen.CONFIGS["C2"]
+    spec = tracegen.make_spec(cfg)
+    x = tracegen.generate(spec, 0, 24, 0, 3000)
+    g = _run_gpu(x, cfg.R, cfg.hazard, mode, ev_mask=3, cap=4096)
+    res = _oracle(oracle_mod, x, cfg.R, cfg.hazard, mode)
+    assert not g["dropped"]
+    _full_check(g, res, mask=3, name=f"C2[:24,:3000] mode={mode}")
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_c3_subset_parity(oracle_mod, mode):
+    cfg = tracegen.CONFIGS["C3"]
+    spec = tracegen.make_spec(cfg)
+    x = tracegen.generate(spec, 0, 16, 0, 2500)
+    g = _run_gpu(x, cfg.R, cfg.hazard, mode, prior_cov=cfg.prior_cov, ev_mask=3, cap=4096)
+    res = _oracle(oracle_mod, x, cfg.R, cfg.hazard, mode, prior_cov=cfg.prior_cov)
+    assert not g["dropped"]
+    _full_check(g, res, mask=3, name=f"C3[:16,:2500] mode={mode}")
+
+
+@pytest.mark.parametrize("R", [7, 100, 300, 1000])
+def test_generic_R_parity(oracle_mod, R):
+    cfg = tracegen.CONFIGS["C3"]
+    x = tracegen.generate(tracegen.make_spec(cfg), 3, 6, 0, 1500)
+    for mode in (0, 1):
+        g = _run_gpu(x, R, 1 / 100, mode, prior_cov=0.3, ev_mask=3, cap=2048)
+        res = _oracle(oracle_mod, x, R, 1 / 100, mode, prior_cov=0.3)
+        assert not g["dropped"]
+        _full_check(g, res, mask=3, name=f"C3[3:9,:1500] R={R} mode={mode}")
+
+
+def test_chunk_split_bit_exact():
+    cfg = tracegen.CONFIGS["C3"]
+    x = tracegen.generate(tracegen.make_spec(cfg), 0, 8, 0, 1300)
+    a = _run_gpu(x, 1024, cfg.hazard, 0, prior_cov=0.3, ev_mask=3)
+    b = _run_gpu(x, 1024, cfg.hazard, 0, prior_cov=0.3, ev_mask=3, chunks=[1, 255, 257, 3, 512, 1, 271])
+    for k in ("map", "pnew", "logz", "logR", "mu", "beta"):
+        assert np.array_equal(a[k], b[k], equal_nan=True), k
+    assert np.array_equal(a["events"], b["events"])
+
+
+def test_series_permutation_bit_exact():
+    cfg = tracegen.CONFIGS["C2"]
+    x = tracegen.generate(tracegen.make_spec(cfg), 0, 12, 0, 800)
+    perm = np.random.default_rng(0).permutation(12)
+    a = _run_gpu(x, 512, cfg.hazard, 0)
+    b = _run_gpu(x[perm], 512, cfg.hazard, 0)
+    for k in ("map", "pnew", "logz", "logR"):
+        assert np.array_equal(a[k][perm], b[k]), k
+
+
+def test_host_path_equals_device_path():
+    cfg = tracegen.CONFIGS["C2"]
+    x = tracegen.generate(tracegen.make_spec(cfg), 0, 10, 0, 700)
+    a = _run_gpu(x, 512, cfg.hazard, 0)
+    h = bocd.BocdBatch(10, R=512, hazard=cfg.hazard, prior_first_obs=True, prior_cov=0.05)
+    xp = torch.from_numpy(x).pin_memory()
+    m1, p1, z1 = h.update_chunk_host(xp[:, :300], outputs=True)
+    m2, p2, z2 = h.update_chunk_host(xp[:, 300:], outputs=True)
+    logR = h.read_posterior()[0].cpu().numpy()
+    h.close()
+    assert np.array_equal(np.concatenate([m1, m2], 1), a["map"])
+    assert np.array_equal(np.concatenate([z1, z2], 1), a["logz"])
+    assert np.array_equal(logR, a["logR"])
+
+
+def test_device_tracegen_matches_numpy():
+    cfg = tracegen.CONFIGS["C3"]
+    spec = tracegen.make_spec(cfg, n_series=64, T=3000)
+    ref = tracegen.generate(spec, 5, 40, 100, 2000)
+    dt = bocd.DeviceTrace(spec, "cuda")
+    out = torch.empty((40, 2000), dtype=torch.float64, device="cuda")
+    dt.generate(out, 5, 100)
+    np.testing.assert_allclose(out.cpu().numpy(), ref, rtol=1e-13, atol=0)
+
+
+def test_nonfinite_input_is_reported():
+    x = np.ones((2, 50))
+    x[1, 20] = np.nan
+    b = bocd.BocdBatch(2, R=64, mu0=1.0, beta0=0.01)
+    b.update_chunk(torch.from_numpy(x).cuda())
+    with pytest.raises(bocd.N.FalconError) as ei:
+        b.changepoints()
+    assert ei.value.code == bocd.N.FALCON_ENONFINITE
+    with pytest.raises(bocd.N.FalconError):
+        b.update_chunk(torch.from_numpy(x).cuda())
+    b.close()
+
+
+def test_event_overflow_warning():
+    cfg = tracegen.CONFIGS["C1"]
+    x = np.tile(tracegen.generate(tracegen.make_spec(cfg)), (3, 1))
+    b = bocd.BocdBatch(3, R=256, hazard=cfg.hazard, prior_first_obs=True, event_mask=3,
+                       event_capacity=1)
+    b.update_chunk(torch.from_numpy(x).cuda())
+    ev, dropped = b.changepoints()
+    b.close()
+    assert len(ev) == 3 and not dropped  # one PROB|MAPRESET event per series fits exactly
+    b = bocd.BocdBatch(3, R=256, hazard=cfg.hazard, prior_first_obs=True, event_mask=3,
+                       event_capacity=1, trunc_mode="drop")
+    b.update_chunk(torch.from_numpy(x).cuda())
+    ev, dropped = b.changepoints()
+    b.close()
+    assert len(ev) == 3 and dropped  # DROP misfires MAPRESET (reading Q6): overflow reported
