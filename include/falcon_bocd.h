@@ -174,6 +174,13 @@ int falcon_bocd_abi_version(void);
 int falcon_bocd_predictive_constants(int32_t R, double kappa0, double alpha0, double *c, double *a,
                                      double *g, double *k1);
 
+/* Test hook (no handle): out_dev[k] = f(in_dev[k]) for k < n on the device with the
+ * kernels' own branch-free transcendentals (csrc/fastmath.cuh): which = 0 -> log
+ * (inputs must be positive normal doubles), which = 1 -> exp (inputs <= ~0, -inf
+ * allowed; arguments below -708 are clamped).  Synchronises `stream`. */
+int falcon_bocd_debug_fastmath(int32_t which, const double *in_dev, double *out_dev, int64_t n,
+                               void *stream);
+
 #ifdef __cplusplus
 }
 #endif

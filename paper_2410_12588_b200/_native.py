@@ -85,6 +85,7 @@ def lib():
         "falcon_bocd_predictive_constants": (ctypes.c_int, [_i32, _f64, _f64, _P, _P, _P, _P]),
         "falcon_trace_generate": (ctypes.c_int, [ctypes.POINTER(TraceSpecC), _P, _i64, _i64, _i64,
                                                  _i64, _i64, _P]),
+        "falcon_bocd_debug_fastmath": (ctypes.c_int, [_i32, _P, _P, _i64, _P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -98,7 +99,7 @@ EXPORTED = ["falcon_bocd_abi_version", "falcon_bocd_config_init", "falcon_bocd_c
             "falcon_bocd_update_chunk", "falcon_bocd_update_chunk_host", "falcon_bocd_changepoints",
             "falcon_bocd_pending_events", "falcon_bocd_read_posterior", "falcon_bocd_steps",
             "falcon_bocd_kernel_shape", "falcon_bocd_destroy", "falcon_bocd_last_error",
-            "falcon_bocd_predictive_constants", "falcon_trace_generate"]
+            "falcon_bocd_predictive_constants", "falcon_trace_generate", "falcon_bocd_debug_fastmath"]
 
 
 def check(code, handle=None):

@@ -9,16 +9,22 @@
 // exactly the one that becomes the new change-point cell.  Per-r constants of
 // the Student-t predictive come from a shared-memory table indexed by r.
 //
-// Per step (all fp64, no fast-math):
+// Per step (all fp64, no fast-math; log/exp are the branch-free table-driven
+// versions of fastmath.cuh):
 //   A1  NIG update           mu' = mu + d/(kappa+1),  beta' = beta + kappa d^2 / (2(kappa+1))
 //   A2  Student-t predictive l_r = c_r + alpha_r (log beta - log beta') - 1/2 log beta'
 //       (= c_r - 1/2 log beta - (alpha_r + 1/2) log1p(kappa d^2 / (2 beta (kappa+1))))
-//   A3/A4  lp_r = v_r + l_r;  group max/argmax (one 64-bit key per cell, REDUX) then
-//       sum_r exp(lp_r - M) (xor-butterfly, fixed order => deterministic)
-//   A5  v'_{r+1} = lp_r - M + log(1-H);  v'_0 = log H + log(sum);  the posterior is kept
-//       UNNORMALISED (log R_t = v' - N_t, N_t = log sum_r e^{v'_r}); only the tail needs N_t
-//   A6  MERGE: v'_{R-1} = log(1-H) + log(e_{R-2} + e_{R-1});  DROP: e_{R-1} discarded
-//   A7  r*, p_new = e_0/sum (MERGE) or e_0/(sum - e_{R-1}) (DROP), flags, events
+//   A3/A4  lp_r = v_r + log(1-H) + l_r  (log(1-H) folded into the c_r table);
+//       group max/argmax (one 64-bit key per cell, REDUX), then sum_r exp(lp_r - M)
+//       (xor butterfly + fixed-order cross-warp sum: deterministic)
+//   A5  growth:  v'_{r+1} = lp_r - M;  v'_0 = log H - log(1-H) + log(sum);  the stored
+//       posterior is UNNORMALISED and offset by -log(1-H):
+//       log R_t(r) = v'_r + log(1-H) - N_t,  N_t = log sum_r exp(v'_r + log(1-H))
+//   A6  MERGE: v'_{R-1} = log(e_{R-2} + e_{R-1});  DROP: e_{R-1} is discarded
+//   A7  r*, p_new = e_0 / sum (MERGE) or e_0 / (sum - e_{R-1}) (DROP), flags, events
+// Every lp is also written to a per-series shared-memory row (double-buffered by
+// step parity) so the O(1) special cells (R-2, R-1, 0, argmax) are read there
+// by the tail lanes instead of being tracked per cell.
 // State stays in registers for the whole call; x is staged per series in
 // double-buffered shared-memory tiles by 1-D TMA bulk copies (cp.async.bulk +
 // mbarrier); state is spilled to HBM (coalesced) once per call.
@@ -27,16 +33,18 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "fastmath.cuh"
+
 namespace fbocd {
 
 constexpr int kTile = 256;  // x steps per shared-memory tile (2 KB)
 
 struct SeriesScalars {  // per-series state carried between calls (HBM), 48 B
     double mu0, beta0;  // prior (set from x_0 when prior_first_obs)
-    double n_prev;      // N_{t-1} = log sum_r exp(v_r): the normaliser of the stored v
+    double n_prev;      // N_{t-1}: log sum_r exp(v_r + log(1-H)) of the stored v
     int32_t map_prev;   // r*_{t-1}
     int32_t ev_count;   // events appended since the last drain (may exceed capacity)
-    int32_t flags;      // bit0: non-finite observation seen; bit1: beta0 <= 0
+    int32_t flags;      // bit0: non-finite observation seen; bit1: bad prior
     int32_t pad;
     double pad2;
 };
@@ -57,9 +65,10 @@ struct KParams {
     int prior_first_obs;
     uint32_t ev_mask;
     int ev_cap;
-    const double2* tab_ca;  // [R] {c_r, alpha_r}
-    const double2* tab_gk;  // [R] {g_r, 1/(kappa_r+1)}
-    double* st_mu;          // [S][R] position order
+    const double2* tab_ca;       // [R] {c_r + log(1-H), alpha_r}
+    const double2* tab_gk;       // [R] {g_r, 1/(kappa_r+1)}
+    const FastMathTables* fm;    // log / exp tables
+    double* st_mu;               // [S][R] position order
     double* st_beta;
     double* st_v;
     SeriesScalars* scal;  // [S]
@@ -81,7 +90,6 @@ struct __align__(16) GroupSmem {
     double xbuf[2][kTile];
     unsigned long long red1[NT / 32 > 0 ? NT / 32 : 1];
     double red2[NT / 32 > 0 ? NT / 32 : 1];
-    double spec[2][8];  // [parity][0 lpA,1 lpB,2 e0,3 eA,4 eB,5 eex]
     double mu0, beta0, L0, n_prev;
     int map_prev, ev_count, flags, pad;
     unsigned long long mbar[2];
@@ -148,9 +156,13 @@ __device__ __forceinline__ double ord_val(long long k) {
     return __longlong_as_double(b);
 }
 
-// Issues (or performs) the load of x tile k for this group.  TMA path: one
-// elected thread, completion on gs.mbar[k & 1].  Returns true if the tile was
-// loaded synchronously (caller must group_sync before reading).
+// Biased (unsigned-ordered) argmax key: lp with its low 12 mantissa bits replaced by
+// (4095 - r), so the max key is the max lp and, among (near-)ties, the smallest r.
+__device__ __forceinline__ unsigned long long argmax_key(double lp, int r) {
+    const long long k = (ord_key(lp) & ~0xFFFLL) | (0xFFF - r);
+    return static_cast<unsigned long long>(k) ^ 0x8000000000000000ull;
+}
+
 template <int NT>
 __device__ __forceinline__ void issue_tile_tma(GroupSmem<NT>& gs, const double* xrow, int k, int T) {
     const int base = k * kTile;
@@ -160,10 +172,18 @@ __device__ __forceinline__ void issue_tile_tma(GroupSmem<NT>& gs, const double* 
     tma_load_1d(gs.xbuf[k & 1], xrow + base, unsigned(n) * 8u, &gs.mbar[k & 1]);
 }
 
-template <int NT>
 __device__ __forceinline__ bool tile_tma_ok(const KParams& P, int k) {
     const int n = min(kTile, P.T - k * kTile);
     return P.tma_ok && ((n & 1) == 0);
+}
+
+// Shared memory of one CTA: tables, then per group: GroupSmem + lp rows [2][R].
+template <int NT>
+__host__ __device__ constexpr size_t group_bytes(int R) {
+    return sizeof(GroupSmem<NT>) + size_t(2) * R * sizeof(double);
+}
+__host__ __device__ constexpr size_t table_bytes(int R) {
+    return size_t(R) * 2 * sizeof(double2) + sizeof(FastMathTables);
 }
 
 // ---------------------------------------------------------------------------
@@ -175,17 +195,24 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     const int R = FULL ? NT * J : P.R;
     double2* s_ca = reinterpret_cast<double2*>(smem_raw);
     double2* s_gk = s_ca + R;
-    GroupSmem<NT>* groups = reinterpret_cast<GroupSmem<NT>*>(s_gk + R);
+    FastMathTables* s_fm = reinterpret_cast<FastMathTables*>(s_gk + R);
+    unsigned char* gbase = reinterpret_cast<unsigned char*>(s_fm + 1);
 
     for (int k = threadIdx.x; k < R; k += blockDim.x) {
         s_ca[k] = P.tab_ca[k];
         s_gk[k] = P.tab_gk[k];
     }
+    {
+        const double* src = reinterpret_cast<const double*>(P.fm);
+        double* dst = reinterpret_cast<double*>(s_fm);
+        for (int k = threadIdx.x; k < int(sizeof(FastMathTables) / 8); k += blockDim.x) dst[k] = src[k];
+    }
     const int g = threadIdx.x / NT;
     const int i = threadIdx.x % NT;
     const int lane = threadIdx.x & 31;
     const int w = i >> 5;
-    GroupSmem<NT>& gs = groups[g];
+    GroupSmem<NT>& gs = *reinterpret_cast<GroupSmem<NT>*>(gbase + size_t(g) * group_bytes<NT>(R));
+    double* s_lp = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(&gs) + sizeof(GroupSmem<NT>));
     const int64_t s = int64_t(blockIdx.x) * SPB + g;
     const bool active = s < P.S;
     const double* xrow = P.x + (active ? s : 0) * P.ld;
@@ -197,10 +224,13 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     }
     __syncthreads();
     if (!active) return;
+    const double2* logtab = s_fm->logtab;
+    const double* exptab = s_fm->exptab;
 
     // Prefetch tile 0 (TMA) as early as possible.
-    if (i == 0 && ntiles > 0 && tile_tma_ok<NT>(P, 0)) issue_tile_tma<NT>(gs, xrow, 0, P.T);
+    if (i == 0 && ntiles > 0 && tile_tma_ok(P, 0)) issue_tile_tma<NT>(gs, xrow, 0, P.T);
 
+    const double logH = P.logH, log1mH = P.log1mH;
     // ---- load or initialise the state ------------------------------------
     double mu[J], be[J], L[J], v[J];
     const int64_t sbase = s * int64_t(R);
@@ -215,13 +245,14 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             sc.n_prev = 0.0;
             sc.map_prev = 0;
         }
+        const bool ok = sc.beta0 >= 2.2250738585072014e-308 && sc.beta0 < 1e300 && isfinite(sc.mu0);
         gs.mu0 = sc.mu0;
-        gs.beta0 = sc.beta0;
-        gs.L0 = log(sc.beta0);
+        gs.beta0 = ok ? sc.beta0 : 1.0;
+        gs.L0 = fast_log(gs.beta0, logtab);
         gs.n_prev = sc.n_prev;
         gs.map_prev = sc.map_prev;
         gs.ev_count = sc.ev_count;
-        gs.flags = sc.flags | ((sc.beta0 > 0.0 && isfinite(sc.beta0) && isfinite(sc.mu0)) ? 0 : 2);
+        gs.flags = sc.flags | (ok ? 0 : 2);
     }
     group_sync<NT>(g);
     const double mu0 = gs.mu0, beta0 = gs.beta0, L0 = gs.L0;
@@ -233,12 +264,12 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 mu[j] = mu0;
                 be[j] = beta0;
                 L[j] = L0;
-                v[j] = (p == 0) ? 0.0 : -INFINITY;
+                v[j] = (p == 0) ? -log1mH : -INFINITY;
             } else {
                 mu[j] = P.st_mu[sbase + p];
                 be[j] = P.st_beta[sbase + p];
                 v[j] = P.st_v[sbase + p];
-                L[j] = log(be[j]);
+                L[j] = fast_log(be[j], logtab);
             }
         } else {
             mu[j] = mu0;
@@ -248,13 +279,11 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         }
     }
 
-    const double logH = P.logH, log1mH = P.log1mH;
     const bool merge = (P.mode == 0);
     // argmax-eligible run lengths: MERGE r <= R-3 (slot R-1 is the bucket), DROP r <= R-2
     const int r_elig = merge ? R - 3 : R - 2;
     const unsigned long long KEY_NONE = 0ull;  // below every real key (biased order)
-    // ring position bookkeeping: tmod = t mod R
-    int tmod = int(P.t0 % R);
+    int tmod = int(P.t0 % R);                  // ring bookkeeping: t mod R
     bool nonfinite = false;
 
     for (int k = 0; k < ntiles; ++k) {
@@ -263,8 +292,8 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         const int buf = k & 1;
         // prefetch the next tile into the other buffer (its previous readers all
         // passed at least one group barrier since their last read)
-        if (i == 0 && k + 1 < ntiles && tile_tma_ok<NT>(P, k + 1)) issue_tile_tma<NT>(gs, xrow, k + 1, P.T);
-        if (tile_tma_ok<NT>(P, k)) {
+        if (i == 0 && k + 1 < ntiles && tile_tma_ok(P, k + 1)) issue_tile_tma<NT>(gs, xrow, k + 1, P.T);
+        if (tile_tma_ok(P, k)) {
             mbar_wait(&gs.mbar[buf], unsigned(k >> 1) & 1u);
         } else {
             for (int q = i; q < n; q += NT) gs.xbuf[buf][q] = xrow[base + q];
@@ -273,7 +302,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         for (int q = 0; q < n; ++q) {
             const int tl = base + q;
             const int64_t t = P.t0 + tl;
-            const int par = tl & 1;
+            double* lprow = s_lp + (tl & 1) * R;
             const double x = gs.xbuf[buf][q];
             // ---- phase 1: A1 + A2 + A3, local argmax key ----------------
             unsigned long long key = KEY_NONE;
@@ -290,23 +319,19 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     const double2 ca = s_ca[r];
                     const double2 gk = s_gk[r];
                     const double d = x - mu[j];
-                    const double gd = gk.x * d;
-                    const double bn = fma(gd, d, be[j]);
+                    const double bn = fma(gk.x * d, d, be[j]);
                     mu[j] = fma(d, gk.y, mu[j]);
-                    const double Ln = log(bn);
+                    const double Ln = fast_log(bn, logtab);
                     const double ell = fma(-0.5, Ln, fma(ca.y, L[j] - Ln, ca.x));
                     be[j] = bn;
                     L[j] = Ln;
                     const double lp = v[j] + ell;
                     v[j] = lp;
+                    lprow[p] = lp;
                     if (r <= r_elig) {
-                        const unsigned long long kk =
-                            (static_cast<unsigned long long>((ord_key(lp) & ~0xFFFLL)) | (0xFFFull - r)) ^
-                            0x8000000000000000ull;
+                        const unsigned long long kk = argmax_key(lp, r);
                         key = kk > key ? kk : key;
                     }
-                    if (r == R - 2) gs.spec[par][0] = lp;
-                    if (r == R - 1) gs.spec[par][1] = lp;
                 }
             }
             // ---- group max/argmax --------------------------------------
@@ -327,8 +352,10 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             } else {
                 group_sync<NT>(g);
             }
-            const double lpA = gs.spec[par][0];
-            const double lpB = gs.spec[par][1];
+            const int pB = (tmod + 1 == R) ? 0 : tmod + 1;  // r = R-1: recycled -> new CP cell
+            const int pA = (pB + 1 == R) ? 0 : pB + 1;      // r = R-2: -> bucket r = R-1 (MERGE)
+            const double lpA = lprow[pA];
+            const double lpB = lprow[pB];
             int r_ex = -1;
             double M = fmax(lpA, lpB);
             if (key != KEY_NONE) {
@@ -342,20 +369,9 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             for (int j = 0; j < J; ++j) {
                 const int p = i + NT * j;
                 if (FULL || p < R) {
-                    int r = tmod - p;
-                    if (FULL) {
-                        r &= (R - 1);
-                    } else {
-                        r += (r < 0) ? R : 0;
-                    }
                     const double dm = v[j] - M;
-                    const double e = exp(dm);
-                    sum += e;
-                    v[j] = dm + log1mH;
-                    if (r == 0) gs.spec[par][2] = e;
-                    if (r == R - 2) gs.spec[par][3] = e;
-                    if (r == R - 1) gs.spec[par][4] = e;
-                    if (r == r_ex) gs.spec[par][5] = e;
+                    sum += fast_exp(dm, exptab);
+                    v[j] = dm;
                 }
             }
 #pragma unroll
@@ -370,23 +386,22 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 group_sync<NT>(g);
             }
             // ---- cell fix-ups and the scalar tail (A5-A8) -----------------
-            const int pB = (tmod + 1 == R) ? 0 : tmod + 1;  // recycled: r = R-1 -> new r = 0
-            const int pA = (pB + 1 == R) ? 0 : pB + 1;      // r = R-2 -> bucket r = R-1 (MERGE)
             const bool ownB = (pB % NT) == i;
             const bool ownA = merge && ((pA % NT) == i);
             if (ownB || ownA) {
-                const double eA = gs.spec[par][3], eB = gs.spec[par][4];
+                const double eA = fast_exp(lpA - M, exptab);
+                const double eB = fast_exp(lpB - M, exptab);
                 // one shared log for both fix-ups: log(sum) for the new CP cell, log(eA+eB) for the bucket
                 const double lg = log(ownB ? sum : (eA + eB));
                 if (ownA && !ownB) {
                     const int jA = pA / NT;
 #pragma unroll
                     for (int j = 0; j < J; ++j)
-                        if (j == jA) v[j] = log1mH + lg;
+                        if (j == jA) v[j] = lg;
                 }
                 if (ownB) {
                     const int jB = pB / NT;
-                    const double vcp = logH + lg;
+                    const double vcp = logH - log1mH + lg;
 #pragma unroll
                     for (int j = 0; j < J; ++j)
                         if (j == jB) {
@@ -395,15 +410,15 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                             be[j] = beta0;
                             L[j] = L0;
                         }
-                    if (merge && ownA) {  // R-1 and R-2 owned by the same thread (tiny R)
+                    if (ownA) {  // R-1 and R-2 owned by the same thread (tiny R)
                         const double lb = log(eA + eB);
                         const int jA = pA / NT;
 #pragma unroll
                         for (int j = 0; j < J; ++j)
-                            if (j == jA) v[j] = log1mH + lb;
+                            if (j == jA) v[j] = lb;
                     }
                     // tail: normaliser, log Z, p_new, r*, flags, events
-                    const double e0 = gs.spec[par][2];
+                    const double e0 = fast_exp(lprow[tmod] - M, exptab);  // r = 0 cell
                     double Nt, pnew;
                     if (merge) {
                         Nt = lg;
@@ -415,7 +430,9 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     const double logz = M + Nt - gs.n_prev;
                     int rstar;
                     if (merge) {
-                        const double eex = gs.spec[par][5];
+                        int pex = tmod - r_ex;
+                        pex += (pex < 0) ? R : 0;
+                        const double eex = r_ex >= 0 ? fast_exp(lprow[pex] - M, exptab) : 0.0;
                         rstar = (r_ex < 0 || (eA + eB) > eex) ? R - 1 : r_ex + 1;
                     } else {
                         rstar = r_ex + 1;
@@ -450,7 +467,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         }
     }
     // ---- spill -------------------------------------------------------------
-    if (nonfinite) gs.flags |= 1;  // benign race: every writer stores the same bit set
+    if (nonfinite) atomicOr(&gs.flags, 1);
     group_sync<NT>(g);
 #pragma unroll
     for (int j = 0; j < J; ++j) {

@@ -12,7 +12,7 @@ static Variant make_variant() {
     v.j = J;
     v.spb = SPB;
     v.full = FULL;
-    v.group_smem = sizeof(GroupSmem<NT>);
+    v.group_smem = sizeof(GroupSmem<NT>);  // + 2 R doubles of lp rows (group_bytes)
     return v;
 }
 
@@ -36,6 +36,26 @@ int select_variant(int R, Variant* out) {
     if (R <= 2048) { *out = make_variant<256, 8, false, 1, 2>(); return 0; }
     *out = make_variant<512, 8, false, 1, 1>();
     return 0;
+}
+
+// Test hook: elementwise fast_log / fast_exp over device arrays.
+__global__ void fastmath_probe_kernel(int which, const double* in, double* out, int64_t n,
+                                      const FastMathTables* tab) {
+    __shared__ FastMathTables st;
+    for (int k = threadIdx.x; k < int(sizeof(FastMathTables) / 8); k += blockDim.x)
+        reinterpret_cast<double*>(&st)[k] = reinterpret_cast<const double*>(tab)[k];
+    __syncthreads();
+    for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x)
+        out[k] = which == 0 ? fast_log(in[k], st.logtab) : fast_exp(in[k], st.exptab);
+}
+
+int launch_fastmath_probe(int which, const double* in, double* out, int64_t n, const FastMathTables* tab,
+                          cudaStream_t st) {
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 4096) blocks = 4096;
+    if (blocks < 1) blocks = 1;
+    fastmath_probe_kernel<<<unsigned(blocks), 256, 0, st>>>(which, in, out, n, tab);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 }  // namespace fbocd

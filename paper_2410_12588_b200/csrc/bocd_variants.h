@@ -2,6 +2,8 @@
 #pragma once
 
 #include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
 
 namespace fbocd {
 
@@ -15,5 +17,9 @@ struct Variant {
 };
 
 int select_variant(int R, Variant* out);
+
+struct FastMathTables;
+int launch_fastmath_probe(int which, const double* in, double* out, int64_t n, const FastMathTables* tab,
+                          cudaStream_t st);
 
 }  // namespace fbocd

@@ -29,6 +29,7 @@ struct falcon_bocd_s {
     int64_t t = 0;  // observations absorbed
     double2* d_ca = nullptr;
     double2* d_gk = nullptr;
+    fbocd::FastMathTables* d_fm = nullptr;
     double* d_mu = nullptr;
     double* d_beta = nullptr;
     double* d_v = nullptr;
@@ -107,14 +108,14 @@ __global__ void init_scalars_kernel(SeriesScalars* scal, const double* mu0, cons
 }
 
 __global__ void init_state_kernel(double* mu, double* beta, double* v, const SeriesScalars* scal, int64_t S,
-                                  int R) {
+                                  int R, double v0) {
     const int64_t n = S * int64_t(R);
     for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
         const int64_t s = k / R;
         const int p = int(k - s * R);
         mu[k] = scal[s].mu0;
         beta[k] = scal[s].beta0;
-        v[k] = (p == 0) ? 0.0 : -INFINITY;
+        v[k] = (p == 0) ? v0 : -INFINITY;
     }
 }
 
@@ -182,7 +183,7 @@ __global__ void drain_gather_kernel(SeriesScalars* scal, const EventRec* ev, int
 // Ring position order -> run-length order; log R = v - N_t.
 __global__ void posterior_kernel(const double* mu, const double* beta, const double* v,
                                  const SeriesScalars* scal, int64_t s0, int64_t count, int R, int64_t t,
-                                 double* logR_out, double* mu_out, double* beta_out) {
+                                 double log1mH, double* logR_out, double* mu_out, double* beta_out) {
     const int64_t n = count * int64_t(R);
     const int tm = int(t % R);
     for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
@@ -191,7 +192,7 @@ __global__ void posterior_kernel(const double* mu, const double* beta, const dou
         int p = tm - r;
         if (p < 0) p += R;
         const int64_t src = (s0 + i) * int64_t(R) + p;
-        if (logR_out) logR_out[k] = v[src] - scal[s0 + i].n_prev;
+        if (logR_out) logR_out[k] = (v[src] + log1mH) - scal[s0 + i].n_prev;
         if (mu_out) mu_out[k] = mu[src];
         if (beta_out) beta_out[k] = beta[src];
     }
@@ -320,7 +321,7 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
         delete h;
         return fail(nullptr, FALCON_EINVAL, "no kernel variant for this R");
     }
-    h->smem = size_t(c.R) * 2 * sizeof(double2) + size_t(h->var.spb) * h->var.group_smem;
+    h->smem = fbocd::table_bytes(c.R) + size_t(h->var.spb) * (h->var.group_smem + size_t(2) * c.R * sizeof(double));
     auto bail = [&](int code) {
         g_create_err = h->err;
         falcon_bocd_destroy(h);
@@ -345,10 +346,21 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
     std::vector<double> tc(R), ta(R), tg(R), tk(R);
     falcon_bocd_predictive_constants(R, c.kappa0, c.alpha0, tc.data(), ta.data(), tg.data(), tk.data());
     std::vector<double2> ca(R), gk(R);
-    for (int r = 0; r < R; ++r) {
-        ca[r] = make_double2(tc[r], ta[r]);
-        gk[r] = make_double2(tg[r], tk[r]);
+    {
+        // the device table folds the growth factor log(1-H) into c_r (bocd_kernel.cuh, A3)
+        const long double l1mh = log1pl(-(long double)c.hazard);
+        long double D = lgammal((long double)c.alpha0 + 0.5L) - lgammal((long double)c.alpha0);
+        const long double two_pi = 6.283185307179586476925286766559005768L;
+        for (int r = 0; r < R; ++r) {
+            const long double kap = (long double)c.kappa0 + r;
+            const long double cr = D - 0.5L * logl(two_pi * (kap + 1.0L) / kap);
+            ca[r] = make_double2((double)(cr + l1mh), ta[r]);
+            gk[r] = make_double2(tg[r], tk[r]);
+            D = logl((long double)c.alpha0 + 0.5L * r) - D;
+        }
     }
+    fbocd::FastMathTables fmt;
+    fbocd::fill_fastmath_tables(&fmt);
     const size_t SR = size_t(S) * size_t(R);
     double *dmu0 = nullptr, *dbeta0 = nullptr;
 #define ALLOC(ptr, bytes)                                                   \
@@ -362,6 +374,7 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
     } while (0)
     ALLOC(h->d_ca, R * sizeof(double2));
     ALLOC(h->d_gk, R * sizeof(double2));
+    ALLOC(h->d_fm, sizeof(fbocd::FastMathTables));
     ALLOC(h->d_mu, SR * sizeof(double));
     ALLOC(h->d_beta, SR * sizeof(double));
     ALLOC(h->d_v, SR * sizeof(double));
@@ -376,12 +389,14 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
     cudaError_t e3 = cudaSuccess;
     if (e3 == cudaSuccess) e3 = cudaMemcpy(h->d_ca, ca.data(), R * sizeof(double2), cudaMemcpyHostToDevice);
     if (e3 == cudaSuccess) e3 = cudaMemcpy(h->d_gk, gk.data(), R * sizeof(double2), cudaMemcpyHostToDevice);
+    if (e3 == cudaSuccess) e3 = cudaMemcpy(h->d_fm, &fmt, sizeof(fmt), cudaMemcpyHostToDevice);
     if (e3 == cudaSuccess) e3 = cudaMemcpy(dmu0, mu0.data(), S * sizeof(double), cudaMemcpyHostToDevice);
     if (e3 == cudaSuccess) e3 = cudaMemcpy(dbeta0, beta0.data(), S * sizeof(double), cudaMemcpyHostToDevice);
     if (e3 == cudaSuccess) e3 = cudaMemset(h->d_err, 0, sizeof(unsigned));
     if (e3 == cudaSuccess) {
         init_scalars_kernel<<<grid_for(S, 256), 256>>>(h->d_scal, dmu0, dbeta0, S);
-        init_state_kernel<<<grid_for(int64_t(SR), 256), 256>>>(h->d_mu, h->d_beta, h->d_v, h->d_scal, S, R);
+        init_state_kernel<<<grid_for(int64_t(SR), 256), 256>>>(h->d_mu, h->d_beta, h->d_v, h->d_scal, S, R,
+                                                                 -std::log1p(-c.hazard));
         e3 = cudaGetLastError();
     }
     if (e3 == cudaSuccess) e3 = cudaDeviceSynchronize();
@@ -414,6 +429,7 @@ static int launch_update(falcon_bocd_t h, const double* x_dev, int64_t ld, int64
         P.ev_cap = c.event_capacity;
         P.tab_ca = h->d_ca;
         P.tab_gk = h->d_gk;
+        P.fm = h->d_fm;
         P.st_mu = h->d_mu;
         P.st_beta = h->d_beta;
         P.st_v = h->d_v;
@@ -616,7 +632,8 @@ int falcon_bocd_read_posterior(falcon_bocd_t h, int64_t s0, int64_t count, doubl
         dst[k] = is_device_ptr(outs[k]) ? outs[k] : tmp + k * n;
     }
     posterior_kernel<<<grid_for(int64_t(n), 256), 256, 0, st>>>(h->d_mu, h->d_beta, h->d_v, h->d_scal, s0, count, R,
-                                                                h->t, dst[0], dst[1], dst[2]);
+                                                                h->t, std::log1p(-h->cfg.hazard), dst[0], dst[1],
+                                                                dst[2]);
     cudaError_t e = cudaGetLastError();
     for (int k = 0; k < 3 && e == cudaSuccess; ++k)
         if (outs[k] && dst[k] != outs[k])
@@ -653,7 +670,7 @@ int falcon_bocd_destroy(falcon_bocd_t h) {
         }
     }
     cudaGetLastError();
-    void* ptrs[] = {h->d_ca, h->d_gk, h->d_mu, h->d_beta, h->d_v, h->d_scal, h->d_ev, h->d_err, h->d_off,
+    void* ptrs[] = {h->d_ca, h->d_gk, h->d_fm, h->d_mu, h->d_beta, h->d_v, h->d_scal, h->d_ev, h->d_err, h->d_off,
                     h->d_meta, h->d_evout, h->d_stage[0], h->d_stage[1], h->d_omap, h->d_opnew, h->d_ologz};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -667,5 +684,20 @@ int falcon_bocd_destroy(falcon_bocd_t h) {
 }
 
 const char* falcon_bocd_last_error(falcon_bocd_t h) { return h ? h->err.c_str() : g_create_err.c_str(); }
+
+int falcon_bocd_debug_fastmath(int32_t which, const double* in_dev, double* out_dev, int64_t n, void* stream) {
+    if ((which != 0 && which != 1) || n < 0 || (n > 0 && (!in_dev || !out_dev))) return FALCON_EINVAL;
+    if (n == 0) return FALCON_OK;
+    fbocd::FastMathTables fmt;
+    fbocd::fill_fastmath_tables(&fmt);
+    fbocd::FastMathTables* d = nullptr;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (cudaMalloc((void**)&d, sizeof(fmt)) != cudaSuccess) return FALCON_ENOMEM;
+    cudaError_t e = cudaMemcpyAsync(d, &fmt, sizeof(fmt), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && fbocd::launch_fastmath_probe(which, in_dev, out_dev, n, d, st) != 0) e = cudaErrorLaunchFailure;
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(d);
+    return e == cudaSuccess ? FALCON_OK : FALCON_ECUDA;
+}
 
 }  // extern "C"

@@ -1,0 +1,62 @@
+"""Accuracy of the kernels' branch-free fp64 log / exp (csrc/fastmath.cuh) vs numpy and
+mpmath, through the falcon_bocd_debug_fastmath C-ABI hook.  The BOCD recursion
+uses log on the NIG scale beta' (> 0, normal) and exp on lp - M (<= ~0)."""
+import ctypes
+import math
+
+import mpmath
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2410_12588_b200 import _native as N  # noqa: E402
+
+
+def _probe(which, x):
+    xd = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).cuda()
+    out = torch.empty_like(xd)
+    rc = N.lib().falcon_bocd_debug_fastmath(which, ctypes.c_void_p(xd.data_ptr()),
+                                            ctypes.c_void_p(out.data_ptr()), xd.numel(),
+                                            ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == 0
+    return out.cpu().numpy()
+
+
+def test_fast_log_accuracy():
+    rng = np.random.default_rng(0)
+    x = np.concatenate([
+        np.exp(rng.uniform(np.log(1e-300), np.log(1e300), 200000)),
+        rng.uniform(0.5, 2.0, 200000),
+        1.0 + rng.normal(0, 1e-6, 20000),
+        np.array([1.0, 2.0, 0.5, 0.70703125, 1.4140625, 0.7070312499999999, 1.4140624999999998,
+                  np.nextafter(1.0, 2), np.nextafter(1.0, 0), 2.2250738585072014e-308, 1.7e308]),
+    ])
+    got = _probe(0, x)
+    ref = np.log(x)
+    ulp = np.spacing(np.abs(ref))
+    err = np.abs(got - ref)
+    assert np.all(err <= 2.0 * ulp + 1e-18), float((err / (ulp + 1e-300)).max())
+    mpmath.mp.dps = 40
+    for v in x[::9973]:  # spot-check numpy itself against 40 digits
+        r = float(mpmath.log(mpmath.mpf(float(v))))
+        assert abs(got[list(x).index(v)] - r) <= 2.0 * math.ulp(r) + 1e-18
+
+
+def test_fast_exp_accuracy():
+    rng = np.random.default_rng(1)
+    x = np.concatenate([-rng.exponential(5.0, 200000), rng.uniform(-708, 0, 200000),
+                        -rng.uniform(0, 1e-3, 20000), np.array([0.0, -0.0, 1e-12, -1e-300, -708.0])])
+    got = _probe(1, x)
+    ref = np.exp(x)
+    err = np.abs(got - ref) / ref
+    assert np.all(err <= 2.5e-16), float(err.max())
+
+
+def test_fast_exp_clamps_below():
+    x = np.array([-np.inf, -1e300, -1000.0, -708.5, -745.2])
+    got = _probe(1, x)
+    assert np.all(np.isfinite(got)) and np.all(got >= 0) and np.all(got < 1e-307)
