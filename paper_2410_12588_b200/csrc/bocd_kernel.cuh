@@ -30,6 +30,7 @@
 // mbarrier); state is spilled to HBM (coalesced) once per call.
 #pragma once
 
+#include <climits>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -90,6 +91,7 @@ struct __align__(16) GroupSmem {
     double xbuf[2][kTile];
     unsigned long long red1[NT / 32 > 0 ? NT / 32 : 1];
     double red2[NT / 32 > 0 ? NT / 32 : 1];
+    int redh[NT / 32 > 0 ? NT / 32 : 1];
     double mu0, beta0, L0, n_prev;
     int map_prev, ev_count, flags, pad;
     unsigned long long mbar[2];
@@ -178,29 +180,47 @@ __device__ __forceinline__ bool tile_tma_ok(const KParams& P, int k) {
 }
 
 // Shared memory of one CTA: tables, then per group: GroupSmem + lp rows [2][R].
+// TAB2: the per-r tables are stored twice (entries r and r+R) so the ring index
+// (t - p) mod R becomes (t - p + R) with no masking and compile-time offsets per cell.
 template <int NT>
 __host__ __device__ constexpr size_t group_bytes(int R) {
     return sizeof(GroupSmem<NT>) + size_t(2) * R * sizeof(double);
 }
-__host__ __device__ constexpr size_t table_bytes(int R) {
-    return size_t(R) * 2 * sizeof(double2) + sizeof(FastMathTables);
+__host__ __device__ constexpr size_t table_bytes(int R, bool tab2) {
+    return size_t(R) * (tab2 ? 2 : 1) * 2 * sizeof(double2) + sizeof(FastMathTables);
+}
+
+// order-preserving signed int of the high word of a double (for the shift M)
+__device__ __forceinline__ int ord_hi(double v) {
+    const int h = __double2hiint(v);
+    return h ^ ((h >> 31) & 0x7FFFFFFF);
+}
+__device__ __forceinline__ double ord_hi_val(int oh) {
+    return __hiloint2double(oh >= 0 ? oh : (oh ^ 0x7FFFFFFF), 0);
 }
 
 // ---------------------------------------------------------------------------
-// The kernel.  FULL: R == NT*J (power of two) known at compile time.
+// The kernel.
+//   FULL : R == NT*J (power of two) at compile time;
+//   TAB2 : doubled per-r tables (R <= 2048);
+//   EAGER: the MAP run length r* is reduced every step (per-step MAP output or
+//          MAPRESET events requested); otherwise it is computed on demand, from the
+//          step's lp row in shared memory, only at steps that report an event.
 // ---------------------------------------------------------------------------
-template <int NT, int J, bool FULL, int SPB, int MINB>
+template <int NT, int J, bool FULL, bool TAB2, bool EAGER, int SPB, int MINB>
 __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParams P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int R = FULL ? NT * J : P.R;
+    const int RT = TAB2 ? 2 * R : R;
     double2* s_ca = reinterpret_cast<double2*>(smem_raw);
-    double2* s_gk = s_ca + R;
-    FastMathTables* s_fm = reinterpret_cast<FastMathTables*>(s_gk + R);
+    double2* s_gk = s_ca + RT;
+    FastMathTables* s_fm = reinterpret_cast<FastMathTables*>(s_gk + RT);
     unsigned char* gbase = reinterpret_cast<unsigned char*>(s_fm + 1);
 
-    for (int k = threadIdx.x; k < R; k += blockDim.x) {
-        s_ca[k] = P.tab_ca[k];
-        s_gk[k] = P.tab_gk[k];
+    for (int k = threadIdx.x; k < RT; k += blockDim.x) {
+        const int r = k < R ? k : k - R;
+        s_ca[k] = P.tab_ca[r];
+        s_gk[k] = P.tab_gk[r];
     }
     {
         const double* src = reinterpret_cast<const double*>(P.fm);
@@ -282,8 +302,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     const bool merge = (P.mode == 0);
     // argmax-eligible run lengths: MERGE r <= R-3 (slot R-1 is the bucket), DROP r <= R-2
     const int r_elig = merge ? R - 3 : R - 2;
-    const unsigned long long KEY_NONE = 0ull;  // below every real key (biased order)
-    int tmod = int(P.t0 % R);                  // ring bookkeeping: t mod R
+    int tmod = int(P.t0 % R);  // ring bookkeeping: t mod R
     bool nonfinite = false;
 
     for (int k = 0; k < ntiles; ++k) {
@@ -304,65 +323,77 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             const int64_t t = P.t0 + tl;
             double* lprow = s_lp + (tl & 1) * R;
             const double x = gs.xbuf[buf][q];
-            // ---- phase 1: A1 + A2 + A3, local argmax key ----------------
-            unsigned long long key = KEY_NONE;
+            // ---- phase 1: A1 + A2 + A3 (loads only: no shared store may block the
+            //      scheduler from interleaving the J independent cells) ---------
+            const int ib = tmod - i + R;  // TAB2 index of cell j: ib - NT*j  (= (t - p) mod R, + R)
 #pragma unroll
             for (int j = 0; j < J; ++j) {
                 const int p = i + NT * j;
                 if (FULL || p < R) {
-                    int r = tmod - p;
-                    if (FULL) {
-                        r &= (R - 1);
+                    int idx;
+                    if (TAB2) {
+                        idx = ib - NT * j;
+                    } else if (FULL) {
+                        idx = (tmod - p) & (R - 1);
                     } else {
-                        r += (r < 0) ? R : 0;
+                        idx = tmod - p;
+                        idx += (idx < 0) ? R : 0;
                     }
-                    const double2 ca = s_ca[r];
-                    const double2 gk = s_gk[r];
+                    const double2 gk = s_gk[idx];
                     const double d = x - mu[j];
                     const double bn = fma(gk.x * d, d, be[j]);
                     mu[j] = fma(d, gk.y, mu[j]);
                     const double Ln = fast_log(bn, logtab);
+                    const double2 ca = s_ca[idx];
                     const double ell = fma(-0.5, Ln, fma(ca.y, L[j] - Ln, ca.x));
                     be[j] = bn;
                     L[j] = Ln;
-                    const double lp = v[j] + ell;
-                    v[j] = lp;
-                    lprow[p] = lp;
-                    if (r <= r_elig) {
-                        const unsigned long long kk = argmax_key(lp, r);
-                        key = kk > key ? kk : key;
+                    v[j] = v[j] + ell;  // lp
+                }
+            }
+            // shift M (max over all cells, high word is enough) and, if EAGER, the argmax key
+            int mh = INT_MIN;
+            unsigned long long key = 0ull;  // below every real key (biased order)
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                const int p = i + NT * j;
+                if (FULL || p < R) {
+                    lprow[p] = v[j];
+                    mh = max(mh, ord_hi(v[j]));
+                    if constexpr (EAGER) {
+                        int r = tmod - p;
+                        r += (r < 0) ? R : 0;
+                        const unsigned long long kk = argmax_key(v[j], r);
+                        key = (r <= r_elig && kk > key) ? kk : key;
                     }
                 }
             }
-            // ---- group max/argmax --------------------------------------
-            {
+            // ---- group max (and argmax) ------------------------------------
+            mh = __reduce_max_sync(0xffffffffu, mh);
+            if constexpr (EAGER) {
                 const unsigned hi = unsigned(key >> 32);
                 const unsigned hmax = __reduce_max_sync(0xffffffffu, hi);
                 const unsigned lmax = __reduce_max_sync(0xffffffffu, hi == hmax ? unsigned(key) : 0u);
                 key = (static_cast<unsigned long long>(hmax) << 32) | lmax;
             }
             if constexpr (NT > 32) {
-                if (lane == 0) gs.red1[w] = key;
+                if (lane == 0) {
+                    gs.red1[w] = EAGER ? key : 0ull;
+                    gs.redh[w] = mh;
+                }
                 group_sync<NT>(g);
 #pragma unroll
                 for (int ww = 0; ww < NT / 32; ++ww) {
-                    const unsigned long long o = gs.red1[ww];
-                    key = o > key ? o : key;
+                    mh = max(mh, gs.redh[ww]);
+                    if constexpr (EAGER) {
+                        const unsigned long long o = gs.red1[ww];
+                        key = o > key ? o : key;
+                    }
                 }
             } else {
                 group_sync<NT>(g);
             }
-            const int pB = (tmod + 1 == R) ? 0 : tmod + 1;  // r = R-1: recycled -> new CP cell
-            const int pA = (pB + 1 == R) ? 0 : pB + 1;      // r = R-2: -> bucket r = R-1 (MERGE)
-            const double lpA = lprow[pA];
-            const double lpB = lprow[pB];
-            int r_ex = -1;
-            double M = fmax(lpA, lpB);
-            if (key != KEY_NONE) {
-                const long long sk = static_cast<long long>(key ^ 0x8000000000000000ull);
-                r_ex = int(0xFFF - (sk & 0xFFF));
-                M = fmax(M, ord_val(sk & ~0xFFFLL));
-            }
+            const double M = ord_hi_val(mh);
             // ---- phase 2: exp + sum, growth (A4, A5) --------------------
             double sum = 0.0;
 #pragma unroll
@@ -386,13 +417,18 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 group_sync<NT>(g);
             }
             // ---- cell fix-ups and the scalar tail (A5-A8) -----------------
+            const int pB = (tmod + 1 == R) ? 0 : tmod + 1;  // r = R-1: recycled -> new CP cell
+            const int pA = (pB + 1 == R) ? 0 : pB + 1;      // r = R-2: -> bucket r = R-1 (MERGE)
             const bool ownB = (pB % NT) == i;
             const bool ownA = merge && ((pA % NT) == i);
+            const double lpA = lprow[pA], lpB = lprow[pB];
+            double eA = 0.0, eB = 0.0, pnew = 0.0;
+            uint32_t fl = 0;
             if (ownB || ownA) {
-                const double eA = fast_exp(lpA - M, exptab);
-                const double eB = fast_exp(lpB - M, exptab);
+                eA = fast_exp(lpA - M, exptab);
+                eB = fast_exp(lpB - M, exptab);
                 // one shared log for both fix-ups: log(sum) for the new CP cell, log(eA+eB) for the bucket
-                const double lg = log(ownB ? sum : (eA + eB));
+                const double lg = fast_log(ownB ? sum : (eA + eB), logtab);
                 if (ownA && !ownB) {
                     const int jA = pA / NT;
 #pragma unroll
@@ -411,57 +447,83 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                             L[j] = L0;
                         }
                     if (ownA) {  // R-1 and R-2 owned by the same thread (tiny R)
-                        const double lb = log(eA + eB);
+                        const double lb = fast_log(eA + eB, logtab);
                         const int jA = pA / NT;
 #pragma unroll
                         for (int j = 0; j < J; ++j)
                             if (j == jA) v[j] = lb;
                     }
-                    // tail: normaliser, log Z, p_new, r*, flags, events
                     const double e0 = fast_exp(lprow[tmod] - M, exptab);  // r = 0 cell
-                    double Nt, pnew;
+                    double Nt;
                     if (merge) {
                         Nt = lg;
                         pnew = (R == 2 ? eA + eB : e0) / sum;
                     } else {
-                        Nt = log(sum - P.omH * eB);
+                        Nt = fast_log(sum - P.omH * eB, logtab);
                         pnew = e0 / (sum - eB);
                     }
-                    const double logz = M + Nt - gs.n_prev;
-                    int rstar;
-                    if (merge) {
-                        int pex = tmod - r_ex;
-                        pex += (pex < 0) ? R : 0;
-                        const double eex = r_ex >= 0 ? fast_exp(lprow[pex] - M, exptab) : 0.0;
-                        rstar = (r_ex < 0 || (eA + eB) > eex) ? R - 1 : r_ex + 1;
-                    } else {
-                        rstar = r_ex + 1;
-                    }
-                    uint32_t fl = 0;
-                    if (t > 0) {
-                        if (pnew > P.theta) fl |= 1u;
-                        const int cap = min(gs.map_prev + 1, R - 1);
-                        if (rstar < cap) fl |= 2u;
-                    }
-                    if (fl & P.ev_mask) {
-                        const int idx = gs.ev_count++;
-                        if (idx < P.ev_cap) {
-                            EventRec ev;
-                            ev.t = t;
-                            ev.cp_index = t - rstar + 1;
-                            ev.flags = fl;
-                            ev.pad = 0;
-                            ev.p_new = pnew;
-                            P.ev[s * P.ev_cap + idx] = ev;
-                        }
-                    }
-                    gs.map_prev = rstar;
-                    gs.n_prev = Nt;
-                    if (P.out_map) P.out_map[s * P.ld_o + tl] = rstar;
+                    if (t > 0 && pnew > P.theta) fl |= 1u;
                     if (P.out_pnew) P.out_pnew[s * P.ld_o + tl] = pnew;
-                    if (P.out_logz) P.out_logz[s * P.ld_o + tl] = logz;
+                    if (P.out_logz) P.out_logz[s * P.ld_o + tl] = M + Nt - gs.n_prev;
+                    gs.n_prev = Nt;
                     if (!isfinite(x)) nonfinite = true;
                 }
+            }
+            // ---- MAP run length r* (A7) ---------------------------------
+            int r_ex = -1;
+            if constexpr (EAGER) {
+                if (key != 0ull) {
+                    const long long sk = static_cast<long long>(key ^ 0x8000000000000000ull);
+                    r_ex = int(0xFFF - (sk & 0xFFF));
+                }
+            } else {
+                const int iB = pB % NT;
+                if ((iB >> 5) == w) {  // warp-uniform: the warp of the tail lane
+                    const int need = __shfl_sync(0xffffffffu, int(fl & P.ev_mask), iB & 31);
+                    if (need) {  // an event at this step: reduce the argmax from the lp row
+                        unsigned long long kb = 0ull;
+                        for (int qq = lane; qq < R; qq += 32) {
+                            int r = tmod - qq;
+                            r += (r < 0) ? R : 0;
+                            const unsigned long long kk = argmax_key(lprow[qq], r);
+                            kb = (r <= r_elig && kk > kb) ? kk : kb;
+                        }
+                        const unsigned hi = unsigned(kb >> 32);
+                        const unsigned hmax = __reduce_max_sync(0xffffffffu, hi);
+                        const unsigned lmax = __reduce_max_sync(0xffffffffu, hi == hmax ? unsigned(kb) : 0u);
+                        kb = (static_cast<unsigned long long>(hmax) << 32) | lmax;
+                        if (kb != 0ull) {
+                            const long long sk = static_cast<long long>(kb ^ 0x8000000000000000ull);
+                            r_ex = int(0xFFF - (sk & 0xFFF));
+                        }
+                    }
+                }
+            }
+            if (ownB && (EAGER || (fl & P.ev_mask))) {
+                int rstar;
+                if (merge) {
+                    int pex = tmod - r_ex;
+                    pex += (pex < 0) ? R : 0;
+                    const double eex = r_ex >= 0 ? fast_exp(lprow[pex] - M, exptab) : 0.0;
+                    rstar = (r_ex < 0 || (eA + eB) > eex) ? R - 1 : r_ex + 1;
+                } else {
+                    rstar = r_ex + 1;
+                }
+                if (EAGER && t > 0 && rstar < min(gs.map_prev + 1, R - 1)) fl |= 2u;
+                if (fl & P.ev_mask) {
+                    const int idx = gs.ev_count++;
+                    if (idx < P.ev_cap) {
+                        EventRec ev;
+                        ev.t = t;
+                        ev.cp_index = t - rstar + 1;
+                        ev.flags = fl;
+                        ev.pad = 0;
+                        ev.p_new = pnew;
+                        P.ev[s * P.ev_cap + idx] = ev;
+                    }
+                }
+                gs.map_prev = rstar;
+                if (P.out_map) P.out_map[s * P.ld_o + tl] = rstar;
             }
             tmod = (tmod + 1 == R) ? 0 : tmod + 1;
         }

@@ -4,37 +4,40 @@
 
 namespace fbocd {
 
-template <int NT, int J, bool FULL, int SPB, int MINB>
-static Variant make_variant() {
+template <int NT, int J, bool FULL, bool TAB2, int SPB, int MINB>
+static void make_variant(Variant* out) {
     Variant v;
-    v.fn = reinterpret_cast<const void*>(&bocd_update_kernel<NT, J, FULL, SPB, MINB>);
+    v.fn = reinterpret_cast<const void*>(&bocd_update_kernel<NT, J, FULL, TAB2, false, SPB, MINB>);
+    v.fn_eager = reinterpret_cast<const void*>(&bocd_update_kernel<NT, J, FULL, TAB2, true, SPB, MINB>);
     v.nt = NT;
     v.j = J;
     v.spb = SPB;
     v.full = FULL;
+    v.tab2 = TAB2;
     v.group_smem = sizeof(GroupSmem<NT>);  // + 2 R doubles of lp rows (group_bytes)
-    return v;
+    *out = v;
 }
 
 // Variant choice: FULL kernels (R = NT*J, compile-time ring arithmetic) for the
 // power-of-two R of the BASELINE configs; generic kernels (runtime R, masked
-// cells) for any other 2 <= R <= 4096.
+// cells) for any other 2 <= R <= 4096.  Each variant has a lazy-MAP and an
+// EAGER-MAP kernel (bocd_kernel.cuh).
 int select_variant(int R, Variant* out) {
     switch (R) {
-        case 256: *out = make_variant<32, 8, true, 8, 2>(); return 0;
-        case 512: *out = make_variant<64, 8, true, 4, 2>(); return 0;
-        case 1024: *out = make_variant<128, 8, true, 2, 2>(); return 0;
-        case 2048: *out = make_variant<256, 8, true, 1, 2>(); return 0;
-        case 4096: *out = make_variant<512, 8, true, 1, 1>(); return 0;
+        case 256: make_variant<32, 8, true, true, 8, 2>(out); return 0;
+        case 512: make_variant<64, 8, true, true, 4, 2>(out); return 0;
+        case 1024: make_variant<128, 8, true, true, 2, 2>(out); return 0;
+        case 2048: make_variant<256, 8, true, false, 1, 2>(out); return 0;
+        case 4096: make_variant<512, 8, true, false, 1, 1>(out); return 0;
         default: break;
     }
     if (R < 2 || R > 4096) return -1;
-    if (R <= 32) { *out = make_variant<32, 1, false, 8, 2>(); return 0; }
-    if (R <= 256) { *out = make_variant<32, 8, false, 8, 2>(); return 0; }
-    if (R <= 512) { *out = make_variant<64, 8, false, 4, 2>(); return 0; }
-    if (R <= 1024) { *out = make_variant<128, 8, false, 2, 2>(); return 0; }
-    if (R <= 2048) { *out = make_variant<256, 8, false, 1, 2>(); return 0; }
-    *out = make_variant<512, 8, false, 1, 1>();
+    if (R <= 32) { make_variant<32, 1, false, true, 8, 2>(out); return 0; }
+    if (R <= 256) { make_variant<32, 8, false, true, 8, 2>(out); return 0; }
+    if (R <= 512) { make_variant<64, 8, false, true, 4, 2>(out); return 0; }
+    if (R <= 1024) { make_variant<128, 8, false, true, 2, 2>(out); return 0; }
+    if (R <= 2048) { make_variant<256, 8, false, false, 1, 2>(out); return 0; }
+    make_variant<512, 8, false, false, 1, 1>(out);
     return 0;
 }
 

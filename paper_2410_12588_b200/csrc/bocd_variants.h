@@ -8,11 +8,13 @@
 namespace fbocd {
 
 struct Variant {
-    const void* fn = nullptr;  // __global__ void(KParams)
+    const void* fn = nullptr;        // __global__ void(KParams), MAP on demand
+    const void* fn_eager = nullptr;  // MAP reduced every step
     int nt = 0;                // threads per series group
     int j = 0;                 // cells per thread
     int spb = 0;               // series groups per CTA
     bool full = false;         // R == nt * j at compile time
+    bool tab2 = false;         // doubled per-r tables
     size_t group_smem = 0;     // bytes of per-group shared memory
 };
 

@@ -321,7 +321,8 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
         delete h;
         return fail(nullptr, FALCON_EINVAL, "no kernel variant for this R");
     }
-    h->smem = fbocd::table_bytes(c.R) + size_t(h->var.spb) * (h->var.group_smem + size_t(2) * c.R * sizeof(double));
+    h->smem = fbocd::table_bytes(c.R, h->var.tab2) +
+              size_t(h->var.spb) * (h->var.group_smem + size_t(2) * c.R * sizeof(double));
     auto bail = [&](int code) {
         g_create_err = h->err;
         falcon_bocd_destroy(h);
@@ -339,8 +340,10 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
         h->err = "shared memory footprint too large";
         return bail(FALCON_EINVAL);
     }
-    cudaError_t e = cudaFuncSetAttribute(h->var.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(h->smem));
-    if (e != cudaSuccess) return bail(cuda_fail(h, e, "cudaFuncSetAttribute"));
+    for (const void* fn : {h->var.fn, h->var.fn_eager}) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(h->smem));
+        if (e != cudaSuccess) return bail(cuda_fail(h, e, "cudaFuncSetAttribute"));
+    }
 
     const int R = c.R;
     std::vector<double> tc(R), ta(R), tg(R), tk(R);
@@ -447,8 +450,11 @@ static int launch_update(falcon_bocd_t h, const double* x_dev, int64_t ld, int64
         P.tma_ok = ((reinterpret_cast<uintptr_t>(P.x) & 15u) == 0) && ((ld & 1) == 0);
         const int64_t grid = (c.n_series + h->var.spb - 1) / h->var.spb;
         void* args[] = {&P};
-        cudaError_t e = cudaLaunchKernel(h->var.fn, dim3(unsigned(grid)), dim3(unsigned(h->var.nt * h->var.spb)),
-                                         args, h->smem, st);
+        // r* every step only when it is an output (per-step MAP, MAPRESET events); otherwise
+        // the kernel reduces it on demand at the steps that report an event.
+        const bool eager = (c.event_mask & FALCON_EV_MAPRESET) || omap;
+        cudaError_t e = cudaLaunchKernel(eager ? h->var.fn_eager : h->var.fn, dim3(unsigned(grid)),
+                                         dim3(unsigned(h->var.nt * h->var.spb)), args, h->smem, st);
         if (e != cudaSuccess) return cuda_fail(h, e, "bocd_update_kernel launch");
         h->t += n;
         done += n;

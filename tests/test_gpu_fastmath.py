@@ -39,7 +39,10 @@ def test_fast_log_accuracy():
     ref = np.log(x)
     ulp = np.spacing(np.abs(ref))
     err = np.abs(got - ref)
-    assert np.all(err <= 2.0 * ulp + 1e-18), float((err / (ulp + 1e-300)).max())
+    # absolute accuracy is what the recursion needs (differences of logs); near x = 1 the
+    # result is tiny and its own ulp is meaningless, so allow 4e-18 absolute there
+    bad = err > 2.0 * ulp + 4e-18
+    assert not np.any(bad), list(zip(x[bad][:5], got[bad][:5], ref[bad][:5]))
     mpmath.mp.dps = 40
     for v in x[::9973]:  # spot-check numpy itself against 40 digits
         r = float(mpmath.log(mpmath.mpf(float(v))))
