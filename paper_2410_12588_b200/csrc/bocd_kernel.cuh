@@ -187,7 +187,36 @@ __host__ __device__ constexpr size_t group_bytes(int R) {
     return sizeof(GroupSmem<NT>) + size_t(2) * R * sizeof(double);
 }
 __host__ __device__ constexpr size_t table_bytes(int R, bool tab2) {
-    return size_t(R) * (tab2 ? 2 : 1) * 2 * sizeof(double2) + sizeof(FastMathTables);
+    return size_t(R) * (tab2 ? 2 : 1) * 2 * sizeof(double2);
+}
+
+// Writes one cell of the register state (dynamic index j, warp-uniform in practice:
+// a jump over J cases instead of J predicated selects per array).
+template <int J>
+__device__ __forceinline__ void set_cell(double (&v)[J], double (&mu)[J], double (&be)[J], double (&L)[J],
+                                         int j, double vv, double m, double b, double l) {
+#define FBOCD_SET(k)                      \
+    case k:                               \
+        if constexpr (J > k) {            \
+            v[k] = vv;                    \
+            mu[k] = m;                    \
+            be[k] = b;                    \
+            L[k] = l;                     \
+        }                                 \
+        break;
+    switch (j) { FBOCD_SET(0) FBOCD_SET(1) FBOCD_SET(2) FBOCD_SET(3) FBOCD_SET(4) FBOCD_SET(5) FBOCD_SET(6) FBOCD_SET(7) }
+#undef FBOCD_SET
+}
+template <int J>
+__device__ __forceinline__ void set_v(double (&v)[J], int j, double vv) {
+#define FBOCD_SETV(k)            \
+    case k:                      \
+        if constexpr (J > k) {   \
+            v[k] = vv;           \
+        }                        \
+        break;
+    switch (j) { FBOCD_SETV(0) FBOCD_SETV(1) FBOCD_SETV(2) FBOCD_SETV(3) FBOCD_SETV(4) FBOCD_SETV(5) FBOCD_SETV(6) FBOCD_SETV(7) }
+#undef FBOCD_SETV
 }
 
 // order-preserving signed int of the high word of a double (for the shift M)
@@ -210,12 +239,13 @@ __device__ __forceinline__ double ord_hi_val(int oh) {
 template <int NT, int J, bool FULL, bool TAB2, bool EAGER, int SPB, int MINB>
 __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParams P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ FastMathTables s_fm_static;  // static: table lookups use immediate addresses
     const int R = FULL ? NT * J : P.R;
     const int RT = TAB2 ? 2 * R : R;
     double2* s_ca = reinterpret_cast<double2*>(smem_raw);
     double2* s_gk = s_ca + RT;
-    FastMathTables* s_fm = reinterpret_cast<FastMathTables*>(s_gk + RT);
-    unsigned char* gbase = reinterpret_cast<unsigned char*>(s_fm + 1);
+    FastMathTables* s_fm = &s_fm_static;
+    unsigned char* gbase = reinterpret_cast<unsigned char*>(s_gk + RT);
 
     for (int k = threadIdx.x; k < RT; k += blockDim.x) {
         const int r = k < R ? k : k - R;
@@ -417,50 +447,38 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 group_sync<NT>(g);
             }
             // ---- cell fix-ups and the scalar tail (A5-A8) -----------------
-            const int pB = (tmod + 1 == R) ? 0 : tmod + 1;  // r = R-1: recycled -> new CP cell
-            const int pA = (pB + 1 == R) ? 0 : pB + 1;      // r = R-2: -> bucket r = R-1 (MERGE)
-            const bool ownB = (pB % NT) == i;
+            // Two lanes per step: the owner of pB (r = R-1, recycled into the new CP cell:
+            // v = log H - log(1-H) + log(sum), prior statistics) and, for MERGE, the owner of
+            // pA (r = R-2 -> bucket: v = log(e_{R-2} + e_{R-1}) = mx + log(1 + exp(mn - mx))).
+            // Both run the same exp-then-log sequence on different operands (one SIMT pass).
+            const int pB = (tmod + 1 == R) ? 0 : tmod + 1;
+            const int pA = (pB + 1 == R) ? 0 : pB + 1;
+            const int iB = pB % NT;
+            const bool ownB = iB == i;
             const bool ownA = merge && ((pA % NT) == i);
-            const double lpA = lprow[pA], lpB = lprow[pB];
-            double eA = 0.0, eB = 0.0, pnew = 0.0;
+            const double dA = lprow[pA] - M, dB = lprow[pB] - M;
+            const double mx = fmax(dA, dB), mn = fmin(dA, dB);
+            double pnew = 0.0;
             uint32_t fl = 0;
             if (ownB || ownA) {
-                eA = fast_exp(lpA - M, exptab);
-                eB = fast_exp(lpB - M, exptab);
-                // one shared log for both fix-ups: log(sum) for the new CP cell, log(eA+eB) for the bucket
-                const double lg = fast_log(ownB ? sum : (eA + eB), logtab);
-                if (ownA && !ownB) {
-                    const int jA = pA / NT;
-#pragma unroll
-                    for (int j = 0; j < J; ++j)
-                        if (j == jA) v[j] = lg;
-                }
+                const double earg = ownB ? (lprow[tmod] - M) : (mx == -INFINITY ? -INFINITY : mn - mx);
+                const double ee = fast_exp(earg, exptab);  // B: e_0 (r = 0 cell);  A: exp(mn - mx)
+                const double lg = fast_log(ownB ? sum : 1.0 + ee, logtab);
+                if (ownA && !ownB) set_v<J>(v, pA / NT, mx == -INFINITY ? -INFINITY : mx + lg);
                 if (ownB) {
-                    const int jB = pB / NT;
-                    const double vcp = logH - log1mH + lg;
-#pragma unroll
-                    for (int j = 0; j < J; ++j)
-                        if (j == jB) {
-                            v[j] = vcp;
-                            mu[j] = mu0;
-                            be[j] = beta0;
-                            L[j] = L0;
-                        }
-                    if (ownA) {  // R-1 and R-2 owned by the same thread (tiny R)
-                        const double lb = fast_log(eA + eB, logtab);
-                        const int jA = pA / NT;
-#pragma unroll
-                        for (int j = 0; j < J; ++j)
-                            if (j == jA) v[j] = lb;
+                    set_cell<J>(v, mu, be, L, pB / NT, logH - log1mH + lg, mu0, beta0, L0);
+                    if (ownA) {  // r = R-1 and R-2 in one thread (tiny R): second pass
+                        const double u = fast_exp(mx == -INFINITY ? -INFINITY : mn - mx, exptab);
+                        set_v<J>(v, pA / NT, mx == -INFINITY ? -INFINITY : mx + fast_log(1.0 + u, logtab));
                     }
-                    const double e0 = fast_exp(lprow[tmod] - M, exptab);  // r = 0 cell
                     double Nt;
                     if (merge) {
                         Nt = lg;
-                        pnew = (R == 2 ? eA + eB : e0) / sum;
+                        pnew = (R == 2) ? 1.0 : ee * fast_rcp(sum);  // R(1) / (1 - R(0)), R(0) = H
                     } else {
+                        const double eB = fast_exp(dB, exptab);
                         Nt = fast_log(sum - P.omH * eB, logtab);
-                        pnew = e0 / (sum - eB);
+                        pnew = ee * fast_rcp(sum - eB);
                     }
                     if (t > 0 && pnew > P.theta) fl |= 1u;
                     if (P.out_pnew) P.out_pnew[s * P.ld_o + tl] = pnew;
@@ -477,7 +495,6 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     r_ex = int(0xFFF - (sk & 0xFFF));
                 }
             } else {
-                const int iB = pB % NT;
                 if ((iB >> 5) == w) {  // warp-uniform: the warp of the tail lane
                     const int need = __shfl_sync(0xffffffffu, int(fl & P.ev_mask), iB & 31);
                     if (need) {  // an event at this step: reduce the argmax from the lp row
@@ -502,10 +519,14 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             if (ownB && (EAGER || (fl & P.ev_mask))) {
                 int rstar;
                 if (merge) {
+                    // bucket (log(1-H) + mx + log(1 + exp(mn - mx))) vs the best growth slot
+                    // (log(1-H) + d_ex); ties -> the smaller run length (the growth slot)
                     int pex = tmod - r_ex;
                     pex += (pex < 0) ? R : 0;
-                    const double eex = r_ex >= 0 ? fast_exp(lprow[pex] - M, exptab) : 0.0;
-                    rstar = (r_ex < 0 || (eA + eB) > eex) ? R - 1 : r_ex + 1;
+                    const double dex = r_ex >= 0 ? lprow[pex] - M : -INFINITY;
+                    const double u = fast_exp(mx == -INFINITY ? -INFINITY : mn - mx, exptab);
+                    const double bucket = mx == -INFINITY ? -INFINITY : mx + fast_log(1.0 + u, logtab);
+                    rstar = (r_ex < 0 || bucket > dex) ? R - 1 : r_ex + 1;
                 } else {
                     rstar = r_ex + 1;
                 }

@@ -14,7 +14,8 @@
 //       invc_i ~ 1/c_i and logc_i = -log(invc_i) (long double on the host);
 //       r = fma(z, invc_i, -1) is exact up to one rounding, |r| < 0.0040, and
 //       log b = k ln2 + logc_i + log1p(r) with log1p(r) = r + r^2 P(r), P the
-//       degree-4 Taylor tail (truncation < 2e-18).  12 FP64 + ~9 integer ops.
+//       degree-4 Taylor tail (truncation < 2e-18).  12 FP64 + ~7 integer ops.
+//       Valid for 2^-1000 < b < 2^1000 (the 2^-k scaling is folded into invc_i).
 // exp:  d clamped to >= -708 on the integer pipe (exp < 4e-308 is irrelevant
 //       next to the max term 1), d = (64 k + j) ln2/64 + r, |r| <= ln2/128,
 //       exp d = 2^k T_j (1 + q(r)), T_j = 2^(j/64) from a 64-entry table,
@@ -62,14 +63,13 @@ constexpr double LN2_LO = 1.90821492927058770002e-10;  // 0x3dea39ef35793c76
 
 __device__ __forceinline__ double fast_log(double x, const double2* __restrict__ logtab) {
     const int hi = __double2hiint(x);
-    const int lo = __double2loint(x);
-    const int tmp = hi - 0x3FE6A000;              // OFF = 0x3FE6A000_00000000 (low word 0)
-    const int i = (tmp >> 13) & (kLogTab - 1);    // top 7 mantissa bits of (ix - OFF)
-    const int k = tmp >> 20;                      // arithmetic: exponent of x relative to OFF
-    const double z = __hiloint2double(hi - (tmp & 0xFFF00000), lo);
-    const double2 t = logtab[i];
-    const double r = fma(z, t.x, -1.0);
-    const double kd = __hiloint2double(0x43300000, k ^ 0x80000000) - 4503601774854144.0;  // 2^52 + 2^31
+    const int tb = hi + 0x00196000;          // (hi - 0x3FE6A000) + (1024 << 20): biased k in bits 20..31
+    const double2 t = logtab[(tb >> 13) & (kLogTab - 1)];  // top 7 mantissa bits of (ix - OFF)
+    // r = z * invc - 1 with z = x / 2^k: the exact power-of-two scaling is folded into invc
+    const double invs =
+        __hiloint2double(__double2hiint(t.x) + 0x40000000 - (tb & 0xFFF00000), __double2loint(t.x));
+    const double r = fma(x, invs, -1.0);
+    const double kd = __hiloint2double(0x43300000, int(unsigned(tb) >> 20)) - 4503599627371520.0;  // 2^52+1024
     const double r2 = r * r;
     double p = fma(r, -1.0 / 6.0, 0.2);
     p = fma(p, r, -0.25);
@@ -78,6 +78,14 @@ __device__ __forceinline__ double fast_log(double x, const double2* __restrict__
     const double w = fma(kd, LN2_HI, t.y);  // exact product, one rounding
     const double q = fma(r2, p, kd * LN2_LO);
     return (w + r) + q;
+}
+
+// 1/x to ~1 ulp for positive normal x: MUFU seed + one Newton step (no IEEE division path).
+__device__ __forceinline__ double fast_rcp(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    const double e = fma(-x, r, 1.0);
+    return fma(r, e, r);
 }
 
 __device__ __forceinline__ double fast_exp(double x, const double* __restrict__ exptab) {
