@@ -9,18 +9,19 @@
 // exactly the one that becomes the new change-point cell.  Per-r constants of
 // the Student-t predictive come from a shared-memory table indexed by r.
 //
-// Per step (all fp64, no fast-math; log/exp are the branch-free table-driven
-// versions of fastmath.cuh):
+// Per step (all fp64, no fast-math).  Every log-domain quantity is kept in BASE-2
+// units (log2), so the transcendentals are the 9-instruction branch-free
+// fast_log2 / fast_exp2 of fastmath.cuh; natural-log outputs are converted once.
 //   A1  NIG update           mu' = mu + d/(kappa+1),  beta' = beta + kappa d^2 / (2(kappa+1))
-//   A2  Student-t predictive l_r = c_r + alpha_r (log beta - log beta') - 1/2 log beta'
-//       (= c_r - 1/2 log beta - (alpha_r + 1/2) log1p(kappa d^2 / (2 beta (kappa+1))))
-//   A3/A4  lp_r = v_r + log(1-H) + l_r  (log(1-H) folded into the c_r table);
-//       group max/argmax (one 64-bit key per cell, REDUX), then sum_r exp(lp_r - M)
+//   A2  Student-t predictive l_r/ln2 = c_r/ln2 + alpha_r (lg beta - lg beta') - 1/2 lg beta'
+//       (lg = log2; = [c_r - 1/2 log beta - (alpha_r + 1/2) log1p(kappa d^2 / (2 beta (kappa+1)))]/ln2)
+//   A3/A4  lp_r = v_r + lg(1-H) + l_r/ln2  (lg(1-H) folded into the c_r table);
+//       group max (order-preserving high word, REDUX), then sum_r 2^(lp_r - M)
 //       (xor butterfly + fixed-order cross-warp sum: deterministic)
-//   A5  growth:  v'_{r+1} = lp_r - M;  v'_0 = log H - log(1-H) + log(sum);  the stored
-//       posterior is UNNORMALISED and offset by -log(1-H):
-//       log R_t(r) = v'_r + log(1-H) - N_t,  N_t = log sum_r exp(v'_r + log(1-H))
-//   A6  MERGE: v'_{R-1} = log(e_{R-2} + e_{R-1});  DROP: e_{R-1} is discarded
+//   A5  growth:  v'_{r+1} = lp_r - M;  v'_0 = lg H - lg(1-H) + lg(sum);  the stored
+//       posterior is UNNORMALISED and offset by -lg(1-H):
+//       log R_t(r) = ln2 (v'_r + lg(1-H) - N_t),  N_t = lg sum_r 2^(v'_r + lg(1-H))
+//   A6  MERGE: v'_{R-1} = lg(e_{R-2} + e_{R-1});  DROP: e_{R-1} is discarded
 //   A7  r*, p_new = e_0 / sum (MERGE) or e_0 / (sum - e_{R-1}) (DROP), flags, events
 // Every lp is also written to a per-series shared-memory row (double-buffered by
 // step parity) so the O(1) special cells (R-2, R-1, 0, argmax) are read there
@@ -42,7 +43,7 @@ constexpr int kTile = 256;  // x steps per shared-memory tile (2 KB)
 
 struct SeriesScalars {  // per-series state carried between calls (HBM), 48 B
     double mu0, beta0;  // prior (set from x_0 when prior_first_obs)
-    double n_prev;      // N_{t-1}: log sum_r exp(v_r + log(1-H)) of the stored v
+    double n_prev;      // N_{t-1}: log2 sum_r 2^(v_r + log2(1-H)) of the stored v (log2 units)
     int32_t map_prev;   // r*_{t-1}
     int32_t ev_count;   // events appended since the last drain (may exceed capacity)
     int32_t flags;      // bit0: non-finite observation seen; bit1: bad prior
@@ -61,12 +62,12 @@ struct EventRec {  // 32 B, series id implicit
 struct KParams {
     int R;
     int64_t S;
-    double logH, log1mH, omH, theta, alpha0, prior_cov;
+    double l2H, l2mH, omH, theta, alpha0, prior_cov;  // l2H = log2 H, l2mH = log2(1-H)
     int mode;  // 0 MERGE, 1 DROP
     int prior_first_obs;
     uint32_t ev_mask;
     int ev_cap;
-    const double2* tab_ca;       // [R] {c_r + log(1-H), alpha_r}
+    const double2* tab_ca;       // [R] {c_r / ln2 + log2(1-H), alpha_r}
     const double2* tab_gk;       // [R] {g_r, 1/(kappa_r+1)}
     const FastMathTables* fm;    // log / exp tables
     double* st_mu;               // [S][R] position order
@@ -280,7 +281,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     // Prefetch tile 0 (TMA) as early as possible.
     if (i == 0 && ntiles > 0 && tile_tma_ok(P, 0)) issue_tile_tma<NT>(gs, xrow, 0, P.T);
 
-    const double logH = P.logH, log1mH = P.log1mH;
+    const double l2H = P.l2H, l2mH = P.l2mH;
     // ---- load or initialise the state ------------------------------------
     double mu[J], be[J], L[J], v[J];
     const int64_t sbase = s * int64_t(R);
@@ -298,7 +299,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         const bool ok = sc.beta0 >= 2.2250738585072014e-308 && sc.beta0 < 1e300 && isfinite(sc.mu0);
         gs.mu0 = sc.mu0;
         gs.beta0 = ok ? sc.beta0 : 1.0;
-        gs.L0 = fast_log(gs.beta0, logtab);
+        gs.L0 = fast_log2(gs.beta0, logtab);
         gs.n_prev = sc.n_prev;
         gs.map_prev = sc.map_prev;
         gs.ev_count = sc.ev_count;
@@ -314,12 +315,12 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 mu[j] = mu0;
                 be[j] = beta0;
                 L[j] = L0;
-                v[j] = (p == 0) ? -log1mH : -INFINITY;
+                v[j] = (p == 0) ? -l2mH : -INFINITY;
             } else {
                 mu[j] = P.st_mu[sbase + p];
                 be[j] = P.st_beta[sbase + p];
                 v[j] = P.st_v[sbase + p];
-                L[j] = fast_log(be[j], logtab);
+                L[j] = fast_log2(be[j], logtab);
             }
         } else {
             mu[j] = mu0;
@@ -373,7 +374,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     const double d = x - mu[j];
                     const double bn = fma(gk.x * d, d, be[j]);
                     mu[j] = fma(d, gk.y, mu[j]);
-                    const double Ln = fast_log(bn, logtab);
+                    const double Ln = fast_log2(bn, logtab);
                     const double2 ca = s_ca[idx];
                     const double ell = fma(-0.5, Ln, fma(ca.y, L[j] - Ln, ca.x));
                     be[j] = bn;
@@ -431,7 +432,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 const int p = i + NT * j;
                 if (FULL || p < R) {
                     const double dm = v[j] - M;
-                    sum += fast_exp(dm, exptab);
+                    sum += fast_exp2(dm, exptab);
                     v[j] = dm;
                 }
             }
@@ -448,8 +449,8 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             }
             // ---- cell fix-ups and the scalar tail (A5-A8) -----------------
             // Two lanes per step: the owner of pB (r = R-1, recycled into the new CP cell:
-            // v = log H - log(1-H) + log(sum), prior statistics) and, for MERGE, the owner of
-            // pA (r = R-2 -> bucket: v = log(e_{R-2} + e_{R-1}) = mx + log(1 + exp(mn - mx))).
+            // v = lg H - lg(1-H) + lg(sum), prior statistics) and, for MERGE, the owner of
+            // pA (r = R-2 -> bucket: v = lg(e_{R-2} + e_{R-1}) = mx + lg(1 + 2^(mn - mx))).
             // Both run the same exp-then-log sequence on different operands (one SIMT pass).
             const int pB = (tmod + 1 == R) ? 0 : tmod + 1;
             const int pA = (pB + 1 == R) ? 0 : pB + 1;
@@ -462,27 +463,27 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             uint32_t fl = 0;
             if (ownB || ownA) {
                 const double earg = ownB ? (lprow[tmod] - M) : (mx == -INFINITY ? -INFINITY : mn - mx);
-                const double ee = fast_exp(earg, exptab);  // B: e_0 (r = 0 cell);  A: exp(mn - mx)
-                const double lg = fast_log(ownB ? sum : 1.0 + ee, logtab);
+                const double ee = fast_exp2(earg, exptab);  // B: e_0 (r = 0 cell);  A: exp(mn - mx)
+                const double lg = fast_log2(ownB ? sum : 1.0 + ee, logtab);
                 if (ownA && !ownB) set_v<J>(v, pA / NT, mx == -INFINITY ? -INFINITY : mx + lg);
                 if (ownB) {
-                    set_cell<J>(v, mu, be, L, pB / NT, logH - log1mH + lg, mu0, beta0, L0);
+                    set_cell<J>(v, mu, be, L, pB / NT, l2H - l2mH + lg, mu0, beta0, L0);
                     if (ownA) {  // r = R-1 and R-2 in one thread (tiny R): second pass
-                        const double u = fast_exp(mx == -INFINITY ? -INFINITY : mn - mx, exptab);
-                        set_v<J>(v, pA / NT, mx == -INFINITY ? -INFINITY : mx + fast_log(1.0 + u, logtab));
+                        const double u = fast_exp2(mx == -INFINITY ? -INFINITY : mn - mx, exptab);
+                        set_v<J>(v, pA / NT, mx == -INFINITY ? -INFINITY : mx + fast_log2(1.0 + u, logtab));
                     }
                     double Nt;
                     if (merge) {
                         Nt = lg;
                         pnew = (R == 2) ? 1.0 : ee * fast_rcp(sum);  // R(1) / (1 - R(0)), R(0) = H
                     } else {
-                        const double eB = fast_exp(dB, exptab);
-                        Nt = fast_log(sum - P.omH * eB, logtab);
+                        const double eB = fast_exp2(dB, exptab);
+                        Nt = fast_log2(sum - P.omH * eB, logtab);
                         pnew = ee * fast_rcp(sum - eB);
                     }
                     if (t > 0 && pnew > P.theta) fl |= 1u;
                     if (P.out_pnew) P.out_pnew[s * P.ld_o + tl] = pnew;
-                    if (P.out_logz) P.out_logz[s * P.ld_o + tl] = M + Nt - gs.n_prev;
+                    if (P.out_logz) P.out_logz[s * P.ld_o + tl] = LN2 * ((M - gs.n_prev) + Nt);
                     gs.n_prev = Nt;
                     if (!isfinite(x)) nonfinite = true;
                 }
@@ -519,13 +520,13 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             if (ownB && (EAGER || (fl & P.ev_mask))) {
                 int rstar;
                 if (merge) {
-                    // bucket (log(1-H) + mx + log(1 + exp(mn - mx))) vs the best growth slot
-                    // (log(1-H) + d_ex); ties -> the smaller run length (the growth slot)
+                    // bucket (lg(1-H) + mx + lg(1 + 2^(mn - mx))) vs the best growth slot
+                    // (lg(1-H) + d_ex); ties -> the smaller run length (the growth slot)
                     int pex = tmod - r_ex;
                     pex += (pex < 0) ? R : 0;
                     const double dex = r_ex >= 0 ? lprow[pex] - M : -INFINITY;
-                    const double u = fast_exp(mx == -INFINITY ? -INFINITY : mn - mx, exptab);
-                    const double bucket = mx == -INFINITY ? -INFINITY : mx + fast_log(1.0 + u, logtab);
+                    const double u = fast_exp2(mx == -INFINITY ? -INFINITY : mn - mx, exptab);
+                    const double bucket = mx == -INFINITY ? -INFINITY : mx + fast_log2(1.0 + u, logtab);
                     rstar = (r_ex < 0 || bucket > dex) ? R - 1 : r_ex + 1;
                 } else {
                     rstar = r_ex + 1;

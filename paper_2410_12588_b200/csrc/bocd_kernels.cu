@@ -41,7 +41,7 @@ int select_variant(int R, Variant* out) {
     return 0;
 }
 
-// Test hook: elementwise fast_log / fast_exp over device arrays.
+// Test hook: elementwise fast_log2 / fast_exp2 over device arrays.
 __global__ void fastmath_probe_kernel(int which, const double* in, double* out, int64_t n,
                                       const FastMathTables* tab) {
     __shared__ FastMathTables st;
@@ -49,7 +49,7 @@ __global__ void fastmath_probe_kernel(int which, const double* in, double* out, 
         reinterpret_cast<double*>(&st)[k] = reinterpret_cast<const double*>(tab)[k];
     __syncthreads();
     for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x)
-        out[k] = which == 0 ? fast_log(in[k], st.logtab) : fast_exp(in[k], st.exptab);
+        out[k] = which == 0 ? fast_log2(in[k], st.logtab) : fast_exp2(in[k], st.exptab);
 }
 
 int launch_fastmath_probe(int which, const double* in, double* out, int64_t n, const FastMathTables* tab,

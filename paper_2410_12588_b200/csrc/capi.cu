@@ -183,7 +183,7 @@ __global__ void drain_gather_kernel(SeriesScalars* scal, const EventRec* ev, int
 // Ring position order -> run-length order; log R = v - N_t.
 __global__ void posterior_kernel(const double* mu, const double* beta, const double* v,
                                  const SeriesScalars* scal, int64_t s0, int64_t count, int R, int64_t t,
-                                 double log1mH, double* logR_out, double* mu_out, double* beta_out) {
+                                 double l2mH, double* logR_out, double* mu_out, double* beta_out) {
     const int64_t n = count * int64_t(R);
     const int tm = int(t % R);
     for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
@@ -192,7 +192,7 @@ __global__ void posterior_kernel(const double* mu, const double* beta, const dou
         int p = tm - r;
         if (p < 0) p += R;
         const int64_t src = (s0 + i) * int64_t(R) + p;
-        if (logR_out) logR_out[k] = (v[src] + log1mH) - scal[s0 + i].n_prev;
+        if (logR_out) logR_out[k] = fbocd::LN2 * ((v[src] + l2mH) - scal[s0 + i].n_prev);
         if (mu_out) mu_out[k] = mu[src];
         if (beta_out) beta_out[k] = beta[src];
     }
@@ -350,14 +350,15 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
     falcon_bocd_predictive_constants(R, c.kappa0, c.alpha0, tc.data(), ta.data(), tg.data(), tk.data());
     std::vector<double2> ca(R), gk(R);
     {
-        // the device table folds the growth factor log(1-H) into c_r (bocd_kernel.cuh, A3)
-        const long double l1mh = log1pl(-(long double)c.hazard);
+        // base-2 units: the device table holds c_r / ln2 + log2(1-H) (bocd_kernel.cuh, A2-A3)
+        const long double l1mh = log2l(1.0L - (long double)c.hazard);
+        const long double inv_ln2 = 1.442695040888963407359924681001892137L;
         long double D = lgammal((long double)c.alpha0 + 0.5L) - lgammal((long double)c.alpha0);
         const long double two_pi = 6.283185307179586476925286766559005768L;
         for (int r = 0; r < R; ++r) {
             const long double kap = (long double)c.kappa0 + r;
             const long double cr = D - 0.5L * logl(two_pi * (kap + 1.0L) / kap);
-            ca[r] = make_double2((double)(cr + l1mh), ta[r]);
+            ca[r] = make_double2((double)(cr * inv_ln2 + l1mh), ta[r]);
             gk[r] = make_double2(tg[r], tk[r]);
             D = logl((long double)c.alpha0 + 0.5L * r) - D;
         }
@@ -399,7 +400,7 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
     if (e3 == cudaSuccess) {
         init_scalars_kernel<<<grid_for(S, 256), 256>>>(h->d_scal, dmu0, dbeta0, S);
         init_state_kernel<<<grid_for(int64_t(SR), 256), 256>>>(h->d_mu, h->d_beta, h->d_v, h->d_scal, S, R,
-                                                                 -std::log1p(-c.hazard));
+                                                                 -(double)log2l(1.0L - (long double)c.hazard));
         e3 = cudaGetLastError();
     }
     if (e3 == cudaSuccess) e3 = cudaDeviceSynchronize();
@@ -420,8 +421,8 @@ static int launch_update(falcon_bocd_t h, const double* x_dev, int64_t ld, int64
         std::memset(&P, 0, sizeof(P));
         P.R = c.R;
         P.S = c.n_series;
-        P.logH = std::log(c.hazard);
-        P.log1mH = std::log1p(-c.hazard);
+        P.l2H = (double)log2l((long double)c.hazard);
+        P.l2mH = (double)log2l(1.0L - (long double)c.hazard);
         P.omH = 1.0 - c.hazard;
         P.theta = c.threshold;
         P.alpha0 = c.alpha0;
@@ -638,7 +639,7 @@ int falcon_bocd_read_posterior(falcon_bocd_t h, int64_t s0, int64_t count, doubl
         dst[k] = is_device_ptr(outs[k]) ? outs[k] : tmp + k * n;
     }
     posterior_kernel<<<grid_for(int64_t(n), 256), 256, 0, st>>>(h->d_mu, h->d_beta, h->d_v, h->d_scal, s0, count, R,
-                                                                h->t, std::log1p(-h->cfg.hazard), dst[0], dst[1],
+                                                                h->t, (double)log2l(1.0L - (long double)h->cfg.hazard), dst[0], dst[1],
                                                                 dst[2]);
     cudaError_t e = cudaGetLastError();
     for (int k = 0; k < 3 && e == cudaSuccess; ++k)
