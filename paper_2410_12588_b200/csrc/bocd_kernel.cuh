@@ -240,12 +240,10 @@ __device__ __forceinline__ double ord_hi_val(int oh) {
 template <int NT, int J, bool FULL, bool TAB2, bool EAGER, int SPB, int MINB>
 __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParams P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ FastMathTables s_fm_static;  // static: table lookups use immediate addresses
     const int R = FULL ? NT * J : P.R;
     const int RT = TAB2 ? 2 * R : R;
     double2* s_ca = reinterpret_cast<double2*>(smem_raw);
     double2* s_gk = s_ca + RT;
-    FastMathTables* s_fm = &s_fm_static;
     unsigned char* gbase = reinterpret_cast<unsigned char*>(s_gk + RT);
 
     for (int k = threadIdx.x; k < RT; k += blockDim.x) {
@@ -253,11 +251,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         s_ca[k] = P.tab_ca[r];
         s_gk[k] = P.tab_gk[r];
     }
-    {
-        const double* src = reinterpret_cast<const double*>(P.fm);
-        double* dst = reinterpret_cast<double*>(s_fm);
-        for (int k = threadIdx.x; k < int(sizeof(FastMathTables) / 8); k += blockDim.x) dst[k] = src[k];
-    }
+    load_fastmath(P.fm);
     const int g = threadIdx.x / NT;
     const int i = threadIdx.x % NT;
     const int lane = threadIdx.x & 31;
@@ -275,8 +269,6 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     }
     __syncthreads();
     if (!active) return;
-    const double2* logtab = s_fm->logtab;
-    const double* exptab = s_fm->exptab;
 
     // Prefetch tile 0 (TMA) as early as possible.
     if (i == 0 && ntiles > 0 && tile_tma_ok(P, 0)) issue_tile_tma<NT>(gs, xrow, 0, P.T);
@@ -299,7 +291,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         const bool ok = sc.beta0 >= 2.2250738585072014e-308 && sc.beta0 < 1e300 && isfinite(sc.mu0);
         gs.mu0 = sc.mu0;
         gs.beta0 = ok ? sc.beta0 : 1.0;
-        gs.L0 = fast_log2(gs.beta0, logtab);
+        gs.L0 = fast_log2(gs.beta0);
         gs.n_prev = sc.n_prev;
         gs.map_prev = sc.map_prev;
         gs.ev_count = sc.ev_count;
@@ -320,7 +312,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 mu[j] = P.st_mu[sbase + p];
                 be[j] = P.st_beta[sbase + p];
                 v[j] = P.st_v[sbase + p];
-                L[j] = fast_log2(be[j], logtab);
+                L[j] = fast_log2(be[j]);
             }
         } else {
             mu[j] = mu0;
@@ -374,7 +366,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     const double d = x - mu[j];
                     const double bn = fma(gk.x * d, d, be[j]);
                     mu[j] = fma(d, gk.y, mu[j]);
-                    const double Ln = fast_log2(bn, logtab);
+                    const double Ln = fast_log2(bn);
                     const double2 ca = s_ca[idx];
                     const double ell = fma(-0.5, Ln, fma(ca.y, L[j] - Ln, ca.x));
                     be[j] = bn;
@@ -431,9 +423,8 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             for (int j = 0; j < J; ++j) {
                 const int p = i + NT * j;
                 if (FULL || p < R) {
-                    const double dm = v[j] - M;
-                    sum += fast_exp2(dm, exptab);
-                    v[j] = dm;
+                    v[j] -= M;
+                    sum += fast_exp2(v[j]);
                 }
             }
 #pragma unroll
@@ -463,22 +454,22 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             uint32_t fl = 0;
             if (ownB || ownA) {
                 const double earg = ownB ? (lprow[tmod] - M) : (mx == -INFINITY ? -INFINITY : mn - mx);
-                const double ee = fast_exp2(earg, exptab);  // B: e_0 (r = 0 cell);  A: exp(mn - mx)
-                const double lg = fast_log2(ownB ? sum : 1.0 + ee, logtab);
+                const double ee = fast_exp2(earg);  // B: e_0 (r = 0 cell);  A: exp(mn - mx)
+                const double lg = fast_log2(ownB ? sum : 1.0 + ee);
                 if (ownA && !ownB) set_v<J>(v, pA / NT, mx == -INFINITY ? -INFINITY : mx + lg);
                 if (ownB) {
                     set_cell<J>(v, mu, be, L, pB / NT, l2H - l2mH + lg, mu0, beta0, L0);
                     if (ownA) {  // r = R-1 and R-2 in one thread (tiny R): second pass
-                        const double u = fast_exp2(mx == -INFINITY ? -INFINITY : mn - mx, exptab);
-                        set_v<J>(v, pA / NT, mx == -INFINITY ? -INFINITY : mx + fast_log2(1.0 + u, logtab));
+                        const double u = fast_exp2(mx == -INFINITY ? -INFINITY : mn - mx);
+                        set_v<J>(v, pA / NT, mx == -INFINITY ? -INFINITY : mx + fast_log2(1.0 + u));
                     }
                     double Nt;
                     if (merge) {
                         Nt = lg;
                         pnew = (R == 2) ? 1.0 : ee * fast_rcp(sum);  // R(1) / (1 - R(0)), R(0) = H
                     } else {
-                        const double eB = fast_exp2(dB, exptab);
-                        Nt = fast_log2(sum - P.omH * eB, logtab);
+                        const double eB = fast_exp2(dB);
+                        Nt = fast_log2(sum - P.omH * eB);
                         pnew = ee * fast_rcp(sum - eB);
                     }
                     if (t > 0 && pnew > P.theta) fl |= 1u;
@@ -525,8 +516,8 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     int pex = tmod - r_ex;
                     pex += (pex < 0) ? R : 0;
                     const double dex = r_ex >= 0 ? lprow[pex] - M : -INFINITY;
-                    const double u = fast_exp2(mx == -INFINITY ? -INFINITY : mn - mx, exptab);
-                    const double bucket = mx == -INFINITY ? -INFINITY : mx + fast_log2(1.0 + u, logtab);
+                    const double u = fast_exp2(mx == -INFINITY ? -INFINITY : mn - mx);
+                    const double bucket = mx == -INFINITY ? -INFINITY : mx + fast_log2(1.0 + u);
                     rstar = (r_ex < 0 || bucket > dex) ? R - 1 : r_ex + 1;
                 } else {
                     rstar = r_ex + 1;

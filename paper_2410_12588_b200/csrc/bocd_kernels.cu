@@ -1,4 +1,7 @@
 // bocd_kernels.cu — instantiations of the resident BOCD kernel and the variant table.
+#include <cstdlib>
+#include <cstring>
+
 #include "bocd_kernel.cuh"
 #include "bocd_variants.h"
 
@@ -23,6 +26,13 @@ static void make_variant(Variant* out) {
 // cells) for any other 2 <= R <= 4096.  Each variant has a lazy-MAP and an
 // EAGER-MAP kernel (bocd_kernel.cuh).
 int select_variant(int R, Variant* out) {
+    // Tuning hook (bench / profiling only): alternative shapes for R = 1024.
+    if (R == 1024) {
+        const char* ev = getenv("FALCON_BOCD_VARIANT");
+        if (ev && strcmp(ev, "256x4s3") == 0) { make_variant<256, 4, true, true, 3, 1>(out); return 0; }
+        if (ev && strcmp(ev, "128x8s5") == 0) { make_variant<128, 8, true, true, 5, 1>(out); return 0; }
+        if (ev && strcmp(ev, "128x8s4") == 0) { make_variant<128, 8, true, true, 4, 1>(out); return 0; }
+    }
     switch (R) {
         case 256: make_variant<32, 8, true, true, 8, 2>(out); return 0;
         case 512: make_variant<64, 8, true, true, 4, 2>(out); return 0;
@@ -44,12 +54,10 @@ int select_variant(int R, Variant* out) {
 // Test hook: elementwise fast_log2 / fast_exp2 over device arrays.
 __global__ void fastmath_probe_kernel(int which, const double* in, double* out, int64_t n,
                                       const FastMathTables* tab) {
-    __shared__ FastMathTables st;
-    for (int k = threadIdx.x; k < int(sizeof(FastMathTables) / 8); k += blockDim.x)
-        reinterpret_cast<double*>(&st)[k] = reinterpret_cast<const double*>(tab)[k];
+    load_fastmath(tab);
     __syncthreads();
     for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x)
-        out[k] = which == 0 ? fast_log2(in[k], st.logtab) : fast_exp2(in[k], st.exptab);
+        out[k] = which == 0 ? fast_log2(in[k]) : fast_exp2(in[k]);
 }
 
 int launch_fastmath_probe(int which, const double* in, double* out, int64_t n, const FastMathTables* tab,

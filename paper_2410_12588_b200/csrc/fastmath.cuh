@@ -59,10 +59,22 @@ inline void fill_fastmath_tables(FastMathTables* t) {
     for (int j = 0; j < kExpTab; ++j) t->exptab[j] = (double)exp2l((long double)j / 64.0L);
 }
 
-__device__ __forceinline__ double fast_log2(double x, const double2* __restrict__ logtab) {
+// The tables live in static shared memory, referenced by name so that every lookup
+// is one LDS with an immediate base (each kernel loads them once with load_fastmath).
+static __shared__ FastMathTables g_fm;
+
+__device__ __forceinline__ void load_fastmath(const FastMathTables* __restrict__ src) {
+    const double* s = reinterpret_cast<const double*>(src);
+    double* d = reinterpret_cast<double*>(&g_fm);
+    for (int k = threadIdx.x; k < int(sizeof(FastMathTables) / 8); k += blockDim.x) d[k] = s[k];
+}
+
+__device__ __forceinline__ double fast_log2(double x) {
     const int hi = __double2hiint(x);
-    const int tb = hi + 0x00196000;          // (hi - 0x3FE6A000) + (1024 << 20): biased k in bits 20..31
-    const double2 t = logtab[(tb >> 13) & (kLogTab - 1)];  // top 7 mantissa bits of (ix - OFF)
+    const int tb = hi + 0x00196000;  // (hi - 0x3FE6A000) + (1024 << 20): biased k in bits 20..31
+    // entry (tb >> 13) & 127 (top 7 mantissa bits of ix - OFF), as a byte offset
+    const double2 t = *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(g_fm.logtab) +
+                                                       ((tb >> 9) & ((kLogTab - 1) << 4)));
     // r = z * invc - 1 with z = x / 2^k: the exact power-of-two scaling is folded into invc
     const double invs =
         __hiloint2double(__double2hiint(t.x) + 0x40000000 - (tb & 0xFFF00000), __double2loint(t.x));
@@ -76,14 +88,11 @@ __device__ __forceinline__ double fast_log2(double x, const double2* __restrict_
     return kd + fma(r, p, t.y);
 }
 
-__device__ __forceinline__ double fast_exp2(double x, const double* __restrict__ exptab) {
-    // clamp x >= -1021 (also maps -inf / NaN patterns) on the integer pipe
-    int xh = __double2hiint(x);
-    int xl = __double2loint(x);
-    const bool clamp = static_cast<unsigned>(xh) > 0xC08FE800u;  // x < -1021
-    xh = clamp ? 0xC08FE800 : xh;
-    xl = clamp ? 0 : xl;
-    const double xc = __hiloint2double(xh, xl);
+__device__ __forceinline__ double fast_exp2(double x) {
+    // clamp x >= -1021 on the integer pipe: only the high word is clamped (a clamped
+    // argument keeps stray low mantissa bits: -1021 - 2^-33 at most, irrelevant)
+    const int xh = int(min(unsigned(__double2hiint(x)), 0xC08FE800u));  // -inf / NaN patterns too
+    const double xc = __hiloint2double(xh, __double2loint(x));
     constexpr double SHIFT = 6755399441055744.0;  // 1.5 * 2^52
     const double zf = fma(xc, 64.0, SHIFT);        // round(64 x) in the low word
     const int ki = __double2loint(zf);
@@ -94,9 +103,11 @@ __device__ __forceinline__ double fast_exp2(double x, const double* __restrict__
     p = fma(p, r, 0.24022650695910072);
     p = fma(p, r, LN2);
     const double q = p * r;
-    const double T = exptab[ki & (kExpTab - 1)];
-    const int e = ki >> 6;
-    const double Ts = __hiloint2double(__double2hiint(T) + e * 1048576, __double2loint(T));
+    const double T =
+        *reinterpret_cast<const double*>(reinterpret_cast<const char*>(g_fm.exptab) + ((ki << 3) & 0x1F8));
+    int th;  // high word of T * 2^(ki >> 6): one IMAD
+    asm("mad.lo.s32 %0, %1, 1048576, %2;" : "=r"(th) : "r"(ki >> 6), "r"(__double2hiint(T)));
+    const double Ts = __hiloint2double(th, __double2loint(T));
     return fma(Ts, q, Ts);
 }
 
