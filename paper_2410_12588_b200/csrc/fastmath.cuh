@@ -63,6 +63,14 @@ inline void fill_fastmath_tables(FastMathTables* t) {
 // is one LDS with an immediate base (each kernel loads them once with load_fastmath).
 static __shared__ FastMathTables g_fm;
 
+// Polynomial / conversion constants in constant memory: DFMA / DADD read them as
+// constant-bank operands instead of re-materialising 64-bit immediates in registers.
+static __constant__ double c_fm[16] = {
+    -0.2404491734814939,   0.28853900817779266,  -0.36067376022224085, 0.4808983469629878,   // log2 P
+    -0.7213475204444817,   1.4426950408889634,   4503599627371520.0,   6755399441055744.0,   // .., 1/ln2, 2^52+1024, 1.5*2^52
+    0.0013333558146428443, 0.009618129107628477, 0.05550410866482158,  0.24022650695910072,  // exp2 poly
+    0.6931471805599453,    64.0,                 -0.015625,            0.0};
+
 __device__ __forceinline__ void load_fastmath(const FastMathTables* __restrict__ src) {
     const double* s = reinterpret_cast<const double*>(src);
     double* d = reinterpret_cast<double*>(&g_fm);
@@ -79,12 +87,12 @@ __device__ __forceinline__ double fast_log2(double x) {
     const double invs =
         __hiloint2double(__double2hiint(t.x) + 0x40000000 - (tb & 0xFFF00000), __double2loint(t.x));
     const double r = fma(x, invs, -1.0);
-    const double kd = __hiloint2double(0x43300000, int(unsigned(tb) >> 20)) - 4503599627371520.0;  // 2^52+1024
-    double p = fma(r, -0.2404491734814939, 0.28853900817779266);
-    p = fma(p, r, -0.36067376022224085);
-    p = fma(p, r, 0.4808983469629878);
-    p = fma(p, r, -0.7213475204444817);
-    p = fma(p, r, INV_LN2);
+    const double kd = __hiloint2double(0x43300000, int(unsigned(tb) >> 20)) - c_fm[6];  // k (2^52 + 1024 bias)
+    double p = fma(r, c_fm[0], c_fm[1]);
+    p = fma(p, r, c_fm[2]);
+    p = fma(p, r, c_fm[3]);
+    p = fma(p, r, c_fm[4]);
+    p = fma(p, r, c_fm[5]);
     return kd + fma(r, p, t.y);
 }
 
@@ -93,15 +101,14 @@ __device__ __forceinline__ double fast_exp2(double x) {
     // argument keeps stray low mantissa bits: -1021 - 2^-33 at most, irrelevant)
     const int xh = int(min(unsigned(__double2hiint(x)), 0xC08FE800u));  // -inf / NaN patterns too
     const double xc = __hiloint2double(xh, __double2loint(x));
-    constexpr double SHIFT = 6755399441055744.0;  // 1.5 * 2^52
-    const double zf = fma(xc, 64.0, SHIFT);        // round(64 x) in the low word
+    const double zf = fma(xc, c_fm[13], c_fm[7]);  // round(64 x) in the low word (1.5 * 2^52 shift)
     const int ki = __double2loint(zf);
-    const double kd = zf - SHIFT;
-    const double r = fma(kd, -0.015625, xc);      // exact: |r| <= 1/128
-    double p = fma(r, 0.0013333558146428443, 0.009618129107628477);
-    p = fma(p, r, 0.05550410866482158);
-    p = fma(p, r, 0.24022650695910072);
-    p = fma(p, r, LN2);
+    const double kd = zf - c_fm[7];
+    const double r = fma(kd, c_fm[14], xc);  // exact: |r| <= 1/128
+    double p = fma(r, c_fm[8], c_fm[9]);
+    p = fma(p, r, c_fm[10]);
+    p = fma(p, r, c_fm[11]);
+    p = fma(p, r, c_fm[12]);
     const double q = p * r;
     const double T =
         *reinterpret_cast<const double*>(reinterpret_cast<const char*>(g_fm.exptab) + ((ki << 3) & 0x1F8));
