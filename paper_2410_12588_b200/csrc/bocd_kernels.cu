@@ -69,4 +69,9 @@ int launch_fastmath_probe(int which, const double* in, double* out, int64_t n, c
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
+// The constant bank is per translation unit: this is the copy the kernels above read.
+int upload_fastmath_constants() {
+    return cudaMemcpyToSymbol(c_fm, kFastMathConstants, sizeof(kFastMathConstants)) == cudaSuccess ? 0 : -1;
+}
+
 }  // namespace fbocd

@@ -21,6 +21,7 @@ struct Variant {
 int select_variant(int R, Variant* out);
 
 struct FastMathTables;
+int upload_fastmath_constants();  // once per device, before any kernel that uses fast_log2/exp2
 int launch_fastmath_probe(int which, const double* in, double* out, int64_t n, const FastMathTables* tab,
                           cudaStream_t st);
 

@@ -340,6 +340,10 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
         h->err = "shared memory footprint too large";
         return bail(FALCON_EINVAL);
     }
+    if (fbocd::upload_fastmath_constants() != 0) {
+        h->err = "cudaMemcpyToSymbol(c_fm) failed";
+        return bail(FALCON_ECUDA);
+    }
     for (const void* fn : {h->var.fn, h->var.fn_eager}) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(h->smem));
         if (e != cudaSuccess) return bail(cuda_fail(h, e, "cudaFuncSetAttribute"));
@@ -699,6 +703,7 @@ int falcon_bocd_debug_fastmath(int32_t which, const double* in_dev, double* out_
     fbocd::fill_fastmath_tables(&fmt);
     fbocd::FastMathTables* d = nullptr;
     cudaStream_t st = (cudaStream_t)stream;
+    if (fbocd::upload_fastmath_constants() != 0) return FALCON_ECUDA;
     if (cudaMalloc((void**)&d, sizeof(fmt)) != cudaSuccess) return FALCON_ENOMEM;
     cudaError_t e = cudaMemcpyAsync(d, &fmt, sizeof(fmt), cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess && fbocd::launch_fastmath_probe(which, in_dev, out_dev, n, d, st) != 0) e = cudaErrorLaunchFailure;

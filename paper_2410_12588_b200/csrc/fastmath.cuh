@@ -63,9 +63,12 @@ inline void fill_fastmath_tables(FastMathTables* t) {
 // is one LDS with an immediate base (each kernel loads them once with load_fastmath).
 static __shared__ FastMathTables g_fm;
 
-// Polynomial / conversion constants in constant memory: DFMA / DADD read them as
-// constant-bank operands instead of re-materialising 64-bit immediates in registers.
-static __constant__ double c_fm[16] = {
+// Polynomial / conversion constants in constant memory, uploaded at handle creation
+// (falcon_bocd_create -> upload_fastmath_constants): not known to the compiler, so DFMA /
+// DADD read them as constant-bank operands instead of re-materialising 64-bit immediates
+// in registers every step.
+static __constant__ double c_fm[16];
+static const double kFastMathConstants[16] = {
     -0.2404491734814939,   0.28853900817779266,  -0.36067376022224085, 0.4808983469629878,   // log2 P
     -0.7213475204444817,   1.4426950408889634,   4503599627371520.0,   6755399441055744.0,   // .., 1/ln2, 2^52+1024, 1.5*2^52
     0.0013333558146428443, 0.009618129107628477, 0.05550410866482158,  0.24022650695910072,  // exp2 poly
