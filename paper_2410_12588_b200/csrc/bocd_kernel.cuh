@@ -85,6 +85,7 @@ struct KParams {
     double* out_logz;
     int64_t ld_o;
     int tma_ok;  // x base 16-B aligned and ld even
+    int dbg;     // profiling experiments only (FALCON_BOCD_DEBUG): 1 no tail, 2 no barriers
 };
 
 template <int NT>
@@ -141,7 +142,8 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
 }
 
 template <int NT>
-__device__ __forceinline__ void group_sync(int g) {
+__device__ __forceinline__ void group_sync(int g, int dbg = 0) {
+    if (dbg == 2) return;
     if constexpr (NT == 32) {
         __syncwarp();
     } else {
@@ -404,7 +406,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     gs.red1[w] = EAGER ? key : 0ull;
                     gs.redh[w] = mh;
                 }
-                group_sync<NT>(g);
+                group_sync<NT>(g, P.dbg);
 #pragma unroll
                 for (int ww = 0; ww < NT / 32; ++ww) {
                     mh = max(mh, gs.redh[ww]);
@@ -431,7 +433,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
             if constexpr (NT > 32) {
                 if (lane == 0) gs.red2[w] = sum;
-                group_sync<NT>(g);
+                group_sync<NT>(g, P.dbg);
                 sum = gs.red2[0];
 #pragma unroll
                 for (int ww = 1; ww < NT / 32; ++ww) sum += gs.red2[ww];
@@ -452,7 +454,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             const double mx = fmax(dA, dB), mn = fmin(dA, dB);
             double pnew = 0.0;
             uint32_t fl = 0;
-            if (ownB || ownA) {
+            if ((ownB || ownA) && P.dbg != 1) {
                 const double earg = ownB ? (lprow[tmod] - M) : (mx == -INFINITY ? -INFINITY : mn - mx);
                 const double ee = fast_exp2(earg);  // B: e_0 (r = 0 cell);  A: exp(mn - mx)
                 const double lg = fast_log2(ownB ? sum : 1.0 + ee);

@@ -7,6 +7,7 @@
 // kernels.  Every computing entry point launches CUDA kernels; there is no CPU
 // fallback.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -453,6 +454,10 @@ static int launch_update(falcon_bocd_t h, const double* x_dev, int64_t ld, int64
         P.out_logz = ologz ? ologz + done : nullptr;
         P.ld_o = ld_o;
         P.tma_ok = ((reinterpret_cast<uintptr_t>(P.x) & 15u) == 0) && ((ld & 1) == 0);
+        {
+            const char* dbg = getenv("FALCON_BOCD_DEBUG");  // profiling experiments only
+            P.dbg = dbg ? atoi(dbg) : 0;
+        }
         const int64_t grid = (c.n_series + h->var.spb - 1) / h->var.spb;
         void* args[] = {&P};
         // r* every step only when it is an output (per-step MAP, MAPRESET events); otherwise
