@@ -62,7 +62,7 @@ struct EventRec {  // 32 B, series id implicit
 struct KParams {
     int R;
     int64_t S;
-    double l2H, l2mH, omH, theta, alpha0, prior_cov;  // l2H = log2 H, l2mH = log2(1-H)
+    double l2H, l2mH, omH, theta, l2theta, alpha0, prior_cov;  // l2H = log2 H, l2mH = log2(1-H)
     int mode;  // 0 MERGE, 1 DROP
     int prior_first_obs;
     uint32_t ev_mask;
@@ -94,6 +94,7 @@ struct __align__(16) GroupSmem {
     unsigned long long red1[NT / 32 > 0 ? NT / 32 : 1];
     double red2[NT / 32 > 0 ? NT / 32 : 1];
     int redh[NT / 32 > 0 ? NT / 32 : 1];
+    unsigned long long red3[NT / 32 > 0 ? NT / 32 : 1];  // on-demand argmax (event steps)
     double mu0, beta0, L0, n_prev;
     int map_prev, ev_count, flags, pad;
     unsigned long long mbar[2];
@@ -193,35 +194,6 @@ __host__ __device__ constexpr size_t table_bytes(int R, bool tab2) {
     return size_t(R) * (tab2 ? 2 : 1) * 2 * sizeof(double2);
 }
 
-// Writes one cell of the register state (dynamic index j, warp-uniform in practice:
-// a jump over J cases instead of J predicated selects per array).
-template <int J>
-__device__ __forceinline__ void set_cell(double (&v)[J], double (&mu)[J], double (&be)[J], double (&L)[J],
-                                         int j, double vv, double m, double b, double l) {
-#define FBOCD_SET(k)                      \
-    case k:                               \
-        if constexpr (J > k) {            \
-            v[k] = vv;                    \
-            mu[k] = m;                    \
-            be[k] = b;                    \
-            L[k] = l;                     \
-        }                                 \
-        break;
-    switch (j) { FBOCD_SET(0) FBOCD_SET(1) FBOCD_SET(2) FBOCD_SET(3) FBOCD_SET(4) FBOCD_SET(5) FBOCD_SET(6) FBOCD_SET(7) }
-#undef FBOCD_SET
-}
-template <int J>
-__device__ __forceinline__ void set_v(double (&v)[J], int j, double vv) {
-#define FBOCD_SETV(k)            \
-    case k:                      \
-        if constexpr (J > k) {   \
-            v[k] = vv;           \
-        }                        \
-        break;
-    switch (j) { FBOCD_SETV(0) FBOCD_SETV(1) FBOCD_SETV(2) FBOCD_SETV(3) FBOCD_SETV(4) FBOCD_SETV(5) FBOCD_SETV(6) FBOCD_SETV(7) }
-#undef FBOCD_SETV
-}
-
 // order-preserving signed int of the high word of a double (for the shift M)
 __device__ __forceinline__ int ord_hi(double v) {
     const int h = __double2hiint(v);
@@ -229,6 +201,37 @@ __device__ __forceinline__ int ord_hi(double v) {
 }
 __device__ __forceinline__ double ord_hi_val(int oh) {
     return __hiloint2double(oh >= 0 ? oh : (oh ^ 0x7FFFFFFF), 0);
+}
+
+// Writes one cell of the register state under a lane predicate.  j is group-uniform,
+// so the switch never diverges; the body is a handful of predicated moves.
+template <int J>
+__device__ __forceinline__ void set_cell_pred(double (&v)[J], double (&mu)[J], double (&be)[J], double (&L)[J],
+                                              int j, bool pred, double vv, double m, double b, double l) {
+#define FBOCD_SET(k)                      \
+    case k:                               \
+        if constexpr (J > k) {            \
+            if (pred) {                   \
+                v[k] = vv;                \
+                mu[k] = m;                \
+                be[k] = b;                \
+                L[k] = l;                 \
+            }                             \
+        }                                 \
+        break;
+    switch (j) { FBOCD_SET(0) FBOCD_SET(1) FBOCD_SET(2) FBOCD_SET(3) FBOCD_SET(4) FBOCD_SET(5) FBOCD_SET(6) FBOCD_SET(7) }
+#undef FBOCD_SET
+}
+template <int J>
+__device__ __forceinline__ void set_v_pred(double (&v)[J], int j, bool pred, double vv) {
+#define FBOCD_SETV(k)            \
+    case k:                      \
+        if constexpr (J > k) {   \
+            if (pred) v[k] = vv; \
+        }                        \
+        break;
+    switch (j) { FBOCD_SETV(0) FBOCD_SETV(1) FBOCD_SETV(2) FBOCD_SETV(3) FBOCD_SETV(4) FBOCD_SETV(5) FBOCD_SETV(6) FBOCD_SETV(7) }
+#undef FBOCD_SETV
 }
 
 // ---------------------------------------------------------------------------
@@ -301,6 +304,8 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     }
     group_sync<NT>(g);
     const double mu0 = gs.mu0, beta0 = gs.beta0, L0 = gs.L0;
+    double n_prev = gs.n_prev;  // per-series scalars are group-uniform registers
+    int map_prev = gs.map_prev, ev_count = gs.ev_count;
 #pragma unroll
     for (int j = 0; j < J; ++j) {
         const int p = i + NT * j;
@@ -440,111 +445,117 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             } else {
                 group_sync<NT>(g);
             }
-            // ---- cell fix-ups and the scalar tail (A5-A8) -----------------
-            // Two lanes per step: the owner of pB (r = R-1, recycled into the new CP cell:
-            // v = lg H - lg(1-H) + lg(sum), prior statistics) and, for MERGE, the owner of
-            // pA (r = R-2 -> bucket: v = lg(e_{R-2} + e_{R-1}) = mx + lg(1 + 2^(mn - mx))).
-            // Both run the same exp-then-log sequence on different operands (one SIMT pass).
+            // ---- the scalar tail (A5-A8), computed UNIFORMLY by every thread -------
+            // (no lane-divergent latency chain between two barriers; the two cells
+            // that change identity are then written by their owners through a
+            // warp-uniform switch with a lane predicate)
+            //   recycled cell pB (r = R-1) -> new CP cell: v = lg H - lg(1-H) + lg(sum), prior stats
+            //   MERGE: cell pA (r = R-2) -> bucket: v = lg(2^dA + 2^dB) = mx + lg(1 + 2^(mn - mx))
             const int pB = (tmod + 1 == R) ? 0 : tmod + 1;
             const int pA = (pB + 1 == R) ? 0 : pB + 1;
-            const int iB = pB % NT;
-            const bool ownB = iB == i;
-            const bool ownA = merge && ((pA % NT) == i);
-            const double dA = lprow[pA] - M, dB = lprow[pB] - M;
+            const double dA = lprow[pA] - M, dB = lprow[pB] - M, d0 = lprow[tmod] - M;
             const double mx = fmax(dA, dB), mn = fmin(dA, dB);
-            double pnew = 0.0;
-            uint32_t fl = 0;
-            if ((ownB || ownA) && P.dbg != 1) {
-                const double earg = ownB ? (lprow[tmod] - M) : (mx == -INFINITY ? -INFINITY : mn - mx);
-                const double ee = fast_exp2(earg);  // B: e_0 (r = 0 cell);  A: exp(mn - mx)
-                const double lg = fast_log2(ownB ? sum : 1.0 + ee);
-                if (ownA && !ownB) set_v<J>(v, pA / NT, mx == -INFINITY ? -INFINITY : mx + lg);
-                if (ownB) {
-                    set_cell<J>(v, mu, be, L, pB / NT, l2H - l2mH + lg, mu0, beta0, L0);
-                    if (ownA) {  // r = R-1 and R-2 in one thread (tiny R): second pass
-                        const double u = fast_exp2(mx == -INFINITY ? -INFINITY : mn - mx);
-                        set_v<J>(v, pA / NT, mx == -INFINITY ? -INFINITY : mx + fast_log2(1.0 + u));
-                    }
-                    double Nt;
-                    if (merge) {
-                        Nt = lg;
-                        pnew = (R == 2) ? 1.0 : ee * fast_rcp(sum);  // R(1) / (1 - R(0)), R(0) = H
-                    } else {
-                        const double eB = fast_exp2(dB);
-                        Nt = fast_log2(sum - P.omH * eB);
-                        pnew = ee * fast_rcp(sum - eB);
-                    }
-                    if (t > 0 && pnew > P.theta) fl |= 1u;
-                    if (P.out_pnew) P.out_pnew[s * P.ld_o + tl] = pnew;
-                    if (P.out_logz) P.out_logz[s * P.ld_o + tl] = LN2 * ((M - gs.n_prev) + Nt);
-                    gs.n_prev = Nt;
-                    if (!isfinite(x)) nonfinite = true;
-                }
+            // one log stream for two values: lanes 0-15 lg(sum), lanes 16-31 lg(1 + u)
+            const double u = fast_exp2(mx == -INFINITY ? -INFINITY : mn - mx);
+            const double lgx = fast_log2(lane >= 16 ? 1.0 + u : sum);
+            const double lg_sum = __shfl_sync(0xffffffffu, lgx, 0);
+            const double lb = __shfl_sync(0xffffffffu, lgx, 16);
+            const double vb = (mx == -INFINITY) ? -INFINITY : mx + lb;
+            double Nt, eB = 0.0;
+            bool prob;
+            if (merge) {
+                Nt = lg_sum;
+                // p_new = R(1) / (1 - R(0)) = 2^(d0 - lg sum)  (R(0) = H exactly; R = 2: p_new = 1)
+                prob = (R == 2) ? (1.0 > P.theta) : (d0 - lg_sum > P.l2theta);
+            } else {
+                eB = fast_exp2(dB);
+                Nt = fast_log2(sum - P.omH * eB);
+                prob = fast_exp2(d0) > P.theta * (sum - eB);  // p_new = e_0 / (sum - e_{R-1})
             }
-            // ---- MAP run length r* (A7) ---------------------------------
+            uint32_t fl = (t > 0 && prob) ? 1u : 0u;
+            {
+                const int jB = pB / NT, jA = pA / NT;
+                set_cell_pred<J>(v, mu, be, L, jB, (pB % NT) == i, l2H - l2mH + lg_sum, mu0, beta0, L0);
+                if (merge) set_v_pred<J>(v, jA, (pA % NT) == i, vb);
+            }
+            if (!isfinite(x)) nonfinite = true;
+            // ---- MAP run length r* (A7): eager (key reduced at barrier A) or on demand ----
             int r_ex = -1;
             if constexpr (EAGER) {
                 if (key != 0ull) {
                     const long long sk = static_cast<long long>(key ^ 0x8000000000000000ull);
                     r_ex = int(0xFFF - (sk & 0xFFF));
                 }
-            } else {
-                if ((iB >> 5) == w) {  // warp-uniform: the warp of the tail lane
-                    const int need = __shfl_sync(0xffffffffu, int(fl & P.ev_mask), iB & 31);
-                    if (need) {  // an event at this step: reduce the argmax from the lp row
-                        unsigned long long kb = 0ull;
-                        for (int qq = lane; qq < R; qq += 32) {
-                            int r = tmod - qq;
-                            r += (r < 0) ? R : 0;
-                            const unsigned long long kk = argmax_key(lprow[qq], r);
-                            kb = (r <= r_elig && kk > kb) ? kk : kb;
-                        }
-                        const unsigned hi = unsigned(kb >> 32);
-                        const unsigned hmax = __reduce_max_sync(0xffffffffu, hi);
-                        const unsigned lmax = __reduce_max_sync(0xffffffffu, hi == hmax ? unsigned(kb) : 0u);
-                        kb = (static_cast<unsigned long long>(hmax) << 32) | lmax;
-                        if (kb != 0ull) {
-                            const long long sk = static_cast<long long>(kb ^ 0x8000000000000000ull);
-                            r_ex = int(0xFFF - (sk & 0xFFF));
-                        }
+            } else if (fl & P.ev_mask) {  // group-uniform: an event at this step
+                unsigned long long kb = 0ull;
+#pragma unroll
+                for (int j = 0; j < J; ++j) {
+                    const int p = i + NT * j;
+                    if (FULL || p < R) {
+                        int r = tmod - p;
+                        r += (r < 0) ? R : 0;
+                        const unsigned long long kk = argmax_key(lprow[p], r);
+                        kb = (r <= r_elig && kk > kb) ? kk : kb;
                     }
                 }
+                const unsigned hi = unsigned(kb >> 32);
+                const unsigned hmax = __reduce_max_sync(0xffffffffu, hi);
+                const unsigned lmax = __reduce_max_sync(0xffffffffu, hi == hmax ? unsigned(kb) : 0u);
+                kb = (static_cast<unsigned long long>(hmax) << 32) | lmax;
+                if constexpr (NT > 32) {
+                    if (lane == 0) gs.red3[w] = kb;
+                    group_sync<NT>(g);
+#pragma unroll
+                    for (int ww = 0; ww < NT / 32; ++ww) {
+                        const unsigned long long o = gs.red3[ww];
+                        kb = o > kb ? o : kb;
+                    }
+                }
+                if (kb != 0ull) {
+                    const long long sk = static_cast<long long>(kb ^ 0x8000000000000000ull);
+                    r_ex = int(0xFFF - (sk & 0xFFF));
+                }
             }
-            if (ownB && (EAGER || (fl & P.ev_mask))) {
+            if (EAGER || (fl & P.ev_mask)) {
                 int rstar;
                 if (merge) {
-                    // bucket (lg(1-H) + mx + lg(1 + 2^(mn - mx))) vs the best growth slot
-                    // (lg(1-H) + d_ex); ties -> the smaller run length (the growth slot)
+                    // bucket vb vs the best growth slot d_ex (ties -> the smaller run length)
                     int pex = tmod - r_ex;
                     pex += (pex < 0) ? R : 0;
                     const double dex = r_ex >= 0 ? lprow[pex] - M : -INFINITY;
-                    const double u = fast_exp2(mx == -INFINITY ? -INFINITY : mn - mx);
-                    const double bucket = mx == -INFINITY ? -INFINITY : mx + fast_log2(1.0 + u);
-                    rstar = (r_ex < 0 || bucket > dex) ? R - 1 : r_ex + 1;
+                    rstar = (r_ex < 0 || vb > dex) ? R - 1 : r_ex + 1;
                 } else {
                     rstar = r_ex + 1;
                 }
-                if (EAGER && t > 0 && rstar < min(gs.map_prev + 1, R - 1)) fl |= 2u;
+                if (EAGER && t > 0 && rstar < min(map_prev + 1, R - 1)) fl |= 2u;
+                map_prev = rstar;
+                if (i == 0 && P.out_map) P.out_map[s * P.ld_o + tl] = rstar;
                 if (fl & P.ev_mask) {
-                    const int idx = gs.ev_count++;
-                    if (idx < P.ev_cap) {
+                    const double pnew = merge ? (R == 2 ? 1.0 : fast_exp2(d0 - lg_sum))
+                                              : fast_exp2(d0) * fast_rcp(sum - eB);
+                    if (i == 0 && ev_count < P.ev_cap) {
                         EventRec ev;
                         ev.t = t;
                         ev.cp_index = t - rstar + 1;
                         ev.flags = fl;
                         ev.pad = 0;
                         ev.p_new = pnew;
-                        P.ev[s * P.ev_cap + idx] = ev;
+                        P.ev[s * P.ev_cap + ev_count] = ev;
                     }
+                    ++ev_count;
                 }
-                gs.map_prev = rstar;
-                if (P.out_map) P.out_map[s * P.ld_o + tl] = rstar;
             }
+            if (i == 0) {
+                if (P.out_pnew)
+                    P.out_pnew[s * P.ld_o + tl] = merge ? (R == 2 ? 1.0 : fast_exp2(d0 - lg_sum))
+                                                        : fast_exp2(d0) * fast_rcp(sum - eB);
+                if (P.out_logz) P.out_logz[s * P.ld_o + tl] = LN2 * ((M - n_prev) + Nt);
+            }
+            n_prev = Nt;
             tmod = (tmod + 1 == R) ? 0 : tmod + 1;
         }
     }
     // ---- spill -------------------------------------------------------------
-    if (nonfinite) atomicOr(&gs.flags, 1);
     group_sync<NT>(g);
 #pragma unroll
     for (int j = 0; j < J; ++j) {
@@ -559,14 +570,14 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         SeriesScalars sc;
         sc.mu0 = gs.mu0;
         sc.beta0 = gs.beta0;
-        sc.n_prev = gs.n_prev;
-        sc.map_prev = gs.map_prev;
-        sc.ev_count = gs.ev_count;
-        sc.flags = gs.flags;
+        sc.n_prev = n_prev;
+        sc.map_prev = map_prev;
+        sc.ev_count = ev_count;
+        sc.flags = gs.flags | (nonfinite ? 1 : 0);
         sc.pad = 0;
         sc.pad2 = 0.0;
         P.scal[s] = sc;
-        if (gs.flags) atomicOr(P.err, unsigned(gs.flags));
+        if (sc.flags) atomicOr(P.err, unsigned(sc.flags));
     }
 }
 

@@ -430,6 +430,7 @@ static int launch_update(falcon_bocd_t h, const double* x_dev, int64_t ld, int64
         P.l2mH = (double)log2l(1.0L - (long double)c.hazard);
         P.omH = 1.0 - c.hazard;
         P.theta = c.threshold;
+        P.l2theta = c.threshold > 0.0 ? std::log2(c.threshold) : -INFINITY;
         P.alpha0 = c.alpha0;
         P.prior_cov = c.prior_cov;
         P.mode = c.trunc_mode;
