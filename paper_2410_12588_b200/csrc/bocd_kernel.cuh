@@ -40,6 +40,7 @@
 namespace fbocd {
 
 constexpr int kTile = 256;  // x steps per shared-memory tile (2 KB)
+constexpr int kG = 4;       // cells per interleaved group in phase 1
 
 struct SeriesScalars {  // per-series state carried between calls (HBM), 48 B
     double mu0, beta0;  // prior (set from x_0 when prior_first_obs)
@@ -356,27 +357,60 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             // ---- phase 1: A1 + A2 + A3 (loads only: no shared store may block the
             //      scheduler from interleaving the J independent cells) ---------
             const int ib = tmod - i + R;  // TAB2 index of cell j: ib - NT*j  (= (t - p) mod R, + R)
+            // The cells are processed in groups of G with every stage written across the
+            // group, so G independent log2 chains are in flight per thread (ILP): the
+            // scheduler cannot be relied on to interleave whole inlined calls.
 #pragma unroll
-            for (int j = 0; j < J; ++j) {
-                const int p = i + NT * j;
-                if (FULL || p < R) {
-                    int idx;
+            for (int j0 = 0; j0 < J; j0 += kG) {
+                constexpr int G = (J < kG) ? J : kG;
+                int idx[G];
+                double bn[G], r[G], kd[G], pp[G];
+                double2 tl[G];
+#pragma unroll
+                for (int k = 0; k < G; ++k) {  // A1: NIG update
+                    const int j = j0 + k;
+                    const int p = i + NT * j;
                     if (TAB2) {
-                        idx = ib - NT * j;
+                        idx[k] = ib - NT * j;
                     } else if (FULL) {
-                        idx = (tmod - p) & (R - 1);
+                        idx[k] = (tmod - p) & (R - 1);
                     } else {
-                        idx = tmod - p;
-                        idx += (idx < 0) ? R : 0;
+                        idx[k] = tmod - p;
+                        idx[k] += (idx[k] < 0) ? R : 0;
                     }
-                    const double2 gk = s_gk[idx];
+                    if (!FULL && p >= R) idx[k] = 0;  // masked cell: any valid entry
+                    const double2 gk = s_gk[idx[k]];
                     const double d = x - mu[j];
-                    const double bn = fma(gk.x * d, d, be[j]);
+                    bn[k] = fma(gk.x * d, d, be[j]);
                     mu[j] = fma(d, gk.y, mu[j]);
-                    const double Ln = fast_log2(bn);
-                    const double2 ca = s_ca[idx];
+                }
+#pragma unroll
+                for (int k = 0; k < G; ++k) {  // fast_log2, staged: table entry
+                    const int tb = __double2hiint(bn[k]) + 0x00196000;
+                    tl[k] = *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(g_fm.logtab) +
+                                                              ((tb >> 9) & ((kLogTab - 1) << 4)));
+                    const double invs = __hiloint2double(__double2hiint(tl[k].x) + 0x40000000 - (tb & 0xFFF00000),
+                                                         __double2loint(tl[k].x));
+                    r[k] = fma(bn[k], invs, -1.0);
+                    kd[k] = __hiloint2double(0x43300000, int(unsigned(tb) >> 20)) - c_fm[6];
+                }
+#pragma unroll
+                for (int k = 0; k < G; ++k) pp[k] = fma(r[k], c_fm[0], c_fm[1]);
+#pragma unroll
+                for (int k = 0; k < G; ++k) pp[k] = fma(pp[k], r[k], c_fm[2]);
+#pragma unroll
+                for (int k = 0; k < G; ++k) pp[k] = fma(pp[k], r[k], c_fm[3]);
+#pragma unroll
+                for (int k = 0; k < G; ++k) pp[k] = fma(pp[k], r[k], c_fm[4]);
+#pragma unroll
+                for (int k = 0; k < G; ++k) pp[k] = fma(pp[k], r[k], c_fm[5]);
+#pragma unroll
+                for (int k = 0; k < G; ++k) {  // A2 + A3
+                    const int j = j0 + k;
+                    const double Ln = kd[k] + fma(r[k], pp[k], tl[k].y);
+                    const double2 ca = s_ca[idx[k]];
                     const double ell = fma(-0.5, Ln, fma(ca.y, L[j] - Ln, ca.x));
-                    be[j] = bn;
+                    be[j] = bn[k];
                     L[j] = Ln;
                     v[j] = v[j] + ell;  // lp
                 }
@@ -425,13 +459,46 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             }
             const double M = ord_hi_val(mh);
             // ---- phase 2: exp + sum, growth (A4, A5) --------------------
+            // (fast_exp2 staged across groups of G cells, as in phase 1; the summation
+            //  order is fixed: cell 0, 1, ..., J-1)
             double sum = 0.0;
 #pragma unroll
-            for (int j = 0; j < J; ++j) {
-                const int p = i + NT * j;
-                if (FULL || p < R) {
+            for (int j0 = 0; j0 < J; j0 += kG) {
+                constexpr int G = (J < kG) ? J : kG;
+                double xc[G], kd[G], rr[G], pp[G];
+                int ki[G];
+#pragma unroll
+                for (int k = 0; k < G; ++k) {
+                    const int j = j0 + k;
                     v[j] -= M;
-                    sum += fast_exp2(v[j]);
+                    // clamp >= -1021 on the high word only (fast_exp2)
+                    const int xh = int(min(unsigned(__double2hiint(v[j])), 0xC08FE800u));
+                    xc[k] = __hiloint2double(xh, __double2loint(v[j]));
+                    const double zf = fma(xc[k], c_fm[13], c_fm[7]);
+                    ki[k] = __double2loint(zf);
+                    kd[k] = zf - c_fm[7];
+                }
+#pragma unroll
+                for (int k = 0; k < G; ++k) rr[k] = fma(kd[k], c_fm[14], xc[k]);
+#pragma unroll
+                for (int k = 0; k < G; ++k) pp[k] = fma(rr[k], c_fm[8], c_fm[9]);
+#pragma unroll
+                for (int k = 0; k < G; ++k) pp[k] = fma(pp[k], rr[k], c_fm[10]);
+#pragma unroll
+                for (int k = 0; k < G; ++k) pp[k] = fma(pp[k], rr[k], c_fm[11]);
+#pragma unroll
+                for (int k = 0; k < G; ++k) pp[k] = fma(pp[k], rr[k], c_fm[12]);
+#pragma unroll
+                for (int k = 0; k < G; ++k) {
+                    const int j = j0 + k;
+                    const double q = pp[k] * rr[k];
+                    const double T = *reinterpret_cast<const double*>(reinterpret_cast<const char*>(g_fm.exptab) +
+                                                                      ((ki[k] << 3) & 0x1F8));
+                    int th;
+                    asm("mad.lo.s32 %0, %1, 1048576, %2;" : "=r"(th) : "r"(ki[k] >> 6), "r"(__double2hiint(T)));
+                    const double Ts = __hiloint2double(th, __double2loint(T));
+                    const double e = fma(Ts, q, Ts);
+                    if (FULL || i + NT * j < R) sum += e;
                 }
             }
 #pragma unroll
