@@ -29,9 +29,10 @@ int select_variant(int R, Variant* out) {
     // Tuning hook (bench / profiling only): alternative shapes for R = 1024.
     if (R == 1024) {
         const char* ev = getenv("FALCON_BOCD_VARIANT");
-        if (ev && strcmp(ev, "256x4s3") == 0) { make_variant<256, 4, true, true, 3, 1>(out); return 0; }
-        if (ev && strcmp(ev, "128x8s5") == 0) { make_variant<128, 8, true, true, 5, 1>(out); return 0; }
         if (ev && strcmp(ev, "128x8s4") == 0) { make_variant<128, 8, true, true, 4, 1>(out); return 0; }
+        if (ev && strcmp(ev, "128x8s3") == 0) { make_variant<128, 8, true, true, 3, 1>(out); return 0; }
+        if (ev && strcmp(ev, "128x8s2m1") == 0) { make_variant<128, 8, true, true, 2, 1>(out); return 0; }
+        if (ev && strcmp(ev, "256x4s1m2") == 0) { make_variant<256, 4, true, true, 1, 2>(out); return 0; }
     }
     switch (R) {
         case 256: make_variant<32, 8, true, true, 8, 2>(out); return 0;
