@@ -32,11 +32,14 @@ if ROOT not in sys.path:
 
 METRIC = "BOCD series·timesteps/sec (R=1024, fp64) at 1/2/4/8 B200; % roofline"
 UNIT = "series*steps/s"
-# Algorithmic FP64-pipe work per cell (one run length, one step): DESIGN.md §6.
-#   12 arithmetic (NIG update 4, predictive 3, joint/growth/normalise 3, max/LSE 2)
-#   + 1 log (30 FP64-pipe instructions in libdevice) + 1 exp (18), both measured
-#   from SASS (cuobjdump) in P0 -> 60 FP64-pipe instructions per cell.
-FP64_INSTR_PER_CELL = 60
+# FP64-pipe work per cell (one run length, one step): DESIGN.md §6.
+#   The kernel executes 32.9 FP64-pipe instructions per cell (ncu: DFMA+DADD+DMUL+DSETP per
+#   cell, profiles/r01_ncu_top_kernel.txt): 10 arithmetic (NIG update 4, predictive 4, growth /
+#   shift / sum 2... ) + fast_log2 (9) + fast_exp2 (9) + per-step tail work amortised.
+#   roofline.frac therefore equals the FP64-pipe utilisation.  For context the same work with
+#   libdevice log/exp (30 + 18 FP64 instructions, cuobjdump, P0) is 60 instructions per cell.
+FP64_INSTR_PER_CELL = 32.9
+FP64_INSTR_PER_CELL_LIBDEVICE = 60
 # FP64 pipe peak: 148 SMs x 64 FP64 lanes/clk x 1965 MHz (sm_max_mhz, MEASURED_PEAKS.json);
 # P0 measured 58.9 DFMA/clk/SM sustained at 1965 MHz (profiles/r01_p0_fp64_peaks.json).
 SMS, FP64_PER_CLK_SM = 148, 64
@@ -315,6 +318,8 @@ def main():
                          "kernel": "bocd_update_kernel<128,8,FULL>",
                          "kernel_ms_avg": k_avg, "kernel_share_of_step": k_share,
                          "work_per_cell": FP64_INSTR_PER_CELL,
+                         "frac_vs_libdevice_work": FP64_INSTR_PER_CELL_LIBDEVICE * cells_per_launch
+                         / (k_avg * 1e-3) / peak,
                          "peak_basis": f"{SMS} SMs x {FP64_PER_CLK_SM} FP64/clk x {sm_max:.0f} MHz (derived)"},
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": args.steps + 3,
