@@ -184,12 +184,12 @@ __device__ __forceinline__ bool tile_tma_ok(const KParams& P, int k) {
     return P.tma_ok && ((n & 1) == 0);
 }
 
-// Shared memory of one CTA: tables, then per group: GroupSmem + lp rows [2][R].
+// Shared memory of one CTA: tables, then per group: GroupSmem + the v row [R].
 // TAB2: the per-r tables are stored twice (entries r and r+R) so the ring index
 // (t - p) mod R becomes (t - p + R) with no masking and compile-time offsets per cell.
 template <int NT>
 __host__ __device__ constexpr size_t group_bytes(int R) {
-    return sizeof(GroupSmem<NT>) + size_t(2) * R * sizeof(double);
+    return sizeof(GroupSmem<NT>) + size_t(R) * sizeof(double);
 }
 __host__ __device__ constexpr size_t table_bytes(int R, bool tab2) {
     return size_t(R) * (tab2 ? 2 : 1) * 2 * sizeof(double2);
@@ -222,6 +222,22 @@ __device__ __forceinline__ void set_cell_pred(double (&v)[J], double (&mu)[J], d
         break;
     switch (j) { FBOCD_SET(0) FBOCD_SET(1) FBOCD_SET(2) FBOCD_SET(3) FBOCD_SET(4) FBOCD_SET(5) FBOCD_SET(6) FBOCD_SET(7) }
 #undef FBOCD_SET
+}
+template <int J>
+__device__ __forceinline__ void set_stats_pred(double (&mu)[J], double (&be)[J], double (&L)[J], int j, bool pred,
+                                               double m, double b, double l) {
+#define FBOCD_SETS(k)                     \
+    case k:                               \
+        if constexpr (J > k) {            \
+            if (pred) {                   \
+                mu[k] = m;                \
+                be[k] = b;                \
+                L[k] = l;                 \
+            }                             \
+        }                                 \
+        break;
+    switch (j) { FBOCD_SETS(0) FBOCD_SETS(1) FBOCD_SETS(2) FBOCD_SETS(3) FBOCD_SETS(4) FBOCD_SETS(5) FBOCD_SETS(6) FBOCD_SETS(7) }
+#undef FBOCD_SETS
 }
 template <int J>
 __device__ __forceinline__ void set_v_pred(double (&v)[J], int j, bool pred, double vv) {
@@ -263,7 +279,8 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     const int lane = threadIdx.x & 31;
     const int w = i >> 5;
     GroupSmem<NT>& gs = *reinterpret_cast<GroupSmem<NT>*>(gbase + size_t(g) * group_bytes<NT>(R));
-    double* s_lp = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(&gs) + sizeof(GroupSmem<NT>));
+    // the series' unnormalised log posterior v, in ring-position order (shared memory)
+    double* vrow = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(&gs) + sizeof(GroupSmem<NT>));
     const int64_t s = int64_t(blockIdx.x) * SPB + g;
     const bool active = s < P.S;
     const double* xrow = P.x + (active ? s : 0) * P.ld;
@@ -281,7 +298,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
 
     const double l2H = P.l2H, l2mH = P.l2mH;
     // ---- load or initialise the state ------------------------------------
-    double mu[J], be[J], L[J], v[J];
+    double mu[J], be[J], L[J];
     const int64_t sbase = s * int64_t(R);
     if (i == 0) {
         SeriesScalars sc = P.scal[s];
@@ -315,18 +332,17 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 mu[j] = mu0;
                 be[j] = beta0;
                 L[j] = L0;
-                v[j] = (p == 0) ? -l2mH : -INFINITY;
+                vrow[p] = (p == 0) ? -l2mH : -INFINITY;
             } else {
                 mu[j] = P.st_mu[sbase + p];
                 be[j] = P.st_beta[sbase + p];
-                v[j] = P.st_v[sbase + p];
+                vrow[p] = P.st_v[sbase + p];
                 L[j] = fast_log2(be[j]);
             }
         } else {
             mu[j] = mu0;
             be[j] = beta0;
             L[j] = L0;
-            v[j] = -INFINITY;
         }
     }
 
@@ -335,6 +351,11 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     const int r_elig = merge ? R - 3 : R - 2;
     int tmod = int(P.t0 % R);  // ring bookkeeping: t mod R
     bool nonfinite = false;
+    // Pending fix-ups of the previous step, applied by their owner lanes when the cell's v
+    // is loaded in the next phase 1 (the row itself is never patched: other threads read
+    // the pre-fix values in the tail).  pos = -1: none.
+    int fixB_pos = -1, fixA_pos = -1;
+    double fixB_v = 0.0, fixA_v = 0.0;
 
     for (int k = 0; k < ntiles; ++k) {
         const int base = k * kTile;
@@ -352,67 +373,69 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         for (int q = 0; q < n; ++q) {
             const int tl = base + q;
             const int64_t t = P.t0 + tl;
-            double* lprow = s_lp + (tl & 1) * R;
             const double x = gs.xbuf[buf][q];
-            // ---- phase 1: A1 + A2 + A3 (loads only: no shared store may block the
-            //      scheduler from interleaving the J independent cells) ---------
+            // ---- phase 1: A1 + A2 + A3 ------------------------------------------
             const int ib = tmod - i + R;  // TAB2 index of cell j: ib - NT*j  (= (t - p) mod R, + R)
+            double lp[J];
             // The cells are processed in groups of G with every stage written across the
-            // group, so G independent log2 chains are in flight per thread (ILP): the
-            // scheduler cannot be relied on to interleave whole inlined calls.
+            // group, so G independent log2 chains are in flight per thread (ILP).
 #pragma unroll
             for (int j0 = 0; j0 < J; j0 += kG) {
                 constexpr int G = (J < kG) ? J : kG;
                 int idx[G];
                 double bn[G], r[G], kd[G], pp[G];
-                double2 tl[G];
+                double2 tl2[G];
 #pragma unroll
-                for (int k = 0; k < G; ++k) {  // A1: NIG update
-                    const int j = j0 + k;
+                for (int kk = 0; kk < G; ++kk) {  // A1: NIG update
+                    const int j = j0 + kk;
                     const int p = i + NT * j;
                     if (TAB2) {
-                        idx[k] = ib - NT * j;
+                        idx[kk] = ib - NT * j;
                     } else if (FULL) {
-                        idx[k] = (tmod - p) & (R - 1);
+                        idx[kk] = (tmod - p) & (R - 1);
                     } else {
-                        idx[k] = tmod - p;
-                        idx[k] += (idx[k] < 0) ? R : 0;
+                        idx[kk] = tmod - p;
+                        idx[kk] += (idx[kk] < 0) ? R : 0;
                     }
-                    if (!FULL && p >= R) idx[k] = 0;  // masked cell: any valid entry
-                    const double2 gk = s_gk[idx[k]];
+                    if (!FULL && p >= R) idx[kk] = 0;  // masked cell: any valid entry
+                    const double2 gk = s_gk[idx[kk]];
                     const double d = x - mu[j];
-                    bn[k] = fma(gk.x * d, d, be[j]);
+                    bn[kk] = fma(gk.x * d, d, be[j]);
                     mu[j] = fma(d, gk.y, mu[j]);
                 }
 #pragma unroll
-                for (int k = 0; k < G; ++k) {  // fast_log2, staged: table entry
-                    const int tb = __double2hiint(bn[k]) + 0x00196000;
-                    tl[k] = *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(g_fm.logtab) +
-                                                              ((tb >> 9) & ((kLogTab - 1) << 4)));
-                    const double invs = __hiloint2double(__double2hiint(tl[k].x) + 0x40000000 - (tb & 0xFFF00000),
-                                                         __double2loint(tl[k].x));
-                    r[k] = fma(bn[k], invs, -1.0);
-                    kd[k] = __hiloint2double(0x43300000, int(unsigned(tb) >> 20)) - c_fm[6];
+                for (int kk = 0; kk < G; ++kk) {  // fast_log2, staged: table entry
+                    const int tb = __double2hiint(bn[kk]) + 0x00196000;
+                    tl2[kk] = *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(g_fm.logtab) +
+                                                                ((tb >> 9) & ((kLogTab - 1) << 4)));
+                    const double invs = __hiloint2double(__double2hiint(tl2[kk].x) + 0x40000000 - (tb & 0xFFF00000),
+                                                         __double2loint(tl2[kk].x));
+                    r[kk] = fma(bn[kk], invs, -1.0);
+                    kd[kk] = __hiloint2double(0x43300000, int(unsigned(tb) >> 20)) - c_fm[6];
                 }
 #pragma unroll
-                for (int k = 0; k < G; ++k) pp[k] = fma(r[k], c_fm[0], c_fm[1]);
+                for (int kk = 0; kk < G; ++kk) pp[kk] = fma(r[kk], c_fm[0], c_fm[1]);
 #pragma unroll
-                for (int k = 0; k < G; ++k) pp[k] = fma(pp[k], r[k], c_fm[2]);
+                for (int kk = 0; kk < G; ++kk) pp[kk] = fma(pp[kk], r[kk], c_fm[2]);
 #pragma unroll
-                for (int k = 0; k < G; ++k) pp[k] = fma(pp[k], r[k], c_fm[3]);
+                for (int kk = 0; kk < G; ++kk) pp[kk] = fma(pp[kk], r[kk], c_fm[3]);
 #pragma unroll
-                for (int k = 0; k < G; ++k) pp[k] = fma(pp[k], r[k], c_fm[4]);
+                for (int kk = 0; kk < G; ++kk) pp[kk] = fma(pp[kk], r[kk], c_fm[4]);
 #pragma unroll
-                for (int k = 0; k < G; ++k) pp[k] = fma(pp[k], r[k], c_fm[5]);
+                for (int kk = 0; kk < G; ++kk) pp[kk] = fma(pp[kk], r[kk], c_fm[5]);
 #pragma unroll
-                for (int k = 0; k < G; ++k) {  // A2 + A3
-                    const int j = j0 + k;
-                    const double Ln = kd[k] + fma(r[k], pp[k], tl[k].y);
-                    const double2 ca = s_ca[idx[k]];
+                for (int kk = 0; kk < G; ++kk) {  // A2 + A3: predictive, joint with v
+                    const int j = j0 + kk;
+                    const int p = i + NT * j;
+                    const double Ln = kd[kk] + fma(r[kk], pp[kk], tl2[kk].y);
+                    const double2 ca = s_ca[idx[kk]];
                     const double ell = fma(-0.5, Ln, fma(ca.y, L[j] - Ln, ca.x));
-                    be[j] = bn[k];
+                    be[j] = bn[kk];
                     L[j] = Ln;
-                    v[j] = v[j] + ell;  // lp
+                    double vj = (FULL || p < R) ? vrow[p] : -INFINITY;
+                    vj = (p == fixB_pos) ? fixB_v : vj;  // owner lanes only (positions are unique)
+                    vj = (p == fixA_pos) ? fixA_v : vj;
+                    lp[j] = vj + ell;
                 }
             }
             // shift M (max over all cells, high word is enough) and, if EAGER, the argmax key
@@ -422,12 +445,11 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             for (int j = 0; j < J; ++j) {
                 const int p = i + NT * j;
                 if (FULL || p < R) {
-                    lprow[p] = v[j];
-                    mh = max(mh, ord_hi(v[j]));
+                    mh = max(mh, ord_hi(lp[j]));
                     if constexpr (EAGER) {
                         int r = tmod - p;
                         r += (r < 0) ? R : 0;
-                        const unsigned long long kk = argmax_key(v[j], r);
+                        const unsigned long long kk = argmax_key(lp[j], r);
                         key = (r <= r_elig && kk > key) ? kk : key;
                     }
                 }
@@ -458,9 +480,8 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 group_sync<NT>(g);
             }
             const double M = ord_hi_val(mh);
-            // ---- phase 2: exp + sum, growth (A4, A5) --------------------
-            // (fast_exp2 staged across groups of G cells, as in phase 1; the summation
-            //  order is fixed: cell 0, 1, ..., J-1)
+            // ---- phase 2: exp + sum, growth (A4, A5): v'_{r+1} = lp_r - M ------------
+            // (fast_exp2 staged across groups of G cells; summation order fixed: cell 0..J-1)
             double sum = 0.0;
 #pragma unroll
             for (int j0 = 0; j0 < J; j0 += kG) {
@@ -468,36 +489,38 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 double xc[G], kd[G], rr[G], pp[G];
                 int ki[G];
 #pragma unroll
-                for (int k = 0; k < G; ++k) {
-                    const int j = j0 + k;
-                    v[j] -= M;
+                for (int kk = 0; kk < G; ++kk) {
+                    const int j = j0 + kk;
+                    const int p = i + NT * j;
+                    const double dm = lp[j] - M;
+                    if (FULL || p < R) vrow[p] = dm;
                     // clamp >= -1021 on the high word only (fast_exp2)
-                    const int xh = int(min(unsigned(__double2hiint(v[j])), 0xC08FE800u));
-                    xc[k] = __hiloint2double(xh, __double2loint(v[j]));
-                    const double zf = fma(xc[k], c_fm[13], c_fm[7]);
-                    ki[k] = __double2loint(zf);
-                    kd[k] = zf - c_fm[7];
+                    const int xh = int(min(unsigned(__double2hiint(dm)), 0xC08FE800u));
+                    xc[kk] = __hiloint2double(xh, __double2loint(dm));
+                    const double zf = fma(xc[kk], c_fm[13], c_fm[7]);
+                    ki[kk] = __double2loint(zf);
+                    kd[kk] = zf - c_fm[7];
                 }
 #pragma unroll
-                for (int k = 0; k < G; ++k) rr[k] = fma(kd[k], c_fm[14], xc[k]);
+                for (int kk = 0; kk < G; ++kk) rr[kk] = fma(kd[kk], c_fm[14], xc[kk]);
 #pragma unroll
-                for (int k = 0; k < G; ++k) pp[k] = fma(rr[k], c_fm[8], c_fm[9]);
+                for (int kk = 0; kk < G; ++kk) pp[kk] = fma(rr[kk], c_fm[8], c_fm[9]);
 #pragma unroll
-                for (int k = 0; k < G; ++k) pp[k] = fma(pp[k], rr[k], c_fm[10]);
+                for (int kk = 0; kk < G; ++kk) pp[kk] = fma(pp[kk], rr[kk], c_fm[10]);
 #pragma unroll
-                for (int k = 0; k < G; ++k) pp[k] = fma(pp[k], rr[k], c_fm[11]);
+                for (int kk = 0; kk < G; ++kk) pp[kk] = fma(pp[kk], rr[kk], c_fm[11]);
 #pragma unroll
-                for (int k = 0; k < G; ++k) pp[k] = fma(pp[k], rr[k], c_fm[12]);
+                for (int kk = 0; kk < G; ++kk) pp[kk] = fma(pp[kk], rr[kk], c_fm[12]);
 #pragma unroll
-                for (int k = 0; k < G; ++k) {
-                    const int j = j0 + k;
-                    const double q = pp[k] * rr[k];
+                for (int kk = 0; kk < G; ++kk) {
+                    const int j = j0 + kk;
+                    const double qq = pp[kk] * rr[kk];
                     const double T = *reinterpret_cast<const double*>(reinterpret_cast<const char*>(g_fm.exptab) +
-                                                                      ((ki[k] << 3) & 0x1F8));
+                                                                      ((ki[kk] << 3) & 0x1F8));
                     int th;
-                    asm("mad.lo.s32 %0, %1, 1048576, %2;" : "=r"(th) : "r"(ki[k] >> 6), "r"(__double2hiint(T)));
+                    asm("mad.lo.s32 %0, %1, 1048576, %2;" : "=r"(th) : "r"(ki[kk] >> 6), "r"(__double2hiint(T)));
                     const double Ts = __hiloint2double(th, __double2loint(T));
-                    const double e = fma(Ts, q, Ts);
+                    const double e = fma(Ts, qq, Ts);
                     if (FULL || i + NT * j < R) sum += e;
                 }
             }
@@ -513,14 +536,13 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 group_sync<NT>(g);
             }
             // ---- the scalar tail (A5-A8), computed UNIFORMLY by every thread -------
-            // (no lane-divergent latency chain between two barriers; the two cells
-            // that change identity are then written by their owners through a
-            // warp-uniform switch with a lane predicate)
             //   recycled cell pB (r = R-1) -> new CP cell: v = lg H - lg(1-H) + lg(sum), prior stats
             //   MERGE: cell pA (r = R-2) -> bucket: v = lg(2^dA + 2^dB) = mx + lg(1 + 2^(mn - mx))
+            // The new v of the two cells become register overrides for their owner lanes in the
+            // next phase 1 (fixB/fixA); only the CP cell's statistics are reset here.
             const int pB = (tmod + 1 == R) ? 0 : tmod + 1;
             const int pA = (pB + 1 == R) ? 0 : pB + 1;
-            const double dA = lprow[pA] - M, dB = lprow[pB] - M, d0 = lprow[tmod] - M;
+            const double dA = vrow[pA], dB = vrow[pB], d0 = vrow[tmod];
             const double mx = fmax(dA, dB), mn = fmin(dA, dB);
             // one log stream for two values: lanes 0-15 lg(sum), lanes 16-31 lg(1 + u)
             const double u = fast_exp2(mx == -INFINITY ? -INFINITY : mn - mx);
@@ -541,9 +563,12 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             }
             uint32_t fl = (t > 0 && prob) ? 1u : 0u;
             {
-                const int jB = pB / NT, jA = pA / NT;
-                set_cell_pred<J>(v, mu, be, L, jB, (pB % NT) == i, l2H - l2mH + lg_sum, mu0, beta0, L0);
-                if (merge) set_v_pred<J>(v, jA, (pA % NT) == i, vb);
+                const bool ownB = (pB % NT) == i;
+                fixB_pos = ownB ? pB : -1;
+                fixB_v = l2H - l2mH + lg_sum;
+                fixA_pos = (merge && (pA % NT) == i) ? pA : -1;
+                fixA_v = vb;
+                set_stats_pred<J>(mu, be, L, pB / NT, ownB, mu0, beta0, L0);
             }
             if (!isfinite(x)) nonfinite = true;
             // ---- MAP run length r* (A7): eager (key reduced at barrier A) or on demand ----
@@ -561,7 +586,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     if (FULL || p < R) {
                         int r = tmod - p;
                         r += (r < 0) ? R : 0;
-                        const unsigned long long kk = argmax_key(lprow[p], r);
+                        const unsigned long long kk = argmax_key(vrow[p], r);  // dm: same order as lp
                         kb = (r <= r_elig && kk > kb) ? kk : kb;
                     }
                 }
@@ -589,7 +614,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     // bucket vb vs the best growth slot d_ex (ties -> the smaller run length)
                     int pex = tmod - r_ex;
                     pex += (pex < 0) ? R : 0;
-                    const double dex = r_ex >= 0 ? lprow[pex] - M : -INFINITY;
+                    const double dex = r_ex >= 0 ? vrow[pex] : -INFINITY;
                     rstar = (r_ex < 0 || vb > dex) ? R - 1 : r_ex + 1;
                 } else {
                     rstar = r_ex + 1;
@@ -622,15 +647,18 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             tmod = (tmod + 1 == R) ? 0 : tmod + 1;
         }
     }
-    // ---- spill -------------------------------------------------------------
+    // ---- spill (with the pending fix-ups applied) ----------------------------
     group_sync<NT>(g);
 #pragma unroll
     for (int j = 0; j < J; ++j) {
         const int p = i + NT * j;
         if (FULL || p < R) {
+            double vj = vrow[p];
+            vj = (p == fixB_pos) ? fixB_v : vj;
+            vj = (p == fixA_pos) ? fixA_v : vj;
             P.st_mu[sbase + p] = mu[j];
             P.st_beta[sbase + p] = be[j];
-            P.st_v[sbase + p] = v[j];
+            P.st_v[sbase + p] = vj;
         }
     }
     if (i == 0) {
