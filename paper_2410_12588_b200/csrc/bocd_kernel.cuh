@@ -189,7 +189,7 @@ __device__ __forceinline__ bool tile_tma_ok(const KParams& P, int k) {
 // (t - p) mod R becomes (t - p + R) with no masking and compile-time offsets per cell.
 template <int NT>
 __host__ __device__ constexpr size_t group_bytes(int R) {
-    return sizeof(GroupSmem<NT>) + size_t(R) * sizeof(double);
+    return sizeof(GroupSmem<NT>) + ((size_t(R) * sizeof(double) + 15) & ~size_t(15));  // keep 16-B alignment
 }
 __host__ __device__ constexpr size_t table_bytes(int R, bool tab2) {
     return size_t(R) * (tab2 ? 2 : 1) * 2 * sizeof(double2);

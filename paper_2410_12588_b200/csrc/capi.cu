@@ -323,7 +323,7 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
         return fail(nullptr, FALCON_EINVAL, "no kernel variant for this R");
     }
     h->smem = fbocd::table_bytes(c.R, h->var.tab2) +
-              size_t(h->var.spb) * (h->var.group_smem + size_t(c.R) * sizeof(double));
+              size_t(h->var.spb) * (h->var.group_smem + ((size_t(c.R) * sizeof(double) + 15) & ~size_t(15)));
     auto bail = [&](int code) {
         g_create_err = h->err;
         falcon_bocd_destroy(h);
