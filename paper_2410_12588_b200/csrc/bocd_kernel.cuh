@@ -96,6 +96,7 @@ struct __align__(16) GroupSmem {
     double red2[NT / 32 > 0 ? NT / 32 : 1];
     int redh[NT / 32 > 0 ? NT / 32 : 1];
     unsigned long long red3[NT / 32 > 0 ? NT / 32 : 1];  // on-demand argmax (event steps)
+    double spec[4];                                       // dm of the cells r = R-2, R-1, 0
     double mu0, beta0, L0, n_prev;
     int map_prev, ev_count, flags, pad;
     unsigned long long mbar[2];
@@ -351,11 +352,6 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     const int r_elig = merge ? R - 3 : R - 2;
     int tmod = int(P.t0 % R);  // ring bookkeeping: t mod R
     bool nonfinite = false;
-    // Pending fix-ups of the previous step, applied by their owner lanes when the cell's v
-    // is loaded in the next phase 1 (the row itself is never patched: other threads read
-    // the pre-fix values in the tail).  pos = -1: none.
-    int fixB_pos = -1, fixA_pos = -1;
-    double fixB_v = 0.0, fixA_v = 0.0;
 
     for (int k = 0; k < ntiles; ++k) {
         const int base = k * kTile;
@@ -432,10 +428,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     const double ell = fma(-0.5, Ln, fma(ca.y, L[j] - Ln, ca.x));
                     be[j] = bn[kk];
                     L[j] = Ln;
-                    double vj = (FULL || p < R) ? vrow[p] : -INFINITY;
-                    vj = (p == fixB_pos) ? fixB_v : vj;  // owner lanes only (positions are unique)
-                    vj = (p == fixA_pos) ? fixA_v : vj;
-                    lp[j] = vj + ell;
+                    lp[j] = ((FULL || p < R) ? vrow[p] : -INFINITY) + ell;
                 }
             }
             // shift M (max over all cells, high word is enough) and, if EAGER, the argmax key
@@ -524,6 +517,13 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     if (FULL || i + NT * j < R) sum += e;
                 }
             }
+            // the three cells the tail needs are published by their owners (the row entries of
+            // pA / pB are overwritten by the fix-ups right after the barrier)
+            const int pB = (tmod + 1 == R) ? 0 : tmod + 1;  // r = R-1 (recycled)
+            const int pA = (pB + 1 == R) ? 0 : pB + 1;      // r = R-2
+            if ((pA % NT) == i) gs.spec[0] = vrow[pA];
+            if ((pB % NT) == i) gs.spec[1] = vrow[pB];
+            if ((tmod % NT) == i) gs.spec[2] = vrow[tmod];
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
             if constexpr (NT > 32) {
@@ -538,11 +538,9 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             // ---- the scalar tail (A5-A8), computed UNIFORMLY by every thread -------
             //   recycled cell pB (r = R-1) -> new CP cell: v = lg H - lg(1-H) + lg(sum), prior stats
             //   MERGE: cell pA (r = R-2) -> bucket: v = lg(2^dA + 2^dB) = mx + lg(1 + 2^(mn - mx))
-            // The new v of the two cells become register overrides for their owner lanes in the
-            // next phase 1 (fixB/fixA); only the CP cell's statistics are reset here.
-            const int pB = (tmod + 1 == R) ? 0 : tmod + 1;
-            const int pA = (pB + 1 == R) ? 0 : pB + 1;
-            const double dA = vrow[pA], dB = vrow[pB], d0 = vrow[tmod];
+            // (the owners write the new v of the two cells into the row and reset the CP cell's
+            //  statistics; everyone else reads the pre-fix values from gs.spec)
+            const double dA = gs.spec[0], dB = gs.spec[1], d0 = gs.spec[2];
             const double mx = fmax(dA, dB), mn = fmin(dA, dB);
             // one log stream for two values: lanes 0-15 lg(sum), lanes 16-31 lg(1 + u)
             const double u = fast_exp2(mx == -INFINITY ? -INFINITY : mn - mx);
@@ -564,10 +562,8 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             uint32_t fl = (t > 0 && prob) ? 1u : 0u;
             {
                 const bool ownB = (pB % NT) == i;
-                fixB_pos = ownB ? pB : -1;
-                fixB_v = l2H - l2mH + lg_sum;
-                fixA_pos = (merge && (pA % NT) == i) ? pA : -1;
-                fixA_v = vb;
+                if (ownB) vrow[pB] = l2H - l2mH + lg_sum;
+                if (merge && (pA % NT) == i) vrow[pA] = vb;
                 set_stats_pred<J>(mu, be, L, pB / NT, ownB, mu0, beta0, L0);
             }
             if (!isfinite(x)) nonfinite = true;
@@ -653,12 +649,9 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     for (int j = 0; j < J; ++j) {
         const int p = i + NT * j;
         if (FULL || p < R) {
-            double vj = vrow[p];
-            vj = (p == fixB_pos) ? fixB_v : vj;
-            vj = (p == fixA_pos) ? fixA_v : vj;
             P.st_mu[sbase + p] = mu[j];
             P.st_beta[sbase + p] = be[j];
-            P.st_v[sbase + p] = vj;
+            P.st_v[sbase + p] = vrow[p];
         }
     }
     if (i == 0) {
