@@ -221,7 +221,8 @@ __device__ __forceinline__ void set_cell_pred(double (&v)[J], double (&mu)[J], d
             }                             \
         }                                 \
         break;
-    switch (j) { FBOCD_SET(0) FBOCD_SET(1) FBOCD_SET(2) FBOCD_SET(3) FBOCD_SET(4) FBOCD_SET(5) FBOCD_SET(6) FBOCD_SET(7) }
+    switch (j) { FBOCD_SET(0) FBOCD_SET(1) FBOCD_SET(2) FBOCD_SET(3) FBOCD_SET(4) FBOCD_SET(5) FBOCD_SET(6) FBOCD_SET(7)
+                 FBOCD_SET(8) FBOCD_SET(9) FBOCD_SET(10) FBOCD_SET(11) FBOCD_SET(12) FBOCD_SET(13) FBOCD_SET(14) FBOCD_SET(15) }
 #undef FBOCD_SET
 }
 template <int J>
@@ -237,7 +238,8 @@ __device__ __forceinline__ void set_stats_pred(double (&mu)[J], double (&be)[J],
             }                             \
         }                                 \
         break;
-    switch (j) { FBOCD_SETS(0) FBOCD_SETS(1) FBOCD_SETS(2) FBOCD_SETS(3) FBOCD_SETS(4) FBOCD_SETS(5) FBOCD_SETS(6) FBOCD_SETS(7) }
+    switch (j) { FBOCD_SETS(0) FBOCD_SETS(1) FBOCD_SETS(2) FBOCD_SETS(3) FBOCD_SETS(4) FBOCD_SETS(5) FBOCD_SETS(6) FBOCD_SETS(7)
+                 FBOCD_SETS(8) FBOCD_SETS(9) FBOCD_SETS(10) FBOCD_SETS(11) FBOCD_SETS(12) FBOCD_SETS(13) FBOCD_SETS(14) FBOCD_SETS(15) }
 #undef FBOCD_SETS
 }
 template <int J>
@@ -248,7 +250,8 @@ __device__ __forceinline__ void set_v_pred(double (&v)[J], int j, bool pred, dou
             if (pred) v[k] = vv; \
         }                        \
         break;
-    switch (j) { FBOCD_SETV(0) FBOCD_SETV(1) FBOCD_SETV(2) FBOCD_SETV(3) FBOCD_SETV(4) FBOCD_SETV(5) FBOCD_SETV(6) FBOCD_SETV(7) }
+    switch (j) { FBOCD_SETV(0) FBOCD_SETV(1) FBOCD_SETV(2) FBOCD_SETV(3) FBOCD_SETV(4) FBOCD_SETV(5) FBOCD_SETV(6) FBOCD_SETV(7)
+                 FBOCD_SETV(8) FBOCD_SETV(9) FBOCD_SETV(10) FBOCD_SETV(11) FBOCD_SETV(12) FBOCD_SETV(13) FBOCD_SETV(14) FBOCD_SETV(15) }
 #undef FBOCD_SETV
 }
 
@@ -524,8 +527,10 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             if ((pA % NT) == i) gs.spec[0] = vrow[pA];
             if ((pB % NT) == i) gs.spec[1] = vrow[pB];
             if ((tmod % NT) == i) gs.spec[2] = vrow[tmod];
+            if (P.dbg != 4) {  // dbg 4 (profiling experiment): no warp butterfly
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+                for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            }
             if constexpr (NT > 32) {
                 if (lane == 0) gs.red2[w] = sum;
                 group_sync<NT>(g, P.dbg);
@@ -534,6 +539,10 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 for (int ww = 1; ww < NT / 32; ++ww) sum += gs.red2[ww];
             } else {
                 group_sync<NT>(g);
+            }
+            if (P.dbg == 1) {  // profiling experiment: no tail
+                tmod = (tmod + 1 == R) ? 0 : tmod + 1;
+                continue;
             }
             // ---- the scalar tail (A5-A8), computed UNIFORMLY by every thread -------
             //   recycled cell pB (r = R-1) -> new CP cell: v = lg H - lg(1-H) + lg(sum), prior stats

@@ -31,6 +31,8 @@ int select_variant(int R, Variant* out) {
         const char* ev = getenv("FALCON_BOCD_VARIANT");
         if (ev && strcmp(ev, "128x8s4") == 0) { make_variant<128, 8, true, true, 4, 1>(out); return 0; }
         if (ev && strcmp(ev, "128x8s3") == 0) { make_variant<128, 8, true, true, 3, 1>(out); return 0; }
+        if (ev && strcmp(ev, "64x16s8") == 0) { make_variant<64, 16, true, true, 8, 1>(out); return 0; }
+        if (ev && strcmp(ev, "64x16s4") == 0) { make_variant<64, 16, true, true, 4, 1>(out); return 0; }
         if (ev && strcmp(ev, "128x8s2m1") == 0) { make_variant<128, 8, true, true, 2, 1>(out); return 0; }
         if (ev && strcmp(ev, "256x4s1m2") == 0) { make_variant<256, 4, true, true, 1, 2>(out); return 0; }
     }
