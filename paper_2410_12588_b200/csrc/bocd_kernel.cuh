@@ -243,18 +243,6 @@ __device__ __forceinline__ void set_stats_pred(double (&mu)[J], double (&be)[J],
 #undef FBOCD_SETS
 }
 template <int J>
-__device__ __forceinline__ void add_lp_pred(double (&lp)[J], int j, bool pred, double add) {
-#define FBOCD_ADD(k)                     \
-    case k:                              \
-        if constexpr (J > k) {           \
-            if (pred) lp[k] = add + lp[k]; \
-        }                                \
-        break;
-    switch (j) { FBOCD_ADD(0) FBOCD_ADD(1) FBOCD_ADD(2) FBOCD_ADD(3) FBOCD_ADD(4) FBOCD_ADD(5) FBOCD_ADD(6) FBOCD_ADD(7)
-                 FBOCD_ADD(8) FBOCD_ADD(9) FBOCD_ADD(10) FBOCD_ADD(11) FBOCD_ADD(12) FBOCD_ADD(13) FBOCD_ADD(14) FBOCD_ADD(15) }
-#undef FBOCD_ADD
-}
-template <int J>
 __device__ __forceinline__ void set_v_pred(double (&v)[J], int j, bool pred, double vv) {
 #define FBOCD_SETV(k)            \
     case k:                      \
@@ -368,121 +356,6 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     int tmod = int(P.t0 % R);  // ring bookkeeping: t mod R
     bool nonfinite = false;
 
-    // ---- the scalar tail of a step (A5-A8), SOFTWARE-PIPELINED into the next step ----
-    // Step t leaves: its exp-sum, its shift M, and the dm of the cells r = R-2 (pA),
-    // r = R-1 (pB) and r = 0 (p0).  The row entries of pB (and pA for MERGE) hold a 0.0
-    // placeholder, so in the next phase 1 those cells produce lp = 0 + l exactly, and the
-    // owners add the new v afterwards (v + l, bit-identical to a finalised row):
-    //   pB -> new change-point cell: v = lg H - lg(1-H) + lg(sum)   (statistics reset at barrier B)
-    //   pA -> MERGE bucket:          v = lg(2^dA + 2^dB) = mx + lg(1 + 2^(mn - mx))
-    // The tail's transcendentals are computed uniformly by every thread at the top of the
-    // next phase 1, independent of the cell chains, so their latency overlaps the cell work.
-    bool have_prev = false;
-    double sum_p = 0.0, M_p = 0.0, sA_p = 0.0, sB_p = 0.0, s0_p = 0.0;
-    int tmod_p = 0, tl_p = 0;
-    int64_t t_p = 0;
-    unsigned long long key_p = 0ull;  // EAGER: argmax key of the pending step
-    // values of the tail (T1), computed from the pending step
-    double vcp = 0.0, vb = 0.0, Nt = 0.0, eB = 0.0;
-    bool prob = false;
-    auto tail_values = [&]() {
-        const double mx = fmax(sA_p, sB_p), mn = fmin(sA_p, sB_p);
-        // one log stream for two values: lanes 0-15 lg(sum), lanes 16-31 lg(1 + u)
-        const double u = fast_exp2(mx == -INFINITY ? -INFINITY : mn - mx);
-        const double lgx = fast_log2(lane >= 16 ? 1.0 + u : sum_p);
-        const double lg_sum = __shfl_sync(0xffffffffu, lgx, 0);
-        const double lb = __shfl_sync(0xffffffffu, lgx, 16);
-        vb = (mx == -INFINITY) ? -INFINITY : mx + lb;
-        vcp = l2H - l2mH + lg_sum;
-        if (merge) {
-            Nt = lg_sum;
-            // p_new = R(1) / (1 - R(0)) = 2^(d0 - lg sum)  (R(0) = H exactly; R = 2: p_new = 1)
-            prob = (R == 2) ? (1.0 > P.theta) : (s0_p - lg_sum > P.l2theta);
-        } else {
-            eB = fast_exp2(sB_p);
-            Nt = fast_log2(sum_p - P.omH * eB);
-            prob = fast_exp2(s0_p) > P.theta * (sum_p - eB);  // p_new = e_0 / (sum - e_{R-1})
-        }
-    };
-    // decision, MAP, events and per-step outputs of the pending step (T2); group-uniform.
-    // vrow must still hold that step's dm (placeholders at pA/pB are never argmax-eligible).
-    auto tail_outputs = [&]() {
-        uint32_t fl = (t_p > 0 && prob) ? 1u : 0u;
-        int r_ex = -1;
-        double dex = -INFINITY;  // dm of the best growth slot, from its key (exact to ~1e-12 rel.)
-        if constexpr (EAGER) {
-            if (key_p != 0ull) {
-                const long long sk = static_cast<long long>(key_p ^ 0x8000000000000000ull);
-                r_ex = int(0xFFF - (sk & 0xFFF));
-                dex = ord_val(sk & ~0xFFFLL) - M_p;  // the eager key is on lp
-            }
-        } else if (fl & P.ev_mask) {  // an event at that step: reduce the argmax from the row
-            unsigned long long kb = 0ull;
-#pragma unroll
-            for (int j = 0; j < J; ++j) {
-                const int p = i + NT * j;
-                if (FULL || p < R) {
-                    int r = tmod_p - p;
-                    r += (r < 0) ? R : 0;
-                    const unsigned long long kk = argmax_key(vrow[p], r);  // dm: same order as lp
-                    kb = (r <= r_elig && kk > kb) ? kk : kb;
-                }
-            }
-            const unsigned hi = unsigned(kb >> 32);
-            const unsigned hmax = __reduce_max_sync(0xffffffffu, hi);
-            const unsigned lmax = __reduce_max_sync(0xffffffffu, hi == hmax ? unsigned(kb) : 0u);
-            kb = (static_cast<unsigned long long>(hmax) << 32) | lmax;
-            if constexpr (NT > 32) {
-                if (lane == 0) gs.red3[w] = kb;
-                group_sync<NT>(g);
-#pragma unroll
-                for (int ww = 0; ww < NT / 32; ++ww) {
-                    const unsigned long long o = gs.red3[ww];
-                    kb = o > kb ? o : kb;
-                }
-                group_sync<NT>(g);  // red3 is reused at the next event step
-            }
-            if (kb != 0ull) {
-                const long long sk = static_cast<long long>(kb ^ 0x8000000000000000ull);
-                r_ex = int(0xFFF - (sk & 0xFFF));
-                dex = ord_val(sk & ~0xFFFLL);  // the on-demand key is on dm
-            }
-        }
-        if (EAGER || (fl & P.ev_mask)) {
-            int rstar;
-            if (merge) {
-                // bucket vb vs the best growth slot d_ex (ties -> the smaller run length)
-                rstar = (r_ex < 0 || vb > dex) ? R - 1 : r_ex + 1;
-            } else {
-                rstar = r_ex + 1;
-            }
-            if (EAGER && t_p > 0 && rstar < min(map_prev + 1, R - 1)) fl |= 2u;
-            map_prev = rstar;
-            if (i == 0 && P.out_map) P.out_map[s * P.ld_o + tl_p] = rstar;
-            if (fl & P.ev_mask) {
-                const double pnew = merge ? (R == 2 ? 1.0 : fast_exp2(s0_p - Nt))
-                                          : fast_exp2(s0_p) * fast_rcp(sum_p - eB);
-                if (i == 0 && ev_count < P.ev_cap) {
-                    EventRec ev;
-                    ev.t = t_p;
-                    ev.cp_index = t_p - rstar + 1;
-                    ev.flags = fl;
-                    ev.pad = 0;
-                    ev.p_new = pnew;
-                    P.ev[s * P.ev_cap + ev_count] = ev;
-                }
-                ++ev_count;
-            }
-        }
-        if (i == 0) {
-            if (P.out_pnew)
-                P.out_pnew[s * P.ld_o + tl_p] = merge ? (R == 2 ? 1.0 : fast_exp2(s0_p - Nt))
-                                                      : fast_exp2(s0_p) * fast_rcp(sum_p - eB);
-            if (P.out_logz) P.out_logz[s * P.ld_o + tl_p] = LN2 * ((M_p - n_prev) + Nt);
-        }
-        n_prev = Nt;
-    };
-
     for (int k = 0; k < ntiles; ++k) {
         const int base = k * kTile;
         const int n = min(kTile, P.T - base);
@@ -500,9 +373,6 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             const int tl = base + q;
             const int64_t t = P.t0 + tl;
             const double x = gs.xbuf[buf][q];
-            if (!isfinite(x)) nonfinite = true;
-            // ---- tail values of the previous step (overlaps the cell chains below) ----
-            if (have_prev) tail_values();
             // ---- phase 1: A1 + A2 + A3 ------------------------------------------
             const int ib = tmod - i + R;  // TAB2 index of cell j: ib - NT*j  (= (t - p) mod R, + R)
             double lp[J];
@@ -564,13 +434,6 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     lp[j] = ((FULL || p < R) ? vrow[p] : -INFINITY) + ell;
                 }
             }
-            // the two cells whose row entry is a placeholder: v + l (owner lanes)
-            if (have_prev) {
-                const int pB = (tmod_p + 1 == R) ? 0 : tmod_p + 1;
-                const int pA = (pB + 1 == R) ? 0 : pB + 1;
-                add_lp_pred<J>(lp, pB / NT, (pB % NT) == i, vcp);
-                if (merge) add_lp_pred<J>(lp, pA / NT, (pA % NT) == i, vb);
-            }
             // shift M (max over all cells, high word is enough) and, if EAGER, the argmax key
             int mh = INT_MIN;
             unsigned long long key = 0ull;  // below every real key (biased order)
@@ -600,7 +463,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     gs.red1[w] = EAGER ? key : 0ull;
                     gs.redh[w] = mh;
                 }
-                group_sync<NT>(g);
+                group_sync<NT>(g, P.dbg);
 #pragma unroll
                 for (int ww = 0; ww < NT / 32; ++ww) {
                     mh = max(mh, gs.redh[ww]);
@@ -613,9 +476,6 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 group_sync<NT>(g);
             }
             const double M = ord_hi_val(mh);
-            // ---- decision / MAP / events / outputs of the previous step -------
-            // (vrow still holds that step's dm: this step's phase 2 has not started)
-            if (have_prev && P.dbg != 1) tail_outputs();
             // ---- phase 2: exp + sum, growth (A4, A5): v'_{r+1} = lp_r - M ------------
             // (fast_exp2 staged across groups of G cells; summation order fixed: cell 0..J-1)
             double sum = 0.0;
@@ -660,58 +520,139 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     if (FULL || i + NT * j < R) sum += e;
                 }
             }
-            // the three cells the tail needs are published by their owners; pB (and pA for
-            // MERGE) then get the 0.0 placeholder
-            {
-                const int pB = (tmod + 1 == R) ? 0 : tmod + 1;  // r = R-1 (recycled)
-                const int pA = (pB + 1 == R) ? 0 : pB + 1;      // r = R-2
-                if ((pA % NT) == i) gs.spec[0] = vrow[pA];
-                if ((pB % NT) == i) gs.spec[1] = vrow[pB];
-                if ((tmod % NT) == i) gs.spec[2] = vrow[tmod];
-                if ((pB % NT) == i) vrow[pB] = 0.0;
-                if (merge && (pA % NT) == i) vrow[pA] = 0.0;
-            }
+            // the three cells the tail needs are published by their owners (the row entries of
+            // pA / pB are overwritten by the fix-ups right after the barrier)
+            const int pB = (tmod + 1 == R) ? 0 : tmod + 1;  // r = R-1 (recycled)
+            const int pA = (pB + 1 == R) ? 0 : pB + 1;      // r = R-2
+            if ((pA % NT) == i) gs.spec[0] = vrow[pA];
+            if ((pB % NT) == i) gs.spec[1] = vrow[pB];
+            if ((tmod % NT) == i) gs.spec[2] = vrow[tmod];
             if (P.dbg != 4) {  // dbg 4 (profiling experiment): no warp butterfly
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
             }
             if constexpr (NT > 32) {
                 if (lane == 0) gs.red2[w] = sum;
-                group_sync<NT>(g);
+                group_sync<NT>(g, P.dbg);
                 sum = gs.red2[0];
 #pragma unroll
                 for (int ww = 1; ww < NT / 32; ++ww) sum += gs.red2[ww];
             } else {
                 group_sync<NT>(g);
             }
-            // ---- this step becomes the pending one; the CP cell's statistics reset --------
-            {
-                const int pB = (tmod + 1 == R) ? 0 : tmod + 1;
-                set_stats_pred<J>(mu, be, L, pB / NT, (pB % NT) == i, mu0, beta0, L0);
+            if (P.dbg == 1) {  // profiling experiment: no tail
+                tmod = (tmod + 1 == R) ? 0 : tmod + 1;
+                continue;
             }
-            have_prev = true;
-            sum_p = sum;
-            M_p = M;
-            sA_p = gs.spec[0];
-            sB_p = gs.spec[1];
-            s0_p = gs.spec[2];
-            tmod_p = tmod;
-            tl_p = tl;
-            t_p = t;
-            key_p = key;
+            // ---- the scalar tail (A5-A8), computed UNIFORMLY by every thread -------
+            //   recycled cell pB (r = R-1) -> new CP cell: v = lg H - lg(1-H) + lg(sum), prior stats
+            //   MERGE: cell pA (r = R-2) -> bucket: v = lg(2^dA + 2^dB) = mx + lg(1 + 2^(mn - mx))
+            // (the owners write the new v of the two cells into the row and reset the CP cell's
+            //  statistics; everyone else reads the pre-fix values from gs.spec)
+            const double dA = gs.spec[0], dB = gs.spec[1], d0 = gs.spec[2];
+            const double mx = fmax(dA, dB), mn = fmin(dA, dB);
+            // one log stream for two values: lanes 0-15 lg(sum), lanes 16-31 lg(1 + u)
+            const double u = fast_exp2(mx == -INFINITY ? -INFINITY : mn - mx);
+            const double lgx = fast_log2(lane >= 16 ? 1.0 + u : sum);
+            const double lg_sum = __shfl_sync(0xffffffffu, lgx, 0);
+            const double lb = __shfl_sync(0xffffffffu, lgx, 16);
+            const double vb = (mx == -INFINITY) ? -INFINITY : mx + lb;
+            double Nt, eB = 0.0;
+            bool prob;
+            if (merge) {
+                Nt = lg_sum;
+                // p_new = R(1) / (1 - R(0)) = 2^(d0 - lg sum)  (R(0) = H exactly; R = 2: p_new = 1)
+                prob = (R == 2) ? (1.0 > P.theta) : (d0 - lg_sum > P.l2theta);
+            } else {
+                eB = fast_exp2(dB);
+                Nt = fast_log2(sum - P.omH * eB);
+                prob = fast_exp2(d0) > P.theta * (sum - eB);  // p_new = e_0 / (sum - e_{R-1})
+            }
+            uint32_t fl = (t > 0 && prob) ? 1u : 0u;
+            {
+                const bool ownB = (pB % NT) == i;
+                if (ownB) vrow[pB] = l2H - l2mH + lg_sum;
+                if (merge && (pA % NT) == i) vrow[pA] = vb;
+                set_stats_pred<J>(mu, be, L, pB / NT, ownB, mu0, beta0, L0);
+            }
+            if (!isfinite(x)) nonfinite = true;
+            // ---- MAP run length r* (A7): eager (key reduced at barrier A) or on demand ----
+            int r_ex = -1;
+            if constexpr (EAGER) {
+                if (key != 0ull) {
+                    const long long sk = static_cast<long long>(key ^ 0x8000000000000000ull);
+                    r_ex = int(0xFFF - (sk & 0xFFF));
+                }
+            } else if (fl & P.ev_mask) {  // group-uniform: an event at this step
+                unsigned long long kb = 0ull;
+#pragma unroll
+                for (int j = 0; j < J; ++j) {
+                    const int p = i + NT * j;
+                    if (FULL || p < R) {
+                        int r = tmod - p;
+                        r += (r < 0) ? R : 0;
+                        const unsigned long long kk = argmax_key(vrow[p], r);  // dm: same order as lp
+                        kb = (r <= r_elig && kk > kb) ? kk : kb;
+                    }
+                }
+                const unsigned hi = unsigned(kb >> 32);
+                const unsigned hmax = __reduce_max_sync(0xffffffffu, hi);
+                const unsigned lmax = __reduce_max_sync(0xffffffffu, hi == hmax ? unsigned(kb) : 0u);
+                kb = (static_cast<unsigned long long>(hmax) << 32) | lmax;
+                if constexpr (NT > 32) {
+                    if (lane == 0) gs.red3[w] = kb;
+                    group_sync<NT>(g);
+#pragma unroll
+                    for (int ww = 0; ww < NT / 32; ++ww) {
+                        const unsigned long long o = gs.red3[ww];
+                        kb = o > kb ? o : kb;
+                    }
+                }
+                if (kb != 0ull) {
+                    const long long sk = static_cast<long long>(kb ^ 0x8000000000000000ull);
+                    r_ex = int(0xFFF - (sk & 0xFFF));
+                }
+            }
+            if (EAGER || (fl & P.ev_mask)) {
+                int rstar;
+                if (merge) {
+                    // bucket vb vs the best growth slot d_ex (ties -> the smaller run length)
+                    int pex = tmod - r_ex;
+                    pex += (pex < 0) ? R : 0;
+                    const double dex = r_ex >= 0 ? vrow[pex] : -INFINITY;
+                    rstar = (r_ex < 0 || vb > dex) ? R - 1 : r_ex + 1;
+                } else {
+                    rstar = r_ex + 1;
+                }
+                if (EAGER && t > 0 && rstar < min(map_prev + 1, R - 1)) fl |= 2u;
+                map_prev = rstar;
+                if (i == 0 && P.out_map) P.out_map[s * P.ld_o + tl] = rstar;
+                if (fl & P.ev_mask) {
+                    const double pnew = merge ? (R == 2 ? 1.0 : fast_exp2(d0 - lg_sum))
+                                              : fast_exp2(d0) * fast_rcp(sum - eB);
+                    if (i == 0 && ev_count < P.ev_cap) {
+                        EventRec ev;
+                        ev.t = t;
+                        ev.cp_index = t - rstar + 1;
+                        ev.flags = fl;
+                        ev.pad = 0;
+                        ev.p_new = pnew;
+                        P.ev[s * P.ev_cap + ev_count] = ev;
+                    }
+                    ++ev_count;
+                }
+            }
+            if (i == 0) {
+                if (P.out_pnew)
+                    P.out_pnew[s * P.ld_o + tl] = merge ? (R == 2 ? 1.0 : fast_exp2(d0 - lg_sum))
+                                                        : fast_exp2(d0) * fast_rcp(sum - eB);
+                if (P.out_logz) P.out_logz[s * P.ld_o + tl] = LN2 * ((M - n_prev) + Nt);
+            }
+            n_prev = Nt;
             tmod = (tmod + 1 == R) ? 0 : tmod + 1;
         }
     }
-    // ---- epilogue: finish the last step, finalise the row, spill -----------------
-    if (have_prev) {
-        tail_values();
-        const int pB = (tmod_p + 1 == R) ? 0 : tmod_p + 1;
-        const int pA = (pB + 1 == R) ? 0 : pB + 1;
-        tail_outputs();
-        group_sync<NT>(g);  // every read of the pending step's row is done
-        if ((pB % NT) == i) vrow[pB] = vcp;
-        if (merge && (pA % NT) == i) vrow[pA] = vb;
-    }
+    // ---- spill (with the pending fix-ups applied) ----------------------------
     group_sync<NT>(g);
 #pragma unroll
     for (int j = 0; j < J; ++j) {
