@@ -98,7 +98,7 @@ __global__ void init_scalars_kernel(SeriesScalars* scal, const double* mu0, cons
         SeriesScalars sc;
         sc.mu0 = mu0[s];
         sc.beta0 = beta0[s];
-        sc.n_prev = 0.0;
+        sc.s_prev = 1.0;
         sc.map_prev = 0;
         sc.ev_count = 0;
         sc.flags = 0;
@@ -108,15 +108,15 @@ __global__ void init_scalars_kernel(SeriesScalars* scal, const double* mu0, cons
     }
 }
 
-__global__ void init_state_kernel(double* mu, double* beta, double* v, const SeriesScalars* scal, int64_t S,
-                                  int R, double v0) {
+__global__ void init_state_kernel(double* mu, double* beta, double* q, const SeriesScalars* scal, int64_t S,
+                                  int R) {
     const int64_t n = S * int64_t(R);
     for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
         const int64_t s = k / R;
         const int p = int(k - s * R);
         mu[k] = scal[s].mu0;
         beta[k] = scal[s].beta0;
-        v[k] = (p == 0) ? v0 : -INFINITY;
+        q[k] = (p == 0) ? 1.0 : 0.0;
     }
 }
 
@@ -181,10 +181,10 @@ __global__ void drain_gather_kernel(SeriesScalars* scal, const EventRec* ev, int
     if (reset && lane == 0) scal[s].ev_count = 0;
 }
 
-// Ring position order -> run-length order; log R = v - N_t.
-__global__ void posterior_kernel(const double* mu, const double* beta, const double* v,
+// Ring position order -> run-length order; R_t(r) = q_r s_t.
+__global__ void posterior_kernel(const double* mu, const double* beta, const double* q,
                                  const SeriesScalars* scal, int64_t s0, int64_t count, int R, int64_t t,
-                                 double l2mH, double* logR_out, double* mu_out, double* beta_out) {
+                                 double* logR_out, double* mu_out, double* beta_out) {
     const int64_t n = count * int64_t(R);
     const int tm = int(t % R);
     for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
@@ -193,7 +193,7 @@ __global__ void posterior_kernel(const double* mu, const double* beta, const dou
         int p = tm - r;
         if (p < 0) p += R;
         const int64_t src = (s0 + i) * int64_t(R) + p;
-        if (logR_out) logR_out[k] = fbocd::LN2 * ((v[src] + l2mH) - scal[s0 + i].n_prev);
+        if (logR_out) logR_out[k] = log(q[src] * scal[s0 + i].s_prev);
         if (mu_out) mu_out[k] = mu[src];
         if (beta_out) beta_out[k] = beta[src];
     }
@@ -355,15 +355,14 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
     falcon_bocd_predictive_constants(R, c.kappa0, c.alpha0, tc.data(), ta.data(), tg.data(), tk.data());
     std::vector<double2> ca(R), gk(R);
     {
-        // base-2 units: the device table holds c_r / ln2 + log2(1-H) (bocd_kernel.cuh, A2-A3)
-        const long double l1mh = log2l(1.0L - (long double)c.hazard);
+        // base-2 units: the device table holds c_r / ln2 (bocd_kernel.cuh, A2)
         const long double inv_ln2 = 1.442695040888963407359924681001892137L;
         long double D = lgammal((long double)c.alpha0 + 0.5L) - lgammal((long double)c.alpha0);
         const long double two_pi = 6.283185307179586476925286766559005768L;
         for (int r = 0; r < R; ++r) {
             const long double kap = (long double)c.kappa0 + r;
             const long double cr = D - 0.5L * logl(two_pi * (kap + 1.0L) / kap);
-            ca[r] = make_double2((double)(cr * inv_ln2 + l1mh), ta[r]);
+            ca[r] = make_double2((double)(cr * inv_ln2), ta[r]);
             gk[r] = make_double2(tg[r], tk[r]);
             D = logl((long double)c.alpha0 + 0.5L * r) - D;
         }
@@ -404,8 +403,7 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
     if (e3 == cudaSuccess) e3 = cudaMemset(h->d_err, 0, sizeof(unsigned));
     if (e3 == cudaSuccess) {
         init_scalars_kernel<<<grid_for(S, 256), 256>>>(h->d_scal, dmu0, dbeta0, S);
-        init_state_kernel<<<grid_for(int64_t(SR), 256), 256>>>(h->d_mu, h->d_beta, h->d_v, h->d_scal, S, R,
-                                                                 -(double)log2l(1.0L - (long double)c.hazard));
+        init_state_kernel<<<grid_for(int64_t(SR), 256), 256>>>(h->d_mu, h->d_beta, h->d_v, h->d_scal, S, R);
         e3 = cudaGetLastError();
     }
     if (e3 == cudaSuccess) e3 = cudaDeviceSynchronize();
@@ -426,11 +424,10 @@ static int launch_update(falcon_bocd_t h, const double* x_dev, int64_t ld, int64
         std::memset(&P, 0, sizeof(P));
         P.R = c.R;
         P.S = c.n_series;
-        P.l2H = (double)log2l((long double)c.hazard);
-        P.l2mH = (double)log2l(1.0L - (long double)c.hazard);
+        P.H = c.hazard;
         P.omH = 1.0 - c.hazard;
+        P.hr = (double)((long double)c.hazard / (1.0L - (long double)c.hazard));
         P.theta = c.threshold;
-        P.l2theta = c.threshold > 0.0 ? std::log2(c.threshold) : -INFINITY;
         P.alpha0 = c.alpha0;
         P.prior_cov = c.prior_cov;
         P.mode = c.trunc_mode;
@@ -442,7 +439,7 @@ static int launch_update(falcon_bocd_t h, const double* x_dev, int64_t ld, int64
         P.fm = h->d_fm;
         P.st_mu = h->d_mu;
         P.st_beta = h->d_beta;
-        P.st_v = h->d_v;
+        P.st_q = h->d_v;
         P.scal = h->d_scal;
         P.ev = h->d_ev;
         P.err = h->d_err;
@@ -455,10 +452,6 @@ static int launch_update(falcon_bocd_t h, const double* x_dev, int64_t ld, int64
         P.out_logz = ologz ? ologz + done : nullptr;
         P.ld_o = ld_o;
         P.tma_ok = ((reinterpret_cast<uintptr_t>(P.x) & 15u) == 0) && ((ld & 1) == 0);
-        {
-            const char* dbg = getenv("FALCON_BOCD_DEBUG");  // profiling experiments only
-            P.dbg = dbg ? atoi(dbg) : 0;
-        }
         const int64_t grid = (c.n_series + h->var.spb - 1) / h->var.spb;
         void* args[] = {&P};
         // r* every step only when it is an output (per-step MAP, MAPRESET events); otherwise
@@ -649,8 +642,7 @@ int falcon_bocd_read_posterior(falcon_bocd_t h, int64_t s0, int64_t count, doubl
         dst[k] = is_device_ptr(outs[k]) ? outs[k] : tmp + k * n;
     }
     posterior_kernel<<<grid_for(int64_t(n), 256), 256, 0, st>>>(h->d_mu, h->d_beta, h->d_v, h->d_scal, s0, count, R,
-                                                                h->t, (double)log2l(1.0L - (long double)h->cfg.hazard), dst[0], dst[1],
-                                                                dst[2]);
+                                                                h->t, dst[0], dst[1], dst[2]);
     cudaError_t e = cudaGetLastError();
     for (int k = 0; k < 3 && e == cudaSuccess; ++k)
         if (outs[k] && dst[k] != outs[k])

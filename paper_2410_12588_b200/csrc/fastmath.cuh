@@ -121,6 +121,34 @@ __device__ __forceinline__ double fast_exp2(double x) {
     return fma(Ts, q, Ts);
 }
 
+// 2^x for the probability-domain recursion: exactly 0 below -1021 (a cell 2^1021 below
+// the change-point cell can never matter again in fp64: it would need a likelihood
+// ratio beyond the double range to come back; reading documented in DESIGN.md), and
+// the argument clamped at +1000 (a posterior predictive 2^1000 denser than the prior
+// predictive: not reachable with finite data scales, guards the range).
+__device__ __forceinline__ double fast_exp2_zero(double x) {
+    const int hx = __double2hiint(x);
+    const bool dead = static_cast<unsigned>(hx) > 0xC08FE800u;  // x < -1021 (or -inf / negative NaN)
+    int xh = int(min(unsigned(hx), 0xC08FE800u));
+    xh = min(xh, 0x408F4000);  // x <= 1000
+    const double xc = __hiloint2double(xh, __double2loint(x));
+    const double zf = fma(xc, c_fm[13], c_fm[7]);  // round(64 x) in the low word (1.5 * 2^52 shift)
+    const int ki = __double2loint(zf);
+    const double kd = zf - c_fm[7];
+    const double r = fma(kd, c_fm[14], xc);  // exact: |r| <= 1/128
+    double p = fma(r, c_fm[8], c_fm[9]);
+    p = fma(p, r, c_fm[10]);
+    p = fma(p, r, c_fm[11]);
+    p = fma(p, r, c_fm[12]);
+    const double q = p * r;
+    const double T =
+        *reinterpret_cast<const double*>(reinterpret_cast<const char*>(g_fm.exptab) + ((ki << 3) & 0x1F8));
+    int th;
+    asm("mad.lo.s32 %0, %1, 1048576, %2;" : "=r"(th) : "r"(ki >> 6), "r"(__double2hiint(T)));
+    const double Ts = __hiloint2double(th, __double2loint(T));
+    return dead ? 0.0 : fma(Ts, q, Ts);
+}
+
 // 1/x to ~1 ulp for positive normal x: MUFU seed + one Newton step (no IEEE division path).
 __device__ __forceinline__ double fast_rcp(double x) {
     double r;
