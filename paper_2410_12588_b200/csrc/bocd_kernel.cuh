@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             }
             if (i == 0) {
                 if (P.out_pnew) P.out_pnew[s * P.ld_o + tl] = pnum * fast_rcp(Zp);
-                if (P.out_logz) P.out_logz[s * P.ld_o + tl] = LN2 * (l0 + fast_log2(Z));
+                if (P.out_logz) P.out_logz[s * P.ld_o + tl] = LN2 * (l0 + fast_log2(Zd));  // kept mass
             }
             s_prev = s_new;
             tmod = (tmod + 1 == R) ? 0 : tmod + 1;
