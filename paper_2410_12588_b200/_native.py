@@ -9,7 +9,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfalcon_bocd.so")
+# FALCON_BOCD_LIB: load an alternative build of the same library (A/B tuning runs only)
+LIB_PATH = os.environ.get("FALCON_BOCD_LIB") or os.path.join(HERE, "libfalcon_bocd.so")
 
 FALCON_OK = 0
 FALCON_WARN_EVENTS_DROPPED = 1

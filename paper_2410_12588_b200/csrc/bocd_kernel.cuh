@@ -9,20 +9,29 @@
 // exactly the one that becomes the new change-point cell.  Per-r constants of
 // the Student-t predictive come from a shared-memory table indexed by r.
 //
-// The recursion runs in the PROBABILITY domain with one scale factor per series
-// (the posterior is R_t(r) = q_r * s_t), so a step needs ONE group reduction (the
-// evidence Z) and a tail without transcendentals.  Predictive densities are
-// evaluated in base-2 log units with the branch-free fast_log2 / fast_exp2 of
-// fastmath.cuh (9 FP64 instructions each) and exponentiated against the prior
-// predictive l0 of the same observation (so the change-point cell's factor is
-// exactly 1 and Z >= H > 0).  All fp64, no fast-math.  Per step:
-//   A1  NIG update            mu' = mu + d/(kappa+1),  beta' = beta + kappa d^2 / (2(kappa+1))
+// The recursion runs in the PROBABILITY domain: the row q is the run-length
+// posterior up to one per-series factor, R_t(r) = q_r (1-H) / Zd_t, so a step
+// needs ONE group reduction (the evidence Z) and a scalar tail without
+// transcendentals.  Predictive densities are evaluated in base-2 log units with
+// branch-free table-driven log2 / exp2 (fastmath.cuh), and every cell is
+// exponentiated against a per-step integer reference N_t = K0_t + z_{t-1}:
+//   K0_t = round(l0_t), l0_t the prior predictive of x_t (log2; the change-point
+//          cell's density, so Z >= H 2^(l0-K0-z) never underflows), computed for a
+//          whole x tile at once;
+//   z_{t-1} = the binary exponent of Zd_{t-1}, which renormalises the row by an
+//          exact power of two instead of a multiply per cell.
+// N_t enters the exp2 range reduction as an exact integer shift of its rounding
+// constant, so the per-cell cost of both is zero.  All fp64, no fast-math.
+// Per step:
+//   A1  NIG update            mu' = mu + d y_r,  beta' = beta + d (x - mu')/2   (d = x - mu,
+//                             y_r = 1/(kappa_r+1): d (x - mu')/2 = kappa_r d^2 / (2(kappa_r+1)))
 //   A2  Student-t predictive  l_r = c_r/ln2 + alpha_r (lg beta - lg beta') - 1/2 lg beta'  (lg = log2;
 //                             = [c_r - 1/2 log beta - (alpha_r+1/2) log1p(kappa d^2/(2 beta (kappa+1)))]/ln2)
-//   A3  joint                 q'_r = (q_r s_{t-1}) 2^(l_r - l0)          (= R_{t-1}(r) pred_r / 2^l0)
+//   A3  joint                 q'_r = q_r 2^(l_r - N_t)        (= R_{t-1}(r) pred_r x (step constant))
 //   A4  evidence              Z = sum_r q'_r  (per-thread sums, xor butterfly, fixed-order
-//                             cross-warp sum: deterministic);  log Z_t = ln2 (l0 + lg Z)
-//   A5  normalisation         s_t = (1-H)/Zd, Zd = Z (MERGE) or Z - (1-H) q'_{R-1} (DROP); slot r+1 <- q'_r
+//                             cross-warp sum: deterministic);
+//                             log Z_t = ln2 (K0_t + z_{t-1} + lg Zd_t - lg Zd_{t-1}) + ln(1-H)
+//   A5  normalisation         Zd = Z (MERGE) or Z - (1-H) q'_{R-1} (DROP); slot r+1 <- q'_r
 //   A6  change point / MERGE  new CP cell (recycled position): q = H Z/(1-H), prior statistics;
 //                             MERGE bucket: q = q'_{R-2} + q'_{R-1};  DROP: q'_{R-1} dropped
 //   A7  decision, MAP         p_new = R_t(1)/(1-R_t(0)) = q'_0/Z (MERGE) or q'_0/(Z - q'_{R-1}) (DROP);
@@ -32,6 +41,8 @@
 // q lives in a per-series shared-memory row; mu, beta, lg beta live in registers
 // for the whole call; x is staged in double-buffered shared-memory tiles by 1-D
 // TMA bulk copies (cp.async.bulk + mbarrier); state is spilled to HBM once per call.
+// The cell loop is written stage-major over groups of kG cells (every stage of a
+// group before the next stage) so the dependent FP64 chains of kG cells interleave.
 #pragma once
 
 #include <climits>
@@ -43,11 +54,14 @@
 namespace fbocd {
 
 constexpr int kTile = 256;  // x steps per shared-memory tile (2 KB)
-constexpr int kG = 4;       // cells per interleaved group (ILP)
+#ifndef FALCON_BOCD_KG
+#define FALCON_BOCD_KG 4
+#endif
+constexpr int kG = FALCON_BOCD_KG;  // cells per interleaved group (ILP)
 
 struct SeriesScalars {  // per-series state carried between calls (HBM), 48 B
     double mu0, beta0;  // prior (set from x_0 when prior_first_obs)
-    double s_prev;      // s_{t-1}: R_{t-1}(r) = q_r * s_{t-1}
+    double zd_prev;     // Zd_{t-1}: R_{t-1}(r) = q_r (1-H) / Zd_{t-1}  (1-H before the first step)
     int32_t map_prev;   // r*_{t-1}
     int32_t ev_count;   // events appended since the last drain (may exceed capacity)
     int32_t flags;      // bit0: non-finite observation seen; bit1: bad prior
@@ -67,12 +81,13 @@ struct KParams {
     int R;
     int64_t S;
     double H, omH, hr, theta, alpha0, prior_cov;  // omH = 1-H, hr = H/(1-H)
+    double ln_omH;                                // log(1-H)
     int mode;                                     // 0 MERGE, 1 DROP
     int prior_first_obs;
     uint32_t ev_mask;
     int ev_cap;
     const double2* tab_ca;     // [R] {c_r / ln2, alpha_r}
-    const double2* tab_gk;     // [R] {kappa_r/(2(kappa_r+1)), 1/(kappa_r+1)}
+    const double* tab_y;       // [R] y_r = 1/(kappa_r+1)
     const FastMathTables* fm;  // log2 / exp2 tables
     double* st_mu;             // [S][R] position order
     double* st_beta;
@@ -94,11 +109,14 @@ struct KParams {
 template <int NT>
 struct __align__(16) GroupSmem {
     double xbuf[2][kTile];
-    double red2[NT / 32 > 0 ? NT / 32 : 1];
-    unsigned long long red1[NT / 32 > 0 ? NT / 32 : 1];  // EAGER argmax keys
-    unsigned long long red3[NT / 32 > 0 ? NT / 32 : 1];  // on-demand argmax (event steps)
-    double spec[4];                                       // q' of the cells r = R-2, R-1, 0
-    double mu0, beta0, L0, s_prev;
+    int kbuf[2][kTile];  // K0_t = round(l0_t) of the tile's steps
+    // red2 / red1 / spec are double-buffered by step parity: a warp that runs ahead into
+    // step t+1 cannot overwrite what a slower warp still reads after barrier t
+    double red2[2][NT / 32 > 0 ? NT / 32 : 1];
+    unsigned long long red1[2][NT / 32 > 0 ? NT / 32 : 1];  // EAGER argmax keys
+    unsigned long long red3[NT / 32 > 0 ? NT / 32 : 1];     // on-demand argmax (event steps)
+    double spec[2][4];                                       // q' of the cells r = R-2, R-1, 0
+    double mu0, beta0, L0, zd_prev;
     int map_prev, ev_count, flags, pad;
     unsigned long long mbar[2];
 };
@@ -195,38 +213,36 @@ __host__ __device__ constexpr size_t group_bytes(int R) {
     return sizeof(GroupSmem<NT>) + ((size_t(R) * sizeof(double) + 15) & ~size_t(15));  // keep 16-B alignment
 }
 __host__ __device__ constexpr size_t table_bytes(int R, bool tab2) {
-    return size_t(R) * (tab2 ? 2 : 1) * 2 * sizeof(double2);
+    return (size_t(R) * (tab2 ? 2 : 1) * (sizeof(double2) + sizeof(double)) + 15) & ~size_t(15);
 }
 
-// Resets one cell's NIG statistics to the prior under a lane predicate.  j is
-// group-uniform, so the switch never diverges.
+// Resets one cell's NIG statistics to the prior (called by the owning thread only;
+// j is uniform within the thread, so this is a plain jump table).
 template <int J>
-__device__ __forceinline__ void set_stats_pred(double (&mu)[J], double (&be)[J], double (&L)[J], int j, bool pred,
-                                               double m, double b, double l) {
-#define FBOCD_SETS(k)                     \
-    case k:                               \
-        if constexpr (J > k) {            \
-            if (pred) {                   \
-                mu[k] = m;                \
-                be[k] = b;                \
-                L[k] = l;                 \
-            }                             \
-        }                                 \
+__device__ __forceinline__ void set_stats(double (&mu)[J], double (&be)[J], double (&L)[J], int j, double m,
+                                          double b, double l) {
+#define FBOCD_SETS(k)          \
+    case k:                    \
+        if constexpr (J > k) { \
+            mu[k] = m;         \
+            be[k] = b;         \
+            L[k] = l;          \
+        }                      \
         break;
     switch (j) { FBOCD_SETS(0) FBOCD_SETS(1) FBOCD_SETS(2) FBOCD_SETS(3) FBOCD_SETS(4) FBOCD_SETS(5) FBOCD_SETS(6) FBOCD_SETS(7)
                  FBOCD_SETS(8) FBOCD_SETS(9) FBOCD_SETS(10) FBOCD_SETS(11) FBOCD_SETS(12) FBOCD_SETS(13) FBOCD_SETS(14) FBOCD_SETS(15) }
 #undef FBOCD_SETS
 }
 
-// Student-t predictive in log2 units of one cell (A1 + A2); the cell loop and the
-// prior-predictive reference both use it, so the change-point cell's l - l0 is 0 exactly.
-__device__ __forceinline__ double predictive_l2(double x, double mu, double be, double L, double2 ca, double2 gk,
-                                                double& bn, double& mun, double& Ln) {
-    const double d = x - mu;
-    bn = fma(gk.x * d, d, be);
-    mun = fma(d, gk.y, mu);
-    Ln = fast_log2(bn);
-    return fma(-0.5, Ln, fma(ca.y, L - Ln, ca.x));
+// Student-t predictive (A1 + A2) of the prior at x, log2 units: the tile's
+// exponent references K0_t = round(l0_t).
+__device__ __forceinline__ double prior_l2(double x, double mu0, double be0, double L0, double2 ca0, double y0,
+                                           unsigned fmb) {
+    const double d = x - mu0;
+    const double mun = fma(d, y0, mu0);
+    const double bn = fma(d, fma(mun, -0.5, 0.5 * x), be0);
+    const double Ln = fast_log2(bn, fmb);
+    return fma(-0.5, Ln, fma(ca0.y, L0 - Ln, ca0.x));
 }
 
 // ---------------------------------------------------------------------------
@@ -242,16 +258,18 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int R = FULL ? NT * J : P.R;
     const int RT = TAB2 ? 2 * R : R;
-    double2* s_ca = reinterpret_cast<double2*>(smem_raw);
-    double2* s_gk = s_ca + RT;
-    unsigned char* gbase = reinterpret_cast<unsigned char*>(s_gk + RT);
+    // dynamic shared memory: [fast-math tables (aligned in kFmSmemBytes)][per-r tables][groups]
+    double2* s_ca = reinterpret_cast<double2*>(smem_raw + kFmSmemBytes);
+    double* s_y = reinterpret_cast<double*>(s_ca + RT);
+    unsigned char* gbase = smem_raw + kFmSmemBytes + table_bytes(R, TAB2);
 
     for (int k = threadIdx.x; k < RT; k += blockDim.x) {
         const int r = k < R ? k : k - R;
         s_ca[k] = P.tab_ca[r];
-        s_gk[k] = P.tab_gk[r];
+        s_y[k] = P.tab_y[r];
     }
-    load_fastmath(P.fm);
+    const unsigned fmb = fm_setup(smem_raw, P.fm);  // logtab, 2048-B aligned
+    const unsigned emb = fmb + 2048u;                // exptab, 512-B aligned
     const int g = threadIdx.x / NT;
     const int i = threadIdx.x % NT;
     const int lane = threadIdx.x & 31;
@@ -285,21 +303,22 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 sc.mu0 = x0;
                 sc.beta0 = P.alpha0 * (P.prior_cov * x0) * (P.prior_cov * x0);
             }
-            sc.s_prev = 1.0;
+            sc.zd_prev = P.omH;  // R_{-1} = [1, 0, ...] = q (1-H)/Zd
             sc.map_prev = 0;
         }
         const bool ok = sc.beta0 >= 2.2250738585072014e-308 && sc.beta0 < 1e300 && isfinite(sc.mu0);
         gs.mu0 = sc.mu0;
         gs.beta0 = ok ? sc.beta0 : 1.0;
-        gs.L0 = fast_log2(gs.beta0);
-        gs.s_prev = sc.s_prev;
+        gs.L0 = fast_log2(gs.beta0, fmb);
+        gs.zd_prev = sc.zd_prev;
         gs.map_prev = sc.map_prev;
         gs.ev_count = sc.ev_count;
         gs.flags = sc.flags | (ok ? 0 : 2);
     }
     group_sync<NT>(g);
     const double mu0 = gs.mu0, beta0 = gs.beta0, L0 = gs.L0;
-    double s_prev = gs.s_prev;  // per-series scalars are group-uniform registers
+    double zd_prev = gs.zd_prev;  // per-series scalars are group-uniform registers
+    int zexp = ((__double2hiint(zd_prev) >> 20) & 0x7FF) - 1023;  // binary exponent of Zd_{t-1}
     int map_prev = gs.map_prev, ev_count = gs.ev_count;
 #pragma unroll
     for (int j = 0; j < J; ++j) {
@@ -314,7 +333,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 mu[j] = P.st_mu[sbase + p];
                 be[j] = P.st_beta[sbase + p];
                 qrow[p] = P.st_q[sbase + p];
-                L[j] = fast_log2(be[j]);
+                L[j] = fast_log2(be[j], fmb);
             }
         } else {
             mu[j] = mu0;
@@ -322,14 +341,17 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             L[j] = L0;
         }
     }
-    // table entries of r = 0 (the prior-predictive reference)
-    const double2 ca0 = s_ca[0], gk0 = s_gk[0];
+    // table entries of r = 0 (the prior predictive)
+    const double2 ca0 = s_ca[0];
+    const double y0 = s_y[0];
 
     const bool merge = (P.mode == 0);
     // argmax-eligible run lengths: MERGE r <= R-3 (slot R-1 is the bucket), DROP r <= R-2
     const int r_elig = merge ? R - 3 : R - 2;
     int tmod = int(P.t0 % R);  // ring bookkeeping: t mod R
     bool nonfinite = false;
+    // lg Zd_{t-1} for the log-evidence output (thread 0 only)
+    double lzd_prev = (i == 0 && P.out_logz) ? fast_log2(zd_prev, fmb) : 0.0;
 
     for (int k = 0; k < ntiles; ++k) {
         const int base = k * kTile;
@@ -344,15 +366,24 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             for (int q = i; q < n; q += NT) gs.xbuf[buf][q] = xrow[base + q];
             group_sync<NT>(g);
         }
+        // the tile's exponent references K0_t = round(l0_t), spread over the group
+        for (int q = i; q < n; q += NT) {
+            const double xq = gs.xbuf[buf][q];
+            if (!isfinite(xq)) nonfinite = true;
+            const double l0 = prior_l2(xq, mu0, beta0, L0, ca0, y0, fmb);
+            gs.kbuf[buf][q] = __double2int_rn(fmin(fmax(l0, -1048576.0), 1048576.0));
+        }
+        group_sync<NT>(g);
         for (int q = 0; q < n; ++q) {
             const int tl = base + q;
             const int64_t t = P.t0 + tl;
             const double x = gs.xbuf[buf][q];
-            if (!isfinite(x)) nonfinite = true;
-            // reference l0: the prior predictive of x_t (group-uniform)
-            double bn0, mun0, Ln0;
-            const double l0 = predictive_l2(x, mu0, beta0, L0, ca0, gk0, bn0, mun0, Ln0);
-            // ---- A1-A4 for the J cells (groups of G, stages written across the group) ----
+            const double hx = 0.5 * x;
+            const int K0 = gs.kbuf[buf][q];
+            // exp2 rounding constant 1.5*2^52 + 2^31 - 64 N_t: zf = fma(l, 64, C7) holds
+            // round(64 l) - 64 N_t + 2^31 in its low word (exact integers below 2^52)
+            const double C7 = __hiloint2double(0x43380000, int(0x80000000u - unsigned(K0 + zexp) * 64u));
+            // ---- A1-A4 for the J cells (groups of G, every stage across the group) ----
             const int ib = tmod - i + R;  // TAB2 index of cell j: ib - NT*j  (= (t - p) mod R, + R)
             double sum = 0.0;
             unsigned long long key = 0ull;
@@ -360,9 +391,10 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             for (int j0 = 0; j0 < J; j0 += kG) {
                 constexpr int G = (J < kG) ? J : kG;
                 int idx[G];
-                double ell[G];
+                double2 ca[G];
+                double yv[G], qv[G], d[G], bn[G];
 #pragma unroll
-                for (int kk = 0; kk < G; ++kk) {  // A1 + A2
+                for (int kk = 0; kk < G; ++kk) {  // table + row loads
                     const int j = j0 + kk;
                     const int p = i + NT * j;
                     if (TAB2) {
@@ -374,18 +406,80 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                         idx[kk] += (idx[kk] < 0) ? R : 0;
                     }
                     if (!FULL && p >= R) idx[kk] = 0;  // masked cell: any valid entry
-                    double bn, mun, Ln;
-                    ell[kk] = predictive_l2(x, mu[j], be[j], L[j], s_ca[idx[kk]], s_gk[idx[kk]], bn, mun, Ln);
-                    be[j] = bn;
-                    mu[j] = mun;
-                    L[j] = Ln;
+                    ca[kk] = s_ca[idx[kk]];
+                    yv[kk] = s_y[idx[kk]];
+                    qv[kk] = (FULL || p < R) ? qrow[p] : 0.0;
+                }
+                // A1: NIG update
+#pragma unroll
+                for (int kk = 0; kk < G; ++kk) d[kk] = x - mu[j0 + kk];
+#pragma unroll
+                for (int kk = 0; kk < G; ++kk) mu[j0 + kk] = fma(d[kk], yv[kk], mu[j0 + kk]);
+#pragma unroll
+                for (int kk = 0; kk < G; ++kk) bn[kk] = fma(d[kk], fma(mu[j0 + kk], -0.5, hx), be[j0 + kk]);
+                // A2: lg beta' (fast_log2 of fastmath.cuh, stage by stage)
+                unsigned tb[G];
+                double2 lt[G];
+                double rl[G], kt[G], pl[G];
+#pragma unroll
+                for (int kk = 0; kk < G; ++kk) {
+                    tb[kk] = unsigned(__double2hiint(bn[kk])) + 0x00196000u;
+                    lt[kk] = lds_v2f64(((tb[kk] >> 9) & 0x7F0u) | fmb);
                 }
 #pragma unroll
-                for (int kk = 0; kk < G; ++kk) {  // A3 + A4
+                for (int kk = 0; kk < G; ++kk) {
+                    const double invs = __hiloint2double(
+                        __double2hiint(lt[kk].x) + 0x40000000 - int(tb[kk] & 0xFFF00000u), __double2loint(lt[kk].x));
+                    rl[kk] = fma(bn[kk], invs, -1.0);
+                    kt[kk] = (__hiloint2double(0x43300000, int(tb[kk] >> 20)) - c_fm[6]) + lt[kk].y;
+                }
+#pragma unroll
+                for (int kk = 0; kk < G; ++kk) pl[kk] = fma(rl[kk], c_fm[0], c_fm[1]);
+#pragma unroll
+                for (int c = 2; c <= 5; ++c) {
+#pragma unroll
+                    for (int kk = 0; kk < G; ++kk) pl[kk] = fma(pl[kk], rl[kk], c_fm[c]);
+                }
+                double ell[G];
+#pragma unroll
+                for (int kk = 0; kk < G; ++kk) {
+                    const int j = j0 + kk;
+                    const double Ln = fma(rl[kk], pl[kk], kt[kk]);
+                    ell[kk] = fma(-0.5, Ln, fma(ca[kk].y, L[j] - Ln, ca[kk].x));
+                    L[j] = Ln;
+                    be[j] = bn[kk];
+                }
+                // A3: q' = q 2^(l - N_t)  (fast_exp2 with the shifted rounding constant)
+                double re[G], pe[G], Tv[G];
+                unsigned ki[G];
+#pragma unroll
+                for (int kk = 0; kk < G; ++kk) {
+                    const double zf = fma(ell[kk], 64.0, C7);
+                    ki[kk] = unsigned(__double2loint(zf));
+                    re[kk] = fma(zf - C7, -0.015625, ell[kk]);  // exact, |re| <= 1/128
+                    Tv[kk] = lds_f64(((ki[kk] << 3) & 0x1F8u) | emb);
+                }
+#pragma unroll
+                for (int kk = 0; kk < G; ++kk) pe[kk] = fma(re[kk], c_fm[8], c_fm[9]);
+#pragma unroll
+                for (int c = 10; c <= 12; ++c) {
+#pragma unroll
+                    for (int kk = 0; kk < G; ++kk) pe[kk] = fma(pe[kk], re[kk], c_fm[c]);
+                }
+#pragma unroll
+                for (int kk = 0; kk < G; ++kk) {
                     const int j = j0 + kk;
                     const int p = i + NT * j;
+                    const double qq = pe[kk] * re[kk];
+                    // 2^e, e = floor(n/64) for n = ki - 2^31: exactly 0 below 2^-1021, e clamped
+                    // at +1000; the 2^31 offset vanishes mod 2^32 in the exponent field
+                    const bool dead = ki[kk] < 0x80000000u - 65344u;
+                    const unsigned kc = min(ki[kk], 0x80000000u + 64063u);
+                    const double Ts =
+                        __hiloint2double(int((kc >> 6) << 20) + __double2hiint(Tv[kk]), __double2loint(Tv[kk]));
+                    const double E = dead ? 0.0 : fma(Ts, qq, Ts);
                     if (FULL || p < R) {
-                        const double qn = (qrow[p] * s_prev) * fast_exp2_zero(ell[kk] - l0);
+                        const double qn = qv[kk] * E;
                         qrow[p] = qn;
                         sum += qn;
                         if constexpr (EAGER) {
@@ -399,28 +493,29 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             }
             // the three cells the tail needs are published by their owners (pB / pA are
             // overwritten right after the barrier)
+            const int par = tl & 1;
             const int pB = (tmod + 1 == R) ? 0 : tmod + 1;  // r = R-1 (recycled)
             const int pA = (pB + 1 == R) ? 0 : pB + 1;      // r = R-2
-            if ((pA % NT) == i) gs.spec[0] = qrow[pA];
-            if ((pB % NT) == i) gs.spec[1] = qrow[pB];
-            if ((tmod % NT) == i) gs.spec[2] = qrow[tmod];
+            if ((pA % NT) == i) gs.spec[par][0] = qrow[pA];
+            if ((pB % NT) == i) gs.spec[par][1] = qrow[pB];
+            if ((tmod % NT) == i) gs.spec[par][2] = qrow[tmod];
             // ---- group sum (and, EAGER, argmax): the step's only barrier ----------------
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
             if constexpr (EAGER) key = warp_max_u64(key);
             if constexpr (NT > 32) {
                 if (lane == 0) {
-                    gs.red2[w] = sum;
-                    if (EAGER) gs.red1[w] = key;
+                    gs.red2[par][w] = sum;
+                    if (EAGER) gs.red1[par][w] = key;
                 }
                 group_sync<NT>(g);
-                sum = gs.red2[0];
+                sum = gs.red2[par][0];
 #pragma unroll
-                for (int ww = 1; ww < NT / 32; ++ww) sum += gs.red2[ww];
+                for (int ww = 1; ww < NT / 32; ++ww) sum += gs.red2[par][ww];
                 if constexpr (EAGER) {
 #pragma unroll
                     for (int ww = 0; ww < NT / 32; ++ww) {
-                        const unsigned long long o = gs.red1[ww];
+                        const unsigned long long o = gs.red1[par][ww];
                         key = o > key ? o : key;
                     }
                 }
@@ -429,17 +524,18 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             }
             // ---- the scalar tail (A5-A8): group-uniform, no transcendentals ---------------
             const double Z = sum;
-            const double qA = gs.spec[0], qB = gs.spec[1], q0 = gs.spec[2];
+            const double qA = gs.spec[par][0], qB = gs.spec[par][1], q0 = gs.spec[par][2];
             const double Zd = merge ? Z : Z - P.omH * qB;       // normaliser of the new posterior
             const double Zp = merge ? Z : Z - qB;               // p_new = pnum / Zp
             const double pnum = (merge && R == 2) ? Z : q0;     // MERGE R = 2: p_new = 1
-            const double s_new = P.omH * fast_rcp(Zd);
             uint32_t fl = (t > 0 && pnum > P.theta * Zp) ? 1u : 0u;
             {
                 const bool ownB = (pB % NT) == i;
-                if (ownB) qrow[pB] = P.hr * Z;                    // R_t(0) = H Z / Zd
+                if (ownB) {
+                    qrow[pB] = P.hr * Z;  // R_t(0) = H Z / Zd
+                    set_stats<J>(mu, be, L, pB / NT, mu0, beta0, L0);
+                }
                 if (merge && (pA % NT) == i) qrow[pA] = qA + qB;  // bucket
-                set_stats_pred<J>(mu, be, L, pB / NT, ownB, mu0, beta0, L0);
             }
             // ---- MAP run length r* (A7): eager (key reduced at the barrier) or on demand ----
             int r_ex = -1;
@@ -503,13 +599,19 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             }
             if (i == 0) {
                 if (P.out_pnew) P.out_pnew[s * P.ld_o + tl] = pnum * fast_rcp(Zp);
-                if (P.out_logz) P.out_logz[s * P.ld_o + tl] = LN2 * (l0 + fast_log2(Zd));  // kept mass
+                if (P.out_logz) {  // kept mass (A4)
+                    const double lzd = fast_log2(Zd, fmb);
+                    P.out_logz[s * P.ld_o + tl] = fma(LN2, double(K0 + zexp) + (lzd - lzd_prev), P.ln_omH);
+                    lzd_prev = lzd;
+                }
             }
-            s_prev = s_new;
+            zd_prev = Zd;
+            zexp = ((__double2hiint(Zd) >> 20) & 0x7FF) - 1023;
             tmod = (tmod + 1 == R) ? 0 : tmod + 1;
         }
     }
     // ---- spill -------------------------------------------------------------
+    if (nonfinite) atomicOr(&gs.flags, 1);
     group_sync<NT>(g);
 #pragma unroll
     for (int j = 0; j < J; ++j) {
@@ -524,10 +626,10 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         SeriesScalars sc;
         sc.mu0 = gs.mu0;
         sc.beta0 = gs.beta0;
-        sc.s_prev = s_prev;
+        sc.zd_prev = zd_prev;
         sc.map_prev = map_prev;
         sc.ev_count = ev_count;
-        sc.flags = gs.flags | (nonfinite ? 1 : 0);
+        sc.flags = gs.flags;
         sc.pad = 0;
         sc.pad2 = 0.0;
         P.scal[s] = sc;

@@ -57,10 +57,11 @@ int select_variant(int R, Variant* out) {
 // Test hook: elementwise fast_log2 / fast_exp2 over device arrays.
 __global__ void fastmath_probe_kernel(int which, const double* in, double* out, int64_t n,
                                       const FastMathTables* tab) {
-    load_fastmath(tab);
+    extern __shared__ __align__(16) unsigned char dyn[];
+    const unsigned fmb = fm_setup(dyn, tab);
     __syncthreads();
     for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x)
-        out[k] = which == 0 ? fast_log2(in[k]) : fast_exp2(in[k]);
+        out[k] = which == 0 ? fast_log2(in[k], fmb) : fast_exp2(in[k], fmb);
 }
 
 int launch_fastmath_probe(int which, const double* in, double* out, int64_t n, const FastMathTables* tab,
@@ -68,7 +69,7 @@ int launch_fastmath_probe(int which, const double* in, double* out, int64_t n, c
     int64_t blocks = (n + 255) / 256;
     if (blocks > 4096) blocks = 4096;
     if (blocks < 1) blocks = 1;
-    fastmath_probe_kernel<<<unsigned(blocks), 256, 0, st>>>(which, in, out, n, tab);
+    fastmath_probe_kernel<<<unsigned(blocks), 256, kFmSmemBytes, st>>>(which, in, out, n, tab);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

@@ -29,7 +29,7 @@ struct falcon_bocd_s {
     size_t smem = 0;
     int64_t t = 0;  // observations absorbed
     double2* d_ca = nullptr;
-    double2* d_gk = nullptr;
+    double* d_y = nullptr;
     fbocd::FastMathTables* d_fm = nullptr;
     double* d_mu = nullptr;
     double* d_beta = nullptr;
@@ -93,12 +93,13 @@ bool is_device_ptr(const void* p) {
 // ---------------------------------------------------------------------------
 // helper kernels
 // ---------------------------------------------------------------------------
-__global__ void init_scalars_kernel(SeriesScalars* scal, const double* mu0, const double* beta0, int64_t S) {
+__global__ void init_scalars_kernel(SeriesScalars* scal, const double* mu0, const double* beta0, int64_t S,
+                                    double omH) {
     for (int64_t s = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; s < S; s += int64_t(gridDim.x) * blockDim.x) {
         SeriesScalars sc;
         sc.mu0 = mu0[s];
         sc.beta0 = beta0[s];
-        sc.s_prev = 1.0;
+        sc.zd_prev = omH;
         sc.map_prev = 0;
         sc.ev_count = 0;
         sc.flags = 0;
@@ -181,10 +182,10 @@ __global__ void drain_gather_kernel(SeriesScalars* scal, const EventRec* ev, int
     if (reset && lane == 0) scal[s].ev_count = 0;
 }
 
-// Ring position order -> run-length order; R_t(r) = q_r s_t.
+// Ring position order -> run-length order; R_t(r) = q_r (1-H) / Zd_t.
 __global__ void posterior_kernel(const double* mu, const double* beta, const double* q,
                                  const SeriesScalars* scal, int64_t s0, int64_t count, int R, int64_t t,
-                                 double* logR_out, double* mu_out, double* beta_out) {
+                                 double omH, double* logR_out, double* mu_out, double* beta_out) {
     const int64_t n = count * int64_t(R);
     const int tm = int(t % R);
     for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
@@ -193,7 +194,7 @@ __global__ void posterior_kernel(const double* mu, const double* beta, const dou
         int p = tm - r;
         if (p < 0) p += R;
         const int64_t src = (s0 + i) * int64_t(R) + p;
-        if (logR_out) logR_out[k] = log(q[src] * scal[s0 + i].s_prev);
+        if (logR_out) logR_out[k] = log(q[src] * (omH / scal[s0 + i].zd_prev));
         if (mu_out) mu_out[k] = mu[src];
         if (beta_out) beta_out[k] = beta[src];
     }
@@ -322,7 +323,7 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
         delete h;
         return fail(nullptr, FALCON_EINVAL, "no kernel variant for this R");
     }
-    h->smem = fbocd::table_bytes(c.R, h->var.tab2) +
+    h->smem = fbocd::kFmSmemBytes + fbocd::table_bytes(c.R, h->var.tab2) +
               size_t(h->var.spb) * (h->var.group_smem + ((size_t(c.R) * sizeof(double) + 15) & ~size_t(15)));
     auto bail = [&](int code) {
         g_create_err = h->err;
@@ -353,7 +354,7 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
     const int R = c.R;
     std::vector<double> tc(R), ta(R), tg(R), tk(R);
     falcon_bocd_predictive_constants(R, c.kappa0, c.alpha0, tc.data(), ta.data(), tg.data(), tk.data());
-    std::vector<double2> ca(R), gk(R);
+    std::vector<double2> ca(R);
     {
         // base-2 units: the device table holds c_r / ln2 (bocd_kernel.cuh, A2)
         const long double inv_ln2 = 1.442695040888963407359924681001892137L;
@@ -363,7 +364,6 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
             const long double kap = (long double)c.kappa0 + r;
             const long double cr = D - 0.5L * logl(two_pi * (kap + 1.0L) / kap);
             ca[r] = make_double2((double)(cr * inv_ln2), ta[r]);
-            gk[r] = make_double2(tg[r], tk[r]);
             D = logl((long double)c.alpha0 + 0.5L * r) - D;
         }
     }
@@ -381,7 +381,7 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
         }                                                                   \
     } while (0)
     ALLOC(h->d_ca, R * sizeof(double2));
-    ALLOC(h->d_gk, R * sizeof(double2));
+    ALLOC(h->d_y, R * sizeof(double));
     ALLOC(h->d_fm, sizeof(fbocd::FastMathTables));
     ALLOC(h->d_mu, SR * sizeof(double));
     ALLOC(h->d_beta, SR * sizeof(double));
@@ -396,13 +396,13 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
 #undef ALLOC
     cudaError_t e3 = cudaSuccess;
     if (e3 == cudaSuccess) e3 = cudaMemcpy(h->d_ca, ca.data(), R * sizeof(double2), cudaMemcpyHostToDevice);
-    if (e3 == cudaSuccess) e3 = cudaMemcpy(h->d_gk, gk.data(), R * sizeof(double2), cudaMemcpyHostToDevice);
+    if (e3 == cudaSuccess) e3 = cudaMemcpy(h->d_y, tk.data(), R * sizeof(double), cudaMemcpyHostToDevice);
     if (e3 == cudaSuccess) e3 = cudaMemcpy(h->d_fm, &fmt, sizeof(fmt), cudaMemcpyHostToDevice);
     if (e3 == cudaSuccess) e3 = cudaMemcpy(dmu0, mu0.data(), S * sizeof(double), cudaMemcpyHostToDevice);
     if (e3 == cudaSuccess) e3 = cudaMemcpy(dbeta0, beta0.data(), S * sizeof(double), cudaMemcpyHostToDevice);
     if (e3 == cudaSuccess) e3 = cudaMemset(h->d_err, 0, sizeof(unsigned));
     if (e3 == cudaSuccess) {
-        init_scalars_kernel<<<grid_for(S, 256), 256>>>(h->d_scal, dmu0, dbeta0, S);
+        init_scalars_kernel<<<grid_for(S, 256), 256>>>(h->d_scal, dmu0, dbeta0, S, 1.0 - c.hazard);
         init_state_kernel<<<grid_for(int64_t(SR), 256), 256>>>(h->d_mu, h->d_beta, h->d_v, h->d_scal, S, R);
         e3 = cudaGetLastError();
     }
@@ -426,6 +426,7 @@ static int launch_update(falcon_bocd_t h, const double* x_dev, int64_t ld, int64
         P.S = c.n_series;
         P.H = c.hazard;
         P.omH = 1.0 - c.hazard;
+        P.ln_omH = log1p(-c.hazard);
         P.hr = (double)((long double)c.hazard / (1.0L - (long double)c.hazard));
         P.theta = c.threshold;
         P.alpha0 = c.alpha0;
@@ -435,7 +436,7 @@ static int launch_update(falcon_bocd_t h, const double* x_dev, int64_t ld, int64
         P.ev_mask = c.event_mask;
         P.ev_cap = c.event_capacity;
         P.tab_ca = h->d_ca;
-        P.tab_gk = h->d_gk;
+        P.tab_y = h->d_y;
         P.fm = h->d_fm;
         P.st_mu = h->d_mu;
         P.st_beta = h->d_beta;
@@ -642,7 +643,7 @@ int falcon_bocd_read_posterior(falcon_bocd_t h, int64_t s0, int64_t count, doubl
         dst[k] = is_device_ptr(outs[k]) ? outs[k] : tmp + k * n;
     }
     posterior_kernel<<<grid_for(int64_t(n), 256), 256, 0, st>>>(h->d_mu, h->d_beta, h->d_v, h->d_scal, s0, count, R,
-                                                                h->t, dst[0], dst[1], dst[2]);
+                                                                h->t, 1.0 - h->cfg.hazard, dst[0], dst[1], dst[2]);
     cudaError_t e = cudaGetLastError();
     for (int k = 0; k < 3 && e == cudaSuccess; ++k)
         if (outs[k] && dst[k] != outs[k])
@@ -679,7 +680,7 @@ int falcon_bocd_destroy(falcon_bocd_t h) {
         }
     }
     cudaGetLastError();
-    void* ptrs[] = {h->d_ca, h->d_gk, h->d_fm, h->d_mu, h->d_beta, h->d_v, h->d_scal, h->d_ev, h->d_err, h->d_off,
+    void* ptrs[] = {h->d_ca, h->d_y, h->d_fm, h->d_mu, h->d_beta, h->d_v, h->d_scal, h->d_ev, h->d_err, h->d_off,
                     h->d_meta, h->d_evout, h->d_stage[0], h->d_stage[1], h->d_omap, h->d_opnew, h->d_ologz};
     for (void* p : ptrs)
         if (p) cudaFree(p);

@@ -59,9 +59,11 @@ inline void fill_fastmath_tables(FastMathTables* t) {
     for (int j = 0; j < kExpTab; ++j) t->exptab[j] = (double)exp2l((long double)j / 64.0L);
 }
 
-// The tables live in static shared memory, referenced by name so that every lookup
-// is one LDS with an immediate base (each kernel loads them once with load_fastmath).
-static __shared__ FastMathTables g_fm;
+// The tables live in DYNAMIC shared memory at a 2048-B aligned address fmb (logtab at
+// fmb, exptab at fmb + 2048), so a lookup address is (index bits) | fmb: one LOP3, no
+// add.  A kernel reserves kFmSmemBytes at the start of its dynamic shared memory
+// (alignment slack included) and calls fm_setup once (then a CTA barrier).
+constexpr unsigned kFmSmemBytes = 2048u + unsigned(sizeof(FastMathTables));
 
 // Polynomial / conversion constants in constant memory, uploaded at handle creation
 // (falcon_bocd_create -> upload_fastmath_constants): not known to the compiler, so DFMA /
@@ -74,38 +76,58 @@ static const double kFastMathConstants[16] = {
     0.0013333558146428443, 0.009618129107628477, 0.05550410866482158,  0.24022650695910072,  // exp2 poly
     0.6931471805599453,    64.0,                 -0.015625,            0.0};
 
-__device__ __forceinline__ void load_fastmath(const FastMathTables* __restrict__ src) {
-    const double* s = reinterpret_cast<const double*>(src);
-    double* d = reinterpret_cast<double*>(&g_fm);
-    for (int k = threadIdx.x; k < int(sizeof(FastMathTables) / 8); k += blockDim.x) d[k] = s[k];
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
 
-__device__ __forceinline__ double fast_log2(double x) {
-    const int hi = __double2hiint(x);
-    const int tb = hi + 0x00196000;  // (hi - 0x3FE6A000) + (1024 << 20): biased k in bits 20..31
+// Copies the tables to the first 2048-B aligned address of dyn (a dynamic shared-memory
+// region of kFmSmemBytes) and returns that address.
+__device__ __forceinline__ unsigned fm_setup(unsigned char* dyn, const FastMathTables* __restrict__ src) {
+    const unsigned b = smem_addr(dyn);
+    const unsigned fmb = (b + 2047u) & ~2047u;
+    const double* s = reinterpret_cast<const double*>(src);
+    double* d = reinterpret_cast<double*>(dyn + (fmb - b));
+    for (int k = threadIdx.x; k < int(sizeof(FastMathTables) / 8); k += blockDim.x) d[k] = s[k];
+    return fmb;
+}
+
+__device__ __forceinline__ double2 lds_v2f64(unsigned a) {
+    double2 v;
+    asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double lds_f64(unsigned a) {
+    double v;
+    asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+
+__device__ __forceinline__ double fast_log2(double x, unsigned fmb) {
+    const unsigned tb = unsigned(__double2hiint(x)) + 0x00196000u;  // (hi - 0x3FE6A000) + (1024 << 20)
     // entry (tb >> 13) & 127 (top 7 mantissa bits of ix - OFF), as a byte offset
-    const double2 t = *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(g_fm.logtab) +
-                                                       ((tb >> 9) & ((kLogTab - 1) << 4)));
+    const double2 t = lds_v2f64(((tb >> 9) & 0x7F0u) | fmb);
     // r = z * invc - 1 with z = x / 2^k: the exact power-of-two scaling is folded into invc
     const double invs =
-        __hiloint2double(__double2hiint(t.x) + 0x40000000 - (tb & 0xFFF00000), __double2loint(t.x));
+        __hiloint2double(__double2hiint(t.x) + 0x40000000 - int(tb & 0xFFF00000u), __double2loint(t.x));
     const double r = fma(x, invs, -1.0);
-    const double kd = __hiloint2double(0x43300000, int(unsigned(tb) >> 20)) - c_fm[6];  // k (2^52 + 1024 bias)
+    // k + l_i first (off the polynomial's dependency chain; the BOCD cell loop evaluates
+    // the same expression stage by stage and must agree bit for bit)
+    const double kt = (__hiloint2double(0x43300000, int(tb >> 20)) - c_fm[6]) + t.y;  // k (2^52 + 1024 bias)
     double p = fma(r, c_fm[0], c_fm[1]);
     p = fma(p, r, c_fm[2]);
     p = fma(p, r, c_fm[3]);
     p = fma(p, r, c_fm[4]);
     p = fma(p, r, c_fm[5]);
-    return kd + fma(r, p, t.y);
+    return fma(r, p, kt);
 }
 
-__device__ __forceinline__ double fast_exp2(double x) {
+__device__ __forceinline__ double fast_exp2(double x, unsigned fmb) {
     // clamp x >= -1021 on the integer pipe: only the high word is clamped (a clamped
     // argument keeps stray low mantissa bits: -1021 - 2^-33 at most, irrelevant)
     const int xh = int(min(unsigned(__double2hiint(x)), 0xC08FE800u));  // -inf / NaN patterns too
     const double xc = __hiloint2double(xh, __double2loint(x));
     const double zf = fma(xc, c_fm[13], c_fm[7]);  // round(64 x) in the low word (1.5 * 2^52 shift)
-    const int ki = __double2loint(zf);
+    const unsigned ki = unsigned(__double2loint(zf));
     const double kd = zf - c_fm[7];
     const double r = fma(kd, c_fm[14], xc);  // exact: |r| <= 1/128
     double p = fma(r, c_fm[8], c_fm[9]);
@@ -113,40 +135,11 @@ __device__ __forceinline__ double fast_exp2(double x) {
     p = fma(p, r, c_fm[11]);
     p = fma(p, r, c_fm[12]);
     const double q = p * r;
-    const double T =
-        *reinterpret_cast<const double*>(reinterpret_cast<const char*>(g_fm.exptab) + ((ki << 3) & 0x1F8));
+    const double T = lds_f64(((ki << 3) & 0x1F8u) | (fmb + 2048u));
     int th;  // high word of T * 2^(ki >> 6): one IMAD
-    asm("mad.lo.s32 %0, %1, 1048576, %2;" : "=r"(th) : "r"(ki >> 6), "r"(__double2hiint(T)));
+    asm("mad.lo.s32 %0, %1, 1048576, %2;" : "=r"(th) : "r"(int(ki) >> 6), "r"(__double2hiint(T)));
     const double Ts = __hiloint2double(th, __double2loint(T));
     return fma(Ts, q, Ts);
-}
-
-// 2^x for the probability-domain recursion: exactly 0 below -1021 (a cell 2^1021 below
-// the change-point cell can never matter again in fp64: it would need a likelihood
-// ratio beyond the double range to come back; reading documented in DESIGN.md), and
-// the argument clamped at +1000 (a posterior predictive 2^1000 denser than the prior
-// predictive: not reachable with finite data scales, guards the range).
-__device__ __forceinline__ double fast_exp2_zero(double x) {
-    const int hx = __double2hiint(x);
-    const bool dead = static_cast<unsigned>(hx) > 0xC08FE800u;  // x < -1021 (or -inf / negative NaN)
-    int xh = int(min(unsigned(hx), 0xC08FE800u));
-    xh = min(xh, 0x408F4000);  // x <= 1000
-    const double xc = __hiloint2double(xh, __double2loint(x));
-    const double zf = fma(xc, c_fm[13], c_fm[7]);  // round(64 x) in the low word (1.5 * 2^52 shift)
-    const int ki = __double2loint(zf);
-    const double kd = zf - c_fm[7];
-    const double r = fma(kd, c_fm[14], xc);  // exact: |r| <= 1/128
-    double p = fma(r, c_fm[8], c_fm[9]);
-    p = fma(p, r, c_fm[10]);
-    p = fma(p, r, c_fm[11]);
-    p = fma(p, r, c_fm[12]);
-    const double q = p * r;
-    const double T =
-        *reinterpret_cast<const double*>(reinterpret_cast<const char*>(g_fm.exptab) + ((ki << 3) & 0x1F8));
-    int th;
-    asm("mad.lo.s32 %0, %1, 1048576, %2;" : "=r"(th) : "r"(ki >> 6), "r"(__double2hiint(T)));
-    const double Ts = __hiloint2double(th, __double2loint(T));
-    return dead ? 0.0 : fma(Ts, q, Ts);
 }
 
 // 1/x to ~1 ulp for positive normal x: MUFU seed + one Newton step (no IEEE division path).
