@@ -212,8 +212,9 @@ template <int NT>
 __host__ __device__ constexpr size_t group_bytes(int R) {
     return sizeof(GroupSmem<NT>) + ((size_t(R) * sizeof(double) + 15) & ~size_t(15));  // keep 16-B alignment
 }
-__host__ __device__ constexpr size_t table_bytes(int R, bool tab2) {
-    return (size_t(R) * (tab2 ? 2 : 1) * (sizeof(double2) + sizeof(double)) + 15) & ~size_t(15);
+// bytes of the per-r tables ({c_r/ln2, alpha_r} and y_r) for `entries` table rows
+__host__ __device__ constexpr size_t table_bytes(int entries) {
+    return (size_t(entries) * (sizeof(double2) + sizeof(double)) + 15) & ~size_t(15);
 }
 
 // Resets one cell's NIG statistics to the prior (called by the owning thread only;
@@ -247,35 +248,62 @@ __device__ __forceinline__ double prior_l2(double x, double mu0, double be0, dou
 
 // ---------------------------------------------------------------------------
 // The kernel.
-//   FULL : R == NT*J (power of two) at compile time;
-//   TAB2 : doubled per-r tables (R <= 2048);
+//   FULL : R == NT*J (powers of two) at compile time.  FULL kernels ROTATE the
+//          slot <-> position map by one slot every NT steps (slot j of thread i
+//          holds position i + NT*((j + phi) mod J), phi = pB / NT for the
+//          position pB the step recycles), so the recycled cell is always slot 0:
+//          its prior reset is a compile-time register write, and every table /
+//          row offset of a slot is a compile-time constant.
+//   TAB2 : doubled per-r tables (generic R <= 2048);
 //   EAGER: the MAP run length r* is reduced every step (per-step MAP output or
 //          MAPRESET events requested); otherwise it is reduced on demand, from the
 //          step's q row in shared memory, only at steps that report an event.
 // ---------------------------------------------------------------------------
+template <int NT, int J, bool FULL, bool TAB2>
+__host__ __device__ constexpr int table_entries(int R) {
+    return FULL ? R + NT : (TAB2 ? 2 * R : R);  // FULL: index r or r + R, r + R < R + NT
+}
+
+// The dynamic shared window of a non-cluster launch starts at this shared address
+// (after the 1 KB system reservation; no static shared memory in this kernel), so
+// the fast-math tables sit at the compile-time address kFmBase (checked at entry).
+constexpr unsigned kFmBase = 0x800u;
+
+__device__ __forceinline__ double2 lds_log_entry(unsigned off) {  // off = (index << 4), index < 128
+    double2 v;
+    asm("ld.shared.v2.f64 {%0, %1}, [%2+2048];" : "=d"(v.x), "=d"(v.y) : "r"(off));
+    return v;
+}
+__device__ __forceinline__ double lds_exp_entry(unsigned off) {  // off = (index << 3), index < 64
+    double v;
+    asm("ld.shared.f64 %0, [%1+4096];" : "=d"(v) : "r"(off));
+    return v;
+}
+
 template <int NT, int J, bool FULL, bool TAB2, bool EAGER, int SPB, int MINB>
 __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParams P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr bool ROT = FULL;
     const int R = FULL ? NT * J : P.R;
-    const int RT = TAB2 ? 2 * R : R;
+    const int RT = table_entries<NT, J, FULL, TAB2>(R);
     // dynamic shared memory: [fast-math tables (aligned in kFmSmemBytes)][per-r tables][groups]
     double2* s_ca = reinterpret_cast<double2*>(smem_raw + kFmSmemBytes);
     double* s_y = reinterpret_cast<double*>(s_ca + RT);
-    unsigned char* gbase = smem_raw + kFmSmemBytes + table_bytes(R, TAB2);
+    unsigned char* gbase = smem_raw + kFmSmemBytes + table_bytes(RT);
 
     for (int k = threadIdx.x; k < RT; k += blockDim.x) {
         const int r = k < R ? k : k - R;
         s_ca[k] = P.tab_ca[r];
         s_y[k] = P.tab_y[r];
     }
-    const unsigned fmb = fm_setup(smem_raw, P.fm);  // logtab, 2048-B aligned
-    const unsigned emb = fmb + 2048u;                // exptab, 512-B aligned
+    const bool fm_ok = fm_setup(smem_raw, P.fm) == kFmBase;
     const int g = threadIdx.x / NT;
     const int i = threadIdx.x % NT;
     const int lane = threadIdx.x & 31;
     const int w = i >> 5;
     GroupSmem<NT>& gs = *reinterpret_cast<GroupSmem<NT>*>(gbase + size_t(g) * group_bytes<NT>(R));
-    // the series' unnormalised run-length posterior q, in ring-position order
+    // the series' unnormalised run-length posterior q: FULL in slot order (element
+    // i + NT*j = slot j of thread i), else in ring-position order
     double* qrow = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(&gs) + sizeof(GroupSmem<NT>));
     const int64_t s = int64_t(blockIdx.x) * SPB + g;
     const bool active = s < P.S;
@@ -309,31 +337,41 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         const bool ok = sc.beta0 >= 2.2250738585072014e-308 && sc.beta0 < 1e300 && isfinite(sc.mu0);
         gs.mu0 = sc.mu0;
         gs.beta0 = ok ? sc.beta0 : 1.0;
-        gs.L0 = fast_log2(gs.beta0, fmb);
+        gs.L0 = fast_log2(gs.beta0, kFmBase);
         gs.zd_prev = sc.zd_prev;
         gs.map_prev = sc.map_prev;
         gs.ev_count = sc.ev_count;
-        gs.flags = sc.flags | (ok ? 0 : 2);
+        gs.flags = sc.flags | (ok ? 0 : 2) | (fm_ok ? 0 : 4);
     }
     group_sync<NT>(g);
     const double mu0 = gs.mu0, beta0 = gs.beta0, L0 = gs.L0;
     double zd_prev = gs.zd_prev;  // per-series scalars are group-uniform registers
     int zexp = ((__double2hiint(zd_prev) >> 20) & 0x7FF) - 1023;  // binary exponent of Zd_{t-1}
     int map_prev = gs.map_prev, ev_count = gs.ev_count;
+    // ring bookkeeping.  FULL: the recycled position pB = (t+1) mod R = NT*phi + iB;
+    // generic: tmod = t mod R.
+    int tmod = int(P.t0 % R);
+    int iB = 0, phi = 0;
+    if constexpr (ROT) {
+        const int pB0 = (tmod + 1 == R) ? 0 : tmod + 1;
+        iB = pB0 % NT;
+        phi = pB0 / NT;
+    }
 #pragma unroll
     for (int j = 0; j < J; ++j) {
-        const int p = i + NT * j;
+        const int p = ROT ? i + NT * ((j + phi) & (J - 1)) : i + NT * j;  // position of slot j
+        const int e = ROT ? i + NT * j : p;                                // its q element
         if (FULL || p < R) {
             if (P.t0 == 0) {
                 mu[j] = mu0;
                 be[j] = beta0;
                 L[j] = L0;
-                qrow[p] = (p == 0) ? 1.0 : 0.0;  // before x_0 a segment starts w.p. 1 (Q8)
+                qrow[e] = (p == 0) ? 1.0 : 0.0;  // before x_0 a segment starts w.p. 1 (Q8)
             } else {
                 mu[j] = P.st_mu[sbase + p];
                 be[j] = P.st_beta[sbase + p];
-                qrow[p] = P.st_q[sbase + p];
-                L[j] = fast_log2(be[j], fmb);
+                qrow[e] = P.st_q[sbase + p];
+                L[j] = fast_log2(be[j], kFmBase);
             }
         } else {
             mu[j] = mu0;
@@ -348,10 +386,9 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     const bool merge = (P.mode == 0);
     // argmax-eligible run lengths: MERGE r <= R-3 (slot R-1 is the bucket), DROP r <= R-2
     const int r_elig = merge ? R - 3 : R - 2;
-    int tmod = int(P.t0 % R);  // ring bookkeeping: t mod R
     bool nonfinite = false;
     // lg Zd_{t-1} for the log-evidence output (thread 0 only)
-    double lzd_prev = (i == 0 && P.out_logz) ? fast_log2(zd_prev, fmb) : 0.0;
+    double lzd_prev = (i == 0 && P.out_logz) ? fast_log2(zd_prev, kFmBase) : 0.0;
 
     for (int k = 0; k < ntiles; ++k) {
         const int base = k * kTile;
@@ -370,7 +407,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         for (int q = i; q < n; q += NT) {
             const double xq = gs.xbuf[buf][q];
             if (!isfinite(xq)) nonfinite = true;
-            const double l0 = prior_l2(xq, mu0, beta0, L0, ca0, y0, fmb);
+            const double l0 = prior_l2(xq, mu0, beta0, L0, ca0, y0, kFmBase);
             gs.kbuf[buf][q] = __double2int_rn(fmin(fmax(l0, -1048576.0), 1048576.0));
         }
         group_sync<NT>(g);
@@ -384,7 +421,9 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             // round(64 l) - 64 N_t + 2^31 in its low word (exact integers below 2^52)
             const double C7 = __hiloint2double(0x43380000, int(0x80000000u - unsigned(K0 + zexp) * 64u));
             // ---- A1-A4 for the J cells (groups of G, every stage across the group) ----
-            const int ib = tmod - i + R;  // TAB2 index of cell j: ib - NT*j  (= (t - p) mod R, + R)
+            // table index of slot j: ib - NT*j  (= r or r + R).  FULL: r of slot j is
+            // (pB - 1 - p) mod R = (iB - 1 - i - NT j) mod R.
+            const int ib = ROT ? iB - 1 - i + R : tmod - i + R;
             double sum = 0.0;
             unsigned long long key = 0ull;
 #pragma unroll
@@ -397,10 +436,8 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 for (int kk = 0; kk < G; ++kk) {  // table + row loads
                     const int j = j0 + kk;
                     const int p = i + NT * j;
-                    if (TAB2) {
+                    if (ROT || TAB2) {
                         idx[kk] = ib - NT * j;
-                    } else if (FULL) {
-                        idx[kk] = (tmod - p) & (R - 1);
                     } else {
                         idx[kk] = tmod - p;
                         idx[kk] += (idx[kk] < 0) ? R : 0;
@@ -424,7 +461,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
 #pragma unroll
                 for (int kk = 0; kk < G; ++kk) {
                     tb[kk] = unsigned(__double2hiint(bn[kk])) + 0x00196000u;
-                    lt[kk] = lds_v2f64(((tb[kk] >> 9) & 0x7F0u) | fmb);
+                    lt[kk] = lds_log_entry((tb[kk] >> 9) & 0x7F0u);
                 }
 #pragma unroll
                 for (int kk = 0; kk < G; ++kk) {
@@ -457,7 +494,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     const double zf = fma(ell[kk], 64.0, C7);
                     ki[kk] = unsigned(__double2loint(zf));
                     re[kk] = fma(zf - C7, -0.015625, ell[kk]);  // exact, |re| <= 1/128
-                    Tv[kk] = lds_f64(((ki[kk] << 3) & 0x1F8u) | emb);
+                    Tv[kk] = lds_exp_entry((ki[kk] << 3) & 0x1F8u);
                 }
 #pragma unroll
                 for (int kk = 0; kk < G; ++kk) pe[kk] = fma(re[kk], c_fm[8], c_fm[9]);
@@ -483,22 +520,30 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                         qrow[p] = qn;
                         sum += qn;
                         if constexpr (EAGER) {
-                            int r = tmod - p;
-                            r += (r < 0) ? R : 0;
+                            int r = idx[kk];
+                            r -= (r >= R) ? R : 0;
                             const unsigned long long kq = argmax_key(qn, r);
                             key = (r <= r_elig && kq > key) ? kq : key;
                         }
                     }
                 }
             }
-            // the three cells the tail needs are published by their owners (pB / pA are
-            // overwritten right after the barrier)
+            // the three cells the tail needs (r = R-2, R-1, 0) are published by their owners
+            // (kB / kA are overwritten right after the barrier); kX = their q elements
             const int par = tl & 1;
-            const int pB = (tmod + 1 == R) ? 0 : tmod + 1;  // r = R-1 (recycled)
-            const int pA = (pB + 1 == R) ? 0 : pB + 1;      // r = R-2
-            if ((pA % NT) == i) gs.spec[par][0] = qrow[pA];
-            if ((pB % NT) == i) gs.spec[par][1] = qrow[pB];
-            if ((tmod % NT) == i) gs.spec[par][2] = qrow[tmod];
+            int kA, kB, k0;
+            if constexpr (ROT) {
+                kB = iB;                        // slot 0 of thread iB
+                kA = iB + 1;                    // slot 0 of thread iB+1, or slot 1 of thread 0
+                k0 = (iB == 0) ? R - 1 : iB - 1;  // slot 0 of thread iB-1, or slot J-1 of thread NT-1
+            } else {
+                kB = (tmod + 1 == R) ? 0 : tmod + 1;
+                kA = (kB + 1 == R) ? 0 : kB + 1;
+                k0 = tmod;
+            }
+            if ((kA % NT) == i) gs.spec[par][0] = qrow[kA];
+            if ((kB % NT) == i) gs.spec[par][1] = qrow[kB];
+            if ((k0 % NT) == i) gs.spec[par][2] = qrow[k0];
             // ---- group sum (and, EAGER, argmax): the step's only barrier ----------------
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
@@ -529,14 +574,17 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             const double Zp = merge ? Z : Z - qB;               // p_new = pnum / Zp
             const double pnum = (merge && R == 2) ? Z : q0;     // MERGE R = 2: p_new = 1
             uint32_t fl = (t > 0 && pnum > P.theta * Zp) ? 1u : 0u;
-            {
-                const bool ownB = (pB % NT) == i;
-                if (ownB) {
-                    qrow[pB] = P.hr * Z;  // R_t(0) = H Z / Zd
-                    set_stats<J>(mu, be, L, pB / NT, mu0, beta0, L0);
+            if ((kB % NT) == i) {
+                qrow[kB] = P.hr * Z;  // R_t(0) = H Z / Zd
+                if constexpr (ROT) {
+                    mu[0] = mu0;  // the recycled cell is slot 0
+                    be[0] = beta0;
+                    L[0] = L0;
+                } else {
+                    set_stats<J>(mu, be, L, kB / NT, mu0, beta0, L0);
                 }
-                if (merge && (pA % NT) == i) qrow[pA] = qA + qB;  // bucket
             }
+            if (merge && (kA % NT) == i) qrow[kA] = qA + qB;  // bucket
             // ---- MAP run length r* (A7): eager (key reduced at the barrier) or on demand ----
             int r_ex = -1;
             double qex = 0.0;
@@ -551,8 +599,14 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 for (int j = 0; j < J; ++j) {
                     const int p = i + NT * j;
                     if (FULL || p < R) {
-                        int r = tmod - p;
-                        r += (r < 0) ? R : 0;
+                        int r;
+                        if (ROT || TAB2) {
+                            r = ib - NT * j;
+                            r -= (r >= R) ? R : 0;
+                        } else {
+                            r = tmod - p;
+                            r += (r < 0) ? R : 0;
+                        }
                         const unsigned long long kq = argmax_key(qrow[p], r);  // own cells only
                         kb = (r <= r_elig && kq > kb) ? kq : kb;
                     }
@@ -600,7 +654,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             if (i == 0) {
                 if (P.out_pnew) P.out_pnew[s * P.ld_o + tl] = pnum * fast_rcp(Zp);
                 if (P.out_logz) {  // kept mass (A4)
-                    const double lzd = fast_log2(Zd, fmb);
+                    const double lzd = fast_log2(Zd, kFmBase);
                     P.out_logz[s * P.ld_o + tl] = fma(LN2, double(K0 + zexp) + (lzd - lzd_prev), P.ln_omH);
                     lzd_prev = lzd;
                 }
@@ -608,6 +662,24 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             zd_prev = Zd;
             zexp = ((__double2hiint(Zd) >> 20) & 0x7FF) - 1023;
             tmod = (tmod + 1 == R) ? 0 : tmod + 1;
+            if constexpr (ROT) {
+                if (++iB == NT) {  // pB crosses a slot boundary: rotate slot j <- slot j+1
+                    iB = 0;
+                    phi = (phi + 1) & (J - 1);
+                    const double m0 = mu[0], b0 = be[0], l0r = L[0], qf = qrow[i];
+#pragma unroll
+                    for (int j = 0; j + 1 < J; ++j) {
+                        mu[j] = mu[j + 1];
+                        be[j] = be[j + 1];
+                        L[j] = L[j + 1];
+                        qrow[i + NT * j] = qrow[i + NT * (j + 1)];
+                    }
+                    mu[J - 1] = m0;
+                    be[J - 1] = b0;
+                    L[J - 1] = l0r;
+                    qrow[i + NT * (J - 1)] = qf;
+                }
+            }
         }
     }
     // ---- spill -------------------------------------------------------------
@@ -615,11 +687,12 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     group_sync<NT>(g);
 #pragma unroll
     for (int j = 0; j < J; ++j) {
-        const int p = i + NT * j;
+        const int p = ROT ? i + NT * ((j + phi) & (J - 1)) : i + NT * j;
+        const int e = ROT ? i + NT * j : p;
         if (FULL || p < R) {
             P.st_mu[sbase + p] = mu[j];
             P.st_beta[sbase + p] = be[j];
-            P.st_q[sbase + p] = qrow[p];
+            P.st_q[sbase + p] = qrow[e];
         }
     }
     if (i == 0) {

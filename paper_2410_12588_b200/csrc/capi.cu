@@ -323,7 +323,9 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
         delete h;
         return fail(nullptr, FALCON_EINVAL, "no kernel variant for this R");
     }
-    h->smem = fbocd::kFmSmemBytes + fbocd::table_bytes(c.R, h->var.tab2) +
+    // per-r table rows: FULL kernels index r and r + R < R + NT, generic TAB2 kernels r + R < 2R
+    const int tab_rows = h->var.full ? c.R + h->var.nt : (h->var.tab2 ? 2 * c.R : c.R);
+    h->smem = fbocd::kFmSmemBytes + fbocd::table_bytes(tab_rows) +
               size_t(h->var.spb) * (h->var.group_smem + ((size_t(c.R) * sizeof(double) + 15) & ~size_t(15)));
     auto bail = [&](int code) {
         g_create_err = h->err;
