@@ -116,7 +116,8 @@ struct __align__(16) GroupSmem {
     unsigned long long red1[2][NT / 32 > 0 ? NT / 32 : 1];  // EAGER argmax keys
     unsigned long long red3[NT / 32 > 0 ? NT / 32 : 1];     // on-demand argmax (event steps)
     double spec[2][4];                                       // q' of the cells r = R-2, R-1, 0
-    double mu0, beta0, L0, zd_prev;
+    double mu0, beta0, L0, zd_prev;  // zd_prev: kept current by thread 0 every step
+    double lzd_prev;                 // lg Zd_{t-1} (log-evidence output, thread 0)
     int map_prev, ev_count, flags, pad;
     unsigned long long mbar[2];
 };
@@ -284,6 +285,11 @@ template <int NT, int J, bool FULL, bool TAB2, bool EAGER, int SPB, int MINB>
 __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParams P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr bool ROT = FULL;
+#ifdef FALCON_BOCD_QREG
+    constexpr bool QREG = ROT;  // q in registers (slot order) instead of the shared row
+#else
+    constexpr bool QREG = false;
+#endif
     const int R = FULL ? NT * J : P.R;
     const int RT = table_entries<NT, J, FULL, TAB2>(R);
     // dynamic shared memory: [fast-math tables (aligned in kFmSmemBytes)][per-r tables][groups]
@@ -322,6 +328,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
 
     // ---- load or initialise the state ------------------------------------
     double mu[J], be[J], L[J];
+    double qr[QREG ? J : 1];
     const int64_t sbase = s * int64_t(R);
     if (i == 0) {
         SeriesScalars sc = P.scal[s];
@@ -344,9 +351,9 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         gs.flags = sc.flags | (ok ? 0 : 2) | (fm_ok ? 0 : 4);
     }
     group_sync<NT>(g);
-    const double mu0 = gs.mu0, beta0 = gs.beta0, L0 = gs.L0;
-    double zd_prev = gs.zd_prev;  // per-series scalars are group-uniform registers
-    int zexp = ((__double2hiint(zd_prev) >> 20) & 0x7FF) - 1023;  // binary exponent of Zd_{t-1}
+    // the prior and the rarely used per-series scalars stay in shared memory (gs) so
+    // that the step loop keeps its registers for the cells
+    int zexp = ((__double2hiint(gs.zd_prev) >> 20) & 0x7FF) - 1023;  // binary exponent of Zd_{t-1}
     int map_prev = gs.map_prev, ev_count = gs.ev_count;
     // ring bookkeeping.  FULL: the recycled position pB = (t+1) mod R = NT*phi + iB;
     // generic: tmod = t mod R.
@@ -363,32 +370,29 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         const int e = ROT ? i + NT * j : p;                                // its q element
         if (FULL || p < R) {
             if (P.t0 == 0) {
-                mu[j] = mu0;
-                be[j] = beta0;
-                L[j] = L0;
-                qrow[e] = (p == 0) ? 1.0 : 0.0;  // before x_0 a segment starts w.p. 1 (Q8)
+                mu[j] = gs.mu0;
+                be[j] = gs.beta0;
+                L[j] = gs.L0;
+                const double q0v = (p == 0) ? 1.0 : 0.0;  // before x_0 a segment starts w.p. 1 (Q8)
+                if constexpr (QREG) qr[j] = q0v; else qrow[e] = q0v;
             } else {
                 mu[j] = P.st_mu[sbase + p];
                 be[j] = P.st_beta[sbase + p];
-                qrow[e] = P.st_q[sbase + p];
+                if constexpr (QREG) qr[j] = P.st_q[sbase + p]; else qrow[e] = P.st_q[sbase + p];
                 L[j] = fast_log2(be[j], kFmBase);
             }
         } else {
-            mu[j] = mu0;
-            be[j] = beta0;
-            L[j] = L0;
+            mu[j] = gs.mu0;
+            be[j] = gs.beta0;
+            L[j] = gs.L0;
         }
     }
-    // table entries of r = 0 (the prior predictive)
-    const double2 ca0 = s_ca[0];
-    const double y0 = s_y[0];
 
     const bool merge = (P.mode == 0);
     // argmax-eligible run lengths: MERGE r <= R-3 (slot R-1 is the bucket), DROP r <= R-2
     const int r_elig = merge ? R - 3 : R - 2;
     bool nonfinite = false;
-    // lg Zd_{t-1} for the log-evidence output (thread 0 only)
-    double lzd_prev = (i == 0 && P.out_logz) ? fast_log2(zd_prev, kFmBase) : 0.0;
+    if (i == 0 && P.out_logz) gs.lzd_prev = fast_log2(gs.zd_prev, kFmBase);
 
     for (int k = 0; k < ntiles; ++k) {
         const int base = k * kTile;
@@ -407,7 +411,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         for (int q = i; q < n; q += NT) {
             const double xq = gs.xbuf[buf][q];
             if (!isfinite(xq)) nonfinite = true;
-            const double l0 = prior_l2(xq, mu0, beta0, L0, ca0, y0, kFmBase);
+            const double l0 = prior_l2(xq, gs.mu0, gs.beta0, gs.L0, s_ca[0], s_y[0], kFmBase);
             gs.kbuf[buf][q] = __double2int_rn(fmin(fmax(l0, -1048576.0), 1048576.0));
         }
         group_sync<NT>(g);
@@ -445,7 +449,8 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     if (!FULL && p >= R) idx[kk] = 0;  // masked cell: any valid entry
                     ca[kk] = s_ca[idx[kk]];
                     yv[kk] = s_y[idx[kk]];
-                    qv[kk] = (FULL || p < R) ? qrow[p] : 0.0;
+                    if constexpr (QREG) qv[kk] = qr[j];
+                    else qv[kk] = (FULL || p < R) ? qrow[p] : 0.0;
                 }
                 // A1: NIG update
 #pragma unroll
@@ -471,7 +476,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     kt[kk] = (__hiloint2double(0x43300000, int(tb[kk] >> 20)) - c_fm[6]) + lt[kk].y;
                 }
 #pragma unroll
-                for (int kk = 0; kk < G; ++kk) pl[kk] = fma(rl[kk], c_fm[0], c_fm[1]);
+                for (int kk = 0; kk < G; ++kk) pl[kk] = fma(rl[kk], kLog2C0, c_fm[1]);
 #pragma unroll
                 for (int c = 2; c <= 5; ++c) {
 #pragma unroll
@@ -497,7 +502,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     Tv[kk] = lds_exp_entry((ki[kk] << 3) & 0x1F8u);
                 }
 #pragma unroll
-                for (int kk = 0; kk < G; ++kk) pe[kk] = fma(re[kk], c_fm[8], c_fm[9]);
+                for (int kk = 0; kk < G; ++kk) pe[kk] = fma(re[kk], kExp2C0, c_fm[9]);
 #pragma unroll
                 for (int c = 10; c <= 12; ++c) {
 #pragma unroll
@@ -517,7 +522,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     const double E = dead ? 0.0 : fma(Ts, qq, Ts);
                     if (FULL || p < R) {
                         const double qn = qv[kk] * E;
-                        qrow[p] = qn;
+                        if constexpr (QREG) qr[j] = qn; else qrow[p] = qn;
                         sum += qn;
                         if constexpr (EAGER) {
                             int r = idx[kk];
@@ -541,9 +546,15 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 kA = (kB + 1 == R) ? 0 : kB + 1;
                 k0 = tmod;
             }
-            if ((kA % NT) == i) gs.spec[par][0] = qrow[kA];
-            if ((kB % NT) == i) gs.spec[par][1] = qrow[kB];
-            if ((k0 % NT) == i) gs.spec[par][2] = qrow[k0];
+            if constexpr (QREG) {
+                if ((kA % NT) == i) gs.spec[par][0] = (kA < NT) ? qr[0] : qr[1];
+                if (kB == i) gs.spec[par][1] = qr[0];
+                if ((k0 % NT) == i) gs.spec[par][2] = (k0 < NT) ? qr[0] : qr[J - 1];
+            } else {
+                if ((kA % NT) == i) gs.spec[par][0] = qrow[kA];
+                if ((kB % NT) == i) gs.spec[par][1] = qrow[kB];
+                if ((k0 % NT) == i) gs.spec[par][2] = qrow[k0];
+            }
             // ---- group sum (and, EAGER, argmax): the step's only barrier ----------------
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
@@ -575,16 +586,22 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             const double pnum = (merge && R == 2) ? Z : q0;     // MERGE R = 2: p_new = 1
             uint32_t fl = (t > 0 && pnum > P.theta * Zp) ? 1u : 0u;
             if ((kB % NT) == i) {
-                qrow[kB] = P.hr * Z;  // R_t(0) = H Z / Zd
+                if constexpr (QREG) qr[0] = P.hr * Z; else qrow[kB] = P.hr * Z;  // R_t(0) = H Z / Zd
                 if constexpr (ROT) {
-                    mu[0] = mu0;  // the recycled cell is slot 0
-                    be[0] = beta0;
-                    L[0] = L0;
+                    mu[0] = gs.mu0;  // the recycled cell is slot 0
+                    be[0] = gs.beta0;
+                    L[0] = gs.L0;
                 } else {
-                    set_stats<J>(mu, be, L, kB / NT, mu0, beta0, L0);
+                    set_stats<J>(mu, be, L, kB / NT, gs.mu0, gs.beta0, gs.L0);
                 }
             }
-            if (merge && (kA % NT) == i) qrow[kA] = qA + qB;  // bucket
+            if (merge && (kA % NT) == i) {  // bucket
+                if constexpr (QREG) {
+                    if (kA < NT) qr[0] = qA + qB; else qr[1] = qA + qB;
+                } else {
+                    qrow[kA] = qA + qB;
+                }
+            }
             // ---- MAP run length r* (A7): eager (key reduced at the barrier) or on demand ----
             int r_ex = -1;
             double qex = 0.0;
@@ -607,7 +624,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                             r = tmod - p;
                             r += (r < 0) ? R : 0;
                         }
-                        const unsigned long long kq = argmax_key(qrow[p], r);  // own cells only
+                        const unsigned long long kq = argmax_key(QREG ? qr[QREG ? j : 0] : qrow[p], r);  // own cells
                         kb = (r <= r_elig && kq > kb) ? kq : kb;
                     }
                 }
@@ -655,29 +672,29 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 if (P.out_pnew) P.out_pnew[s * P.ld_o + tl] = pnum * fast_rcp(Zp);
                 if (P.out_logz) {  // kept mass (A4)
                     const double lzd = fast_log2(Zd, kFmBase);
-                    P.out_logz[s * P.ld_o + tl] = fma(LN2, double(K0 + zexp) + (lzd - lzd_prev), P.ln_omH);
-                    lzd_prev = lzd;
+                    P.out_logz[s * P.ld_o + tl] = fma(LN2, double(K0 + zexp) + (lzd - gs.lzd_prev), P.ln_omH);
+                    gs.lzd_prev = lzd;
                 }
+                gs.zd_prev = Zd;
             }
-            zd_prev = Zd;
             zexp = ((__double2hiint(Zd) >> 20) & 0x7FF) - 1023;
             tmod = (tmod + 1 == R) ? 0 : tmod + 1;
             if constexpr (ROT) {
                 if (++iB == NT) {  // pB crosses a slot boundary: rotate slot j <- slot j+1
                     iB = 0;
                     phi = (phi + 1) & (J - 1);
-                    const double m0 = mu[0], b0 = be[0], l0r = L[0], qf = qrow[i];
+                    const double m0 = mu[0], b0 = be[0], l0r = L[0], qf = QREG ? qr[0] : qrow[i];
 #pragma unroll
                     for (int j = 0; j + 1 < J; ++j) {
                         mu[j] = mu[j + 1];
                         be[j] = be[j + 1];
                         L[j] = L[j + 1];
-                        qrow[i + NT * j] = qrow[i + NT * (j + 1)];
+                        if constexpr (QREG) qr[j] = qr[j + 1]; else qrow[i + NT * j] = qrow[i + NT * (j + 1)];
                     }
                     mu[J - 1] = m0;
                     be[J - 1] = b0;
                     L[J - 1] = l0r;
-                    qrow[i + NT * (J - 1)] = qf;
+                    if constexpr (QREG) qr[J - 1] = qf; else qrow[i + NT * (J - 1)] = qf;
                 }
             }
         }
@@ -692,14 +709,14 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         if (FULL || p < R) {
             P.st_mu[sbase + p] = mu[j];
             P.st_beta[sbase + p] = be[j];
-            P.st_q[sbase + p] = qrow[e];
+            P.st_q[sbase + p] = QREG ? qr[QREG ? j : 0] : qrow[e];
         }
     }
     if (i == 0) {
         SeriesScalars sc;
         sc.mu0 = gs.mu0;
         sc.beta0 = gs.beta0;
-        sc.zd_prev = zd_prev;
+        sc.zd_prev = gs.zd_prev;
         sc.map_prev = map_prev;
         sc.ev_count = ev_count;
         sc.flags = gs.flags;

@@ -70,6 +70,12 @@ constexpr unsigned kFmSmemBytes = 2048u + unsigned(sizeof(FastMathTables));
 // DADD read them as constant-bank operands instead of re-materialising 64-bit immediates
 // in registers every step.
 static __constant__ double c_fm[16];
+// Leading (highest-degree) coefficients rounded to 20 mantissa bits, so that DFMA takes
+// them as 32-bit immediates (no register or uniform-register operand): the rounding
+// (relative 7e-8) is weighted by r^6 < 5e-15 (log2) and r^5 < 3e-11 (exp2), i.e. below
+// 1e-20 absolute.
+constexpr double kLog2C0 = -0.2404491901397705;   // 0xbfcec70a00000000 ~ c_fm[0]
+constexpr double kExp2C0 = 0.0013333559036254883;  // 0x3f55d88000000000 ~ c_fm[8]
 static const double kFastMathConstants[16] = {
     -0.2404491734814939,   0.28853900817779266,  -0.36067376022224085, 0.4808983469629878,   // log2 P
     -0.7213475204444817,   1.4426950408889634,   4503599627371520.0,   6755399441055744.0,   // .., 1/ln2, 2^52+1024, 1.5*2^52
@@ -113,7 +119,7 @@ __device__ __forceinline__ double fast_log2(double x, unsigned fmb) {
     // k + l_i first (off the polynomial's dependency chain; the BOCD cell loop evaluates
     // the same expression stage by stage and must agree bit for bit)
     const double kt = (__hiloint2double(0x43300000, int(tb >> 20)) - c_fm[6]) + t.y;  // k (2^52 + 1024 bias)
-    double p = fma(r, c_fm[0], c_fm[1]);
+    double p = fma(r, kLog2C0, c_fm[1]);
     p = fma(p, r, c_fm[2]);
     p = fma(p, r, c_fm[3]);
     p = fma(p, r, c_fm[4]);
@@ -130,7 +136,7 @@ __device__ __forceinline__ double fast_exp2(double x, unsigned fmb) {
     const unsigned ki = unsigned(__double2loint(zf));
     const double kd = zf - c_fm[7];
     const double r = fma(kd, c_fm[14], xc);  // exact: |r| <= 1/128
-    double p = fma(r, c_fm[8], c_fm[9]);
+    double p = fma(r, kExp2C0, c_fm[9]);
     p = fma(p, r, c_fm[10]);
     p = fma(p, r, c_fm[11]);
     p = fma(p, r, c_fm[12]);
