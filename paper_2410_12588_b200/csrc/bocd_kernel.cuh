@@ -268,6 +268,7 @@ __host__ __device__ constexpr int table_entries(int R) {
 // The dynamic shared window of a non-cluster launch starts at this shared address
 // (after the 1 KB system reservation; no static shared memory in this kernel), so
 // the fast-math tables sit at the compile-time address kFmBase (checked at entry).
+constexpr unsigned kDynBase = 0x400u;
 constexpr unsigned kFmBase = 0x800u;
 
 __device__ __forceinline__ double2 lds_log_entry(unsigned off) {  // off = (index << 4), index < 128
@@ -293,16 +294,17 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     const int R = FULL ? NT * J : P.R;
     const int RT = table_entries<NT, J, FULL, TAB2>(R);
     // dynamic shared memory: [fast-math tables (aligned in kFmSmemBytes)][per-r tables][groups]
-    double2* s_ca = reinterpret_cast<double2*>(smem_raw + kFmSmemBytes);
+    unsigned char* const smem = smem_raw;
+    double2* s_ca = reinterpret_cast<double2*>(smem + kFmSmemBytes);
     double* s_y = reinterpret_cast<double*>(s_ca + RT);
-    unsigned char* gbase = smem_raw + kFmSmemBytes + table_bytes(RT);
+    unsigned char* gbase = smem + kFmSmemBytes + table_bytes(RT);
 
     for (int k = threadIdx.x; k < RT; k += blockDim.x) {
         const int r = k < R ? k : k - R;
         s_ca[k] = P.tab_ca[r];
         s_y[k] = P.tab_y[r];
     }
-    const bool fm_ok = fm_setup(smem_raw, P.fm) == kFmBase;
+    const bool fm_ok = smem_addr(smem_raw) == kDynBase && fm_setup(smem_raw, P.fm) == kFmBase;
     const int g = threadIdx.x / NT;
     const int i = threadIdx.x % NT;
     const int lane = threadIdx.x & 31;
