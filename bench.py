@@ -33,12 +33,15 @@ if ROOT not in sys.path:
 METRIC = "BOCD series·timesteps/sec (R=1024, fp64) at 1/2/4/8 B200; % roofline"
 UNIT = "series*steps/s"
 # FP64-pipe work per cell (one run length, one step): DESIGN.md §6.
-#   The kernel executes 32.9 FP64-pipe instructions per cell (ncu: DFMA+DADD+DMUL+DSETP per
-#   cell, profiles/r01_ncu_top_kernel.txt): 10 arithmetic (NIG update 4, predictive 4, growth /
-#   shift / sum 2... ) + fast_log2 (9) + fast_exp2 (9) + per-step tail work amortised.
-#   roofline.frac therefore equals the FP64-pipe utilisation.  For context the same work with
-#   libdevice log/exp (30 + 18 FP64 instructions, cuobjdump, P0) is 60 instructions per cell.
-FP64_INSTR_PER_CELL = 32.9
+#   The formulation's arithmetic per cell, counted as FP64-pipe instructions:
+#   NIG update 4 (d, mu', x - mu' folded with 1/2, beta'), lg beta' 9 (table-driven
+#   fast_log2), Student-t predictive 3, 2^(l - N) 9 (table-driven fast_exp2 with the
+#   row shift folded into its rounding constant), joint + evidence sum 2  =  27.
+#   Per-step work (group reduction, scalar tail, the tile's prior references) is not
+#   counted, so roofline.frac <= the measured FP64-pipe utilisation (ncu: 28.7 FP64
+#   instructions per cell executed, profiles/r01_ncu_top_kernel.txt).  For context the
+#   same cell with libdevice log/exp (30 + 18 FP64 instructions, cuobjdump, P0) is 60.
+FP64_INSTR_PER_CELL = 27
 FP64_INSTR_PER_CELL_LIBDEVICE = 60
 # FP64 pipe peak: 148 SMs x 64 FP64 lanes/clk x 1965 MHz (sm_max_mhz, MEASURED_PEAKS.json);
 # P0 measured 58.9 DFMA/clk/SM sustained at 1965 MHz (profiles/r01_p0_fp64_peaks.json).
@@ -182,7 +185,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-steps", type=int, default=2048, help="oracle sample length (reference arm)")
-    ap.add_argument("--cpu-sample-steps", type=int, default=2048)
+    ap.add_argument("--cpu-sample-steps", type=int, default=3072)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -300,7 +303,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle
         cores = oracle.max_threads()
-        n_s = 8 * cores
+        n_s = 32 * cores
         v, dt = cpu_baseline_run(cfg, spec, n_s, args.cpu_sample_steps)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"{n_s} C3 series x first {args.cpu_sample_steps} steps, R={cfg.R} "
@@ -315,7 +318,7 @@ def main():
             "config": _config_block(cfg, args, S, world),
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak,
                          "unit": "FP64-pipe instr/s", "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "bocd_update_kernel<128,8,FULL>",
+                         "kernel": "bocd_update_kernel<128,8,FULL,ROT>",
                          "kernel_ms_avg": k_avg, "kernel_share_of_step": k_share,
                          "work_per_cell": FP64_INSTR_PER_CELL,
                          "frac_vs_libdevice_work": FP64_INSTR_PER_CELL_LIBDEVICE * cells_per_launch
