@@ -29,7 +29,7 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, lib: str = LIB, defines: tuple = ()) -> str:
+def build(force: bool = False, verbose: bool = False, lib: str = LIB, defines: tuple = (), extra: tuple = ()) -> str:
     """Builds the library; `lib`/`defines` give alternative builds for A/B tuning (tools/tune_build.py)."""
     if not force and lib == LIB and not _stale():
         return LIB
@@ -38,7 +38,7 @@ def build(force: bool = False, verbose: bool = False, lib: str = LIB, defines: t
 
     def compile_one(src):
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-Xptxas", "-v", "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *FLAGS, *extra, *[f"-D{d}" for d in defines], "-Xptxas", "-v", "-c", os.path.join(CSRC, src), "-o", obj]
         p = subprocess.run(cmd, capture_output=True, text=True)
         if p.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{p.stderr}")

@@ -12,7 +12,9 @@ sys.path.insert(0, ROOT)
 from paper_2410_12588_b200 import build as B  # noqa: E402
 
 if __name__ == "__main__":
-    name, defines = sys.argv[1], tuple(sys.argv[2:])
+    name = sys.argv[1]
+    defines = tuple(a for a in sys.argv[2:] if not a.startswith("-"))
+    extra = tuple(a for a in sys.argv[2:] if a.startswith("-"))  # raw nvcc flags, e.g. -Xptxas=...
     d = os.path.join(ROOT, "tune", name)
     os.makedirs(d, exist_ok=True)
-    print(B.build(force=True, lib=os.path.join(d, "libfalcon_bocd.so"), defines=defines))
+    print(B.build(force=True, lib=os.path.join(d, "libfalcon_bocd.so"), defines=defines, extra=extra))
