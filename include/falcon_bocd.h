@@ -80,7 +80,9 @@ typedef struct {
 } falcon_bocd_config;
 
 /* One reported change point.  t: global step; cp_index = t - r*_t + 1, the
- * first index of the MAP segment; flags: FALCON_EV_*; p_new as defined above. */
+ * first index of the MAP segment; flags: the FALCON_EV_* bits of event_mask that
+ * fired at t (bits outside event_mask are never reported, so records do not depend
+ * on which per-step outputs a call requested); p_new as defined above. */
 typedef struct {
     int64_t series;
     int64_t t;

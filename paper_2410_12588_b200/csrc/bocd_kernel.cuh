@@ -119,7 +119,8 @@ struct __align__(16) GroupSmem {
     double mu0, beta0, L0, zd_prev;  // zd_prev: kept current by thread 0 every step
     double lzd_prev;                 // lg Zd_{t-1} (log-evidence output, thread 0)
     int map_prev, ev_count, flags, pad;
-    unsigned long long mbar[2];
+    unsigned long long mbar[2];  // x tiles
+    unsigned long long mbar_st;  // prefetched state of the next unit (PREF kernels)
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -209,9 +210,12 @@ __device__ __forceinline__ bool tile_tma_ok(const KParams& P, int k) {
 // Shared memory of one CTA: tables, then per group: GroupSmem + the q row [R].
 // TAB2: the per-r tables are stored twice (entries r and r+R) so the ring index
 // (t - p) mod R becomes (t - p + R) with no masking and compile-time offsets per cell.
-template <int NT>
+__host__ __device__ constexpr size_t q_row_doubles(int R) { return (size_t(R) + 1) & ~size_t(1); }  // 16-B rows
+// per group: GroupSmem, the q row, and (PREF) the prefetch buffer [mu R][beta R][q R][scalars]
+template <int NT, bool PREF>
 __host__ __device__ constexpr size_t group_bytes(int R) {
-    return sizeof(GroupSmem<NT>) + ((size_t(R) * sizeof(double) + 15) & ~size_t(15));  // keep 16-B alignment
+    return sizeof(GroupSmem<NT>) + q_row_doubles(R) * sizeof(double) +
+           (PREF ? ((3 * size_t(R) * sizeof(double) + sizeof(SeriesScalars) + 15) & ~size_t(15)) : 0);
 }
 // bytes of the per-r tables ({c_r/ln2, alpha_r} and y_r) for `entries` table rows
 __host__ __device__ constexpr size_t table_bytes(int entries) {
@@ -282,15 +286,23 @@ __device__ __forceinline__ double lds_exp_entry(unsigned off) {  // off = (index
     return v;
 }
 
-template <int NT, int J, bool FULL, bool TAB2, bool EAGER, int SPB, int MINB>
+// PREF is used for power-of-two R up to 1024, where the buffer (24 B x R per series) fits
+// without lowering the 2-CTA/SM occupancy
+template <int NT, int J, bool FULL>
+constexpr bool kPrefOk = FULL && NT * J <= 1024;
+
+// Persistent kernel: each CTA loops over work units of SPB series (unit u = series
+// [u*SPB, u*SPB + SPB)), u = blockIdx.x, blockIdx.x + gridDim.x, ...  Tables are set up
+// once per CTA.  PREF: the state rows (mu, beta, q) and scalars of the group's NEXT unit
+// are prefetched into shared memory by 1-D TMA bulk copies while the current unit computes
+// (streaming calls with a few steps per call are then bound by HBM, not by load latency).
+template <int NT, int J, bool FULL, bool TAB2, bool EAGER, int SPB, int MINB, bool PERSIST>
 __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParams P) {
+    // PERSIST: grid = co-resident CTAs looping over units (streaming calls); otherwise one
+    // unit per CTA (long calls: the hardware scheduler, no loop overhead).  Same arithmetic.
+    constexpr bool PREF = PERSIST && kPrefOk<NT, J, FULL>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr bool ROT = FULL;
-#ifdef FALCON_BOCD_QREG
-    constexpr bool QREG = ROT;  // q in registers (slot order) instead of the shared row
-#else
-    constexpr bool QREG = false;
-#endif
     const int R = FULL ? NT * J : P.R;
     const int RT = table_entries<NT, J, FULL, TAB2>(R);
     // dynamic shared memory: [fast-math tables (aligned in kFmSmemBytes)][per-r tables][groups]
@@ -309,423 +321,451 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     const int i = threadIdx.x % NT;
     const int lane = threadIdx.x & 31;
     const int w = i >> 5;
-    GroupSmem<NT>& gs = *reinterpret_cast<GroupSmem<NT>*>(gbase + size_t(g) * group_bytes<NT>(R));
+    GroupSmem<NT>& gs = *reinterpret_cast<GroupSmem<NT>*>(gbase + size_t(g) * group_bytes<NT, PREF>(R));
     // the series' unnormalised run-length posterior q: FULL in slot order (element
     // i + NT*j = slot j of thread i), else in ring-position order
     double* qrow = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(&gs) + sizeof(GroupSmem<NT>));
-    const int64_t s = int64_t(blockIdx.x) * SPB + g;
-    const bool active = s < P.S;
-    const double* xrow = P.x + (active ? s : 0) * P.ld;
-    const int ntiles = (P.T + kTile - 1) / kTile;
+    // PREF: the prefetched next-unit state [mu R][beta R][q R][SeriesScalars], position order
+    double* const pf = qrow + q_row_doubles(R);
+    SeriesScalars* const pf_sc = reinterpret_cast<SeriesScalars*>(pf + 3 * size_t(R));
+    const int64_t nunits = (P.S + SPB - 1) / SPB;
     if (i == 0) {
         mbar_init(&gs.mbar[0], 1);
         mbar_init(&gs.mbar[1], 1);
+        mbar_init(&gs.mbar_st, 1);
         mbar_fence_init();
     }
     __syncthreads();
-    if (!active) return;
-
-    // Prefetch tile 0 (TMA) as early as possible.
-    if (i == 0 && ntiles > 0 && tile_tma_ok(P, 0)) issue_tile_tma<NT>(gs, xrow, 0, P.T);
-
-    // ---- load or initialise the state ------------------------------------
-    double mu[J], be[J], L[J];
-    double qr[QREG ? J : 1];
-    const int64_t sbase = s * int64_t(R);
-    if (i == 0) {
-        SeriesScalars sc = P.scal[s];
-        if (P.t0 == 0) {
-            if (P.prior_first_obs && P.T > 0) {
-                const double x0 = xrow[0];
-                sc.mu0 = x0;
-                sc.beta0 = P.alpha0 * (P.prior_cov * x0) * (P.prior_cov * x0);
-            }
-            sc.zd_prev = P.omH;  // R_{-1} = [1, 0, ...] = q (1-H)/Zd
-            sc.map_prev = 0;
-        }
-        const bool ok = sc.beta0 >= 2.2250738585072014e-308 && sc.beta0 < 1e300 && isfinite(sc.mu0);
-        gs.mu0 = sc.mu0;
-        gs.beta0 = ok ? sc.beta0 : 1.0;
-        gs.L0 = fast_log2(gs.beta0, kFmBase);
-        gs.zd_prev = sc.zd_prev;
-        gs.map_prev = sc.map_prev;
-        gs.ev_count = sc.ev_count;
-        gs.flags = sc.flags | (ok ? 0 : 2) | (fm_ok ? 0 : 4);
-    }
-    group_sync<NT>(g);
-    // the prior and the rarely used per-series scalars stay in shared memory (gs) so
-    // that the step loop keeps its registers for the cells
-    int zexp = ((__double2hiint(gs.zd_prev) >> 20) & 0x7FF) - 1023;  // binary exponent of Zd_{t-1}
-    int map_prev = gs.map_prev, ev_count = gs.ev_count;
-    // ring bookkeeping.  FULL: the recycled position pB = (t+1) mod R = NT*phi + iB;
-    // generic: tmod = t mod R.
-    int tmod = int(P.t0 % R);
-    int iB = 0, phi = 0;
-    if constexpr (ROT) {
-        const int pB0 = (tmod + 1 == R) ? 0 : tmod + 1;
-        iB = pB0 % NT;
-        phi = pB0 / NT;
-    }
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-        const int p = ROT ? i + NT * ((j + phi) & (J - 1)) : i + NT * j;  // position of slot j
-        const int e = ROT ? i + NT * j : p;                                // its q element
-        if (FULL || p < R) {
-            if (P.t0 == 0) {
-                mu[j] = gs.mu0;
-                be[j] = gs.beta0;
-                L[j] = gs.L0;
-                const double q0v = (p == 0) ? 1.0 : 0.0;  // before x_0 a segment starts w.p. 1 (Q8)
-                if constexpr (QREG) qr[j] = q0v; else qrow[e] = q0v;
-            } else {
-                mu[j] = P.st_mu[sbase + p];
-                be[j] = P.st_beta[sbase + p];
-                if constexpr (QREG) qr[j] = P.st_q[sbase + p]; else qrow[e] = P.st_q[sbase + p];
-                L[j] = fast_log2(be[j], kFmBase);
-            }
-        } else {
-            mu[j] = gs.mu0;
-            be[j] = gs.beta0;
-            L[j] = gs.L0;
-        }
-    }
-
+    const int ntiles = (P.T + kTile - 1) / kTile;
     const bool merge = (P.mode == 0);
     // argmax-eligible run lengths: MERGE r <= R-3 (slot R-1 is the bucket), DROP r <= R-2
     const int r_elig = merge ? R - 3 : R - 2;
-    bool nonfinite = false;
-    if (i == 0 && P.out_logz) gs.lzd_prev = fast_log2(gs.zd_prev, kFmBase);
+    unsigned xphase = 0u;  // parity of the two x-tile mbarriers (bit b: mbar[b])
+    unsigned sphase = 0u;  // parity of the state mbarrier
+    auto issue_state = [&](int64_t sn) {  // thread 0 of the group: next unit's state -> pf
+        const unsigned bytes = unsigned(3 * size_t(R) * sizeof(double) + sizeof(SeriesScalars));
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&gs.mbar_st, bytes);
+        const size_t rb = size_t(R) * sizeof(double);
+        tma_load_1d(pf, P.st_mu + sn * R, unsigned(rb), &gs.mbar_st);
+        tma_load_1d(pf + R, P.st_beta + sn * R, unsigned(rb), &gs.mbar_st);
+        tma_load_1d(pf + 2 * size_t(R), P.st_q + sn * R, unsigned(rb), &gs.mbar_st);
+        tma_load_1d(pf_sc, P.scal + sn, unsigned(sizeof(SeriesScalars)), &gs.mbar_st);
+    };
+    if constexpr (PREF) {
+        const int64_t s0 = int64_t(blockIdx.x) * SPB + g;
+        if (i == 0 && P.t0 > 0 && blockIdx.x < nunits && s0 < P.S) issue_state(s0);
+    }
 
-    for (int k = 0; k < ntiles; ++k) {
-        const int base = k * kTile;
-        const int n = min(kTile, P.T - base);
-        const int buf = k & 1;
-        // prefetch the next tile into the other buffer (its previous readers all
-        // passed at least one group barrier since their last read)
-        if (i == 0 && k + 1 < ntiles && tile_tma_ok(P, k + 1)) issue_tile_tma<NT>(gs, xrow, k + 1, P.T);
-        if (tile_tma_ok(P, k)) {
-            mbar_wait(&gs.mbar[buf], unsigned(k >> 1) & 1u);
-        } else {
-            for (int q = i; q < n; q += NT) gs.xbuf[buf][q] = xrow[base + q];
-            group_sync<NT>(g);
+    for (int64_t u = blockIdx.x; u < nunits; u += PERSIST ? int64_t(gridDim.x) : nunits) {
+        const int64_t s = u * SPB + g;
+        if (s >= P.S) break;  // group-uniform; later units only have larger s
+        const double* xrow = P.x + s * P.ld;
+        // Prefetch tile 0 (TMA) as early as possible.
+        if (i == 0 && ntiles > 0 && tile_tma_ok(P, 0)) issue_tile_tma<NT>(gs, xrow, 0, P.T);
+
+        // ---- load or initialise the state --------------------------------
+        double mu[J], be[J], L[J];
+        const int64_t sbase = s * int64_t(R);
+        if constexpr (PREF) {
+            if (P.t0 > 0) {
+                mbar_wait(&gs.mbar_st, sphase);
+                sphase ^= 1u;
+            }
         }
-        // the tile's exponent references K0_t = round(l0_t), spread over the group
-        for (int q = i; q < n; q += NT) {
-            const double xq = gs.xbuf[buf][q];
-            if (!isfinite(xq)) nonfinite = true;
-            const double l0 = prior_l2(xq, gs.mu0, gs.beta0, gs.L0, s_ca[0], s_y[0], kFmBase);
-            gs.kbuf[buf][q] = __double2int_rn(fmin(fmax(l0, -1048576.0), 1048576.0));
+        if (i == 0) {
+            SeriesScalars sc = (PREF && P.t0 > 0) ? *pf_sc : P.scal[s];
+            if (P.t0 == 0) {
+                if (P.prior_first_obs && P.T > 0) {
+                    const double x0 = xrow[0];
+                    sc.mu0 = x0;
+                    sc.beta0 = P.alpha0 * (P.prior_cov * x0) * (P.prior_cov * x0);
+                }
+                sc.zd_prev = P.omH;  // R_{-1} = [1, 0, ...] = q (1-H)/Zd
+                sc.map_prev = 0;
+            }
+            const bool ok = sc.beta0 >= 2.2250738585072014e-308 && sc.beta0 < 1e300 && isfinite(sc.mu0);
+            gs.mu0 = sc.mu0;
+            gs.beta0 = ok ? sc.beta0 : 1.0;
+            gs.L0 = fast_log2(gs.beta0, kFmBase);
+            gs.zd_prev = sc.zd_prev;
+            gs.map_prev = sc.map_prev;
+            gs.ev_count = sc.ev_count;
+            gs.flags = sc.flags | (ok ? 0 : 2) | (fm_ok ? 0 : 4);
         }
         group_sync<NT>(g);
-        for (int q = 0; q < n; ++q) {
-            const int tl = base + q;
-            const int64_t t = P.t0 + tl;
-            const double x = gs.xbuf[buf][q];
-            const double hx = 0.5 * x;
-            const int K0 = gs.kbuf[buf][q];
-            // exp2 rounding constant 1.5*2^52 + 2^31 - 64 N_t: zf = fma(l, 64, C7) holds
-            // round(64 l) - 64 N_t + 2^31 in its low word (exact integers below 2^52)
-            const double C7 = __hiloint2double(0x43380000, int(0x80000000u - unsigned(K0 + zexp) * 64u));
-            // ---- A1-A4 for the J cells (groups of G, every stage across the group) ----
-            // table index of slot j: ib - NT*j  (= r or r + R).  FULL: r of slot j is
-            // (pB - 1 - p) mod R = (iB - 1 - i - NT j) mod R.
-            const int ib = ROT ? iB - 1 - i + R : tmod - i + R;
-            double sum = 0.0;
-            unsigned long long key = 0ull;
+        // the prior and the rarely used per-series scalars stay in shared memory (gs) so
+        // that the step loop keeps its registers for the cells
+        int zexp = ((__double2hiint(gs.zd_prev) >> 20) & 0x7FF) - 1023;  // binary exponent of Zd_{t-1}
+        int map_prev = gs.map_prev, ev_count = gs.ev_count;
+        // ring bookkeeping.  FULL: the recycled position pB = (t+1) mod R = NT*phi + iB;
+        // generic: tmod = t mod R.
+        int tmod = int(P.t0 % R);
+        int iB = 0, phi = 0;
+        if constexpr (ROT) {
+            const int pB0 = (tmod + 1 == R) ? 0 : tmod + 1;
+            iB = pB0 % NT;
+            phi = pB0 / NT;
+        }
 #pragma unroll
-            for (int j0 = 0; j0 < J; j0 += kG) {
-                constexpr int G = (J < kG) ? J : kG;
-                int idx[G];
-                double2 ca[G];
-                double yv[G], qv[G], d[G], bn[G];
-#pragma unroll
-                for (int kk = 0; kk < G; ++kk) {  // table + row loads
-                    const int j = j0 + kk;
-                    const int p = i + NT * j;
-                    if (ROT || TAB2) {
-                        idx[kk] = ib - NT * j;
+        for (int j = 0; j < J; ++j) {
+            const int p = ROT ? i + NT * ((j + phi) & (J - 1)) : i + NT * j;  // position of slot j
+            const int e = ROT ? i + NT * j : p;                                // its q element
+            if (FULL || p < R) {
+                if (P.t0 == 0) {
+                    mu[j] = gs.mu0;
+                    be[j] = gs.beta0;
+                    L[j] = gs.L0;
+                    qrow[e] = (p == 0) ? 1.0 : 0.0;  // before x_0 a segment starts w.p. 1 (Q8)
+                } else {
+                    if constexpr (PREF) {
+                        mu[j] = pf[p];
+                        be[j] = pf[R + p];
+                        qrow[e] = pf[2 * R + p];
                     } else {
-                        idx[kk] = tmod - p;
-                        idx[kk] += (idx[kk] < 0) ? R : 0;
+                        mu[j] = P.st_mu[sbase + p];
+                        be[j] = P.st_beta[sbase + p];
+                        qrow[e] = P.st_q[sbase + p];
                     }
-                    if (!FULL && p >= R) idx[kk] = 0;  // masked cell: any valid entry
-                    ca[kk] = s_ca[idx[kk]];
-                    yv[kk] = s_y[idx[kk]];
-                    if constexpr (QREG) qv[kk] = qr[j];
-                    else qv[kk] = (FULL || p < R) ? qrow[p] : 0.0;
+                    L[j] = fast_log2(be[j], kFmBase);
                 }
-                // A1: NIG update
+            } else {
+                mu[j] = gs.mu0;
+                be[j] = gs.beta0;
+                L[j] = gs.L0;
+            }
+        }
+        if constexpr (PREF) {
+            // pf is free once every thread of the group has read it: prefetch the next unit
+            group_sync<NT>(g);
+            const int64_t sn = s + int64_t(gridDim.x) * SPB;
+            if (i == 0 && P.t0 > 0 && sn < P.S) issue_state(sn);
+        }
+        bool nonfinite = false;
+        if (i == 0 && P.out_logz) gs.lzd_prev = fast_log2(gs.zd_prev, kFmBase);
+
+        for (int k = 0; k < ntiles; ++k) {
+            const int base = k * kTile;
+            const int n = min(kTile, P.T - base);
+            const int buf = k & 1;
+            // prefetch the next tile into the other buffer (its previous readers all
+            // passed at least one group barrier since their last read)
+            if (i == 0 && k + 1 < ntiles && tile_tma_ok(P, k + 1)) issue_tile_tma<NT>(gs, xrow, k + 1, P.T);
+            if (tile_tma_ok(P, k)) {
+                mbar_wait(&gs.mbar[buf], (xphase >> buf) & 1u);
+                xphase ^= 1u << buf;
+            } else {
+                for (int q = i; q < n; q += NT) gs.xbuf[buf][q] = xrow[base + q];
+                group_sync<NT>(g);
+            }
+            // the tile's exponent references K0_t = round(l0_t), spread over the group
+            for (int q = i; q < n; q += NT) {
+                const double xq = gs.xbuf[buf][q];
+                if (!isfinite(xq)) nonfinite = true;
+                const double l0 = prior_l2(xq, gs.mu0, gs.beta0, gs.L0, s_ca[0], s_y[0], kFmBase);
+                gs.kbuf[buf][q] = __double2int_rn(fmin(fmax(l0, -1048576.0), 1048576.0));
+            }
+            group_sync<NT>(g);
+            for (int q = 0; q < n; ++q) {
+                const int tl = base + q;
+                const int64_t t = P.t0 + tl;
+                const double x = gs.xbuf[buf][q];
+                const double hx = 0.5 * x;
+                const int K0 = gs.kbuf[buf][q];
+                // exp2 rounding constant 1.5*2^52 + 2^31 - 64 N_t: zf = fma(l, 64, C7) holds
+                // round(64 l) - 64 N_t + 2^31 in its low word (exact integers below 2^52)
+                const double C7 = __hiloint2double(0x43380000, int(0x80000000u - unsigned(K0 + zexp) * 64u));
+                // ---- A1-A4 for the J cells (groups of G, every stage across the group) ----
+                // table index of slot j: ib - NT*j  (= r or r + R).  FULL: r of slot j is
+                // (pB - 1 - p) mod R = (iB - 1 - i - NT j) mod R.
+                const int ib = ROT ? iB - 1 - i + R : tmod - i + R;
+                double sum = 0.0;
+                unsigned long long key = 0ull;
 #pragma unroll
-                for (int kk = 0; kk < G; ++kk) d[kk] = x - mu[j0 + kk];
+                for (int j0 = 0; j0 < J; j0 += kG) {
+                    constexpr int G = (J < kG) ? J : kG;
+                    int idx[G];
+                    double2 ca[G];
+                    double yv[G], qv[G], d[G], bn[G];
 #pragma unroll
-                for (int kk = 0; kk < G; ++kk) mu[j0 + kk] = fma(d[kk], yv[kk], mu[j0 + kk]);
+                    for (int kk = 0; kk < G; ++kk) {  // table + row loads
+                        const int j = j0 + kk;
+                        const int p = i + NT * j;
+                        if (ROT || TAB2) {
+                            idx[kk] = ib - NT * j;
+                        } else {
+                            idx[kk] = tmod - p;
+                            idx[kk] += (idx[kk] < 0) ? R : 0;
+                        }
+                        if (!FULL && p >= R) idx[kk] = 0;  // masked cell: any valid entry
+                        ca[kk] = s_ca[idx[kk]];
+                        yv[kk] = s_y[idx[kk]];
+                        qv[kk] = (FULL || p < R) ? qrow[p] : 0.0;
+                    }
+                    // A1: NIG update
 #pragma unroll
-                for (int kk = 0; kk < G; ++kk) bn[kk] = fma(d[kk], fma(mu[j0 + kk], -0.5, hx), be[j0 + kk]);
-                // A2: lg beta' (fast_log2 of fastmath.cuh, stage by stage)
-                unsigned tb[G];
-                double2 lt[G];
-                double rl[G], kt[G], pl[G];
+                    for (int kk = 0; kk < G; ++kk) d[kk] = x - mu[j0 + kk];
 #pragma unroll
-                for (int kk = 0; kk < G; ++kk) {
-                    tb[kk] = unsigned(__double2hiint(bn[kk])) + 0x00196000u;
-                    lt[kk] = lds_log_entry((tb[kk] >> 9) & 0x7F0u);
-                }
+                    for (int kk = 0; kk < G; ++kk) mu[j0 + kk] = fma(d[kk], yv[kk], mu[j0 + kk]);
 #pragma unroll
-                for (int kk = 0; kk < G; ++kk) {
-                    const double invs = __hiloint2double(
-                        __double2hiint(lt[kk].x) + 0x40000000 - int(tb[kk] & 0xFFF00000u), __double2loint(lt[kk].x));
-                    rl[kk] = fma(bn[kk], invs, -1.0);
-                    kt[kk] = (__hiloint2double(0x43300000, int(tb[kk] >> 20)) - c_fm[6]) + lt[kk].y;
-                }
+                    for (int kk = 0; kk < G; ++kk) bn[kk] = fma(d[kk], fma(mu[j0 + kk], -0.5, hx), be[j0 + kk]);
+                    // A2: lg beta' (fast_log2 of fastmath.cuh, stage by stage)
+                    unsigned tb[G];
+                    double2 lt[G];
+                    double rl[G], kt[G], pl[G];
 #pragma unroll
-                for (int kk = 0; kk < G; ++kk) pl[kk] = fma(rl[kk], kLog2C0, c_fm[1]);
+                    for (int kk = 0; kk < G; ++kk) {
+                        tb[kk] = unsigned(__double2hiint(bn[kk])) + 0x00196000u;
+                        lt[kk] = lds_log_entry((tb[kk] >> 9) & 0x7F0u);
+                    }
 #pragma unroll
-                for (int c = 2; c <= 5; ++c) {
+                    for (int kk = 0; kk < G; ++kk) {
+                        const double invs = __hiloint2double(__double2hiint(lt[kk].x) + 0x40000000 -
+                                                                 int(tb[kk] & 0xFFF00000u),
+                                                             __double2loint(lt[kk].x));
+                        rl[kk] = fma(bn[kk], invs, -1.0);
+                        kt[kk] = (__hiloint2double(0x43300000, int(tb[kk] >> 20)) - c_fm[6]) + lt[kk].y;
+                    }
 #pragma unroll
-                    for (int kk = 0; kk < G; ++kk) pl[kk] = fma(pl[kk], rl[kk], c_fm[c]);
-                }
-                double ell[G];
+                    for (int kk = 0; kk < G; ++kk) pl[kk] = fma(rl[kk], kLog2C0, c_fm[1]);
 #pragma unroll
-                for (int kk = 0; kk < G; ++kk) {
-                    const int j = j0 + kk;
-                    const double Ln = fma(rl[kk], pl[kk], kt[kk]);
-                    ell[kk] = fma(-0.5, Ln, fma(ca[kk].y, L[j] - Ln, ca[kk].x));
-                    L[j] = Ln;
-                    be[j] = bn[kk];
-                }
-                // A3: q' = q 2^(l - N_t)  (fast_exp2 with the shifted rounding constant)
-                double re[G], pe[G], Tv[G];
-                unsigned ki[G];
+                    for (int c = 2; c <= 5; ++c) {
 #pragma unroll
-                for (int kk = 0; kk < G; ++kk) {
-                    const double zf = fma(ell[kk], 64.0, C7);
-                    ki[kk] = unsigned(__double2loint(zf));
-                    re[kk] = fma(zf - C7, -0.015625, ell[kk]);  // exact, |re| <= 1/128
-                    Tv[kk] = lds_exp_entry((ki[kk] << 3) & 0x1F8u);
-                }
+                        for (int kk = 0; kk < G; ++kk) pl[kk] = fma(pl[kk], rl[kk], c_fm[c]);
+                    }
+                    double ell[G];
 #pragma unroll
-                for (int kk = 0; kk < G; ++kk) pe[kk] = fma(re[kk], kExp2C0, c_fm[9]);
+                    for (int kk = 0; kk < G; ++kk) {
+                        const int j = j0 + kk;
+                        const double Ln = fma(rl[kk], pl[kk], kt[kk]);
+                        ell[kk] = fma(-0.5, Ln, fma(ca[kk].y, L[j] - Ln, ca[kk].x));
+                        L[j] = Ln;
+                        be[j] = bn[kk];
+                    }
+                    // A3: q' = q 2^(l - N_t)  (fast_exp2 with the shifted rounding constant)
+                    double re[G], pe[G], Tv[G];
+                    unsigned ki[G];
 #pragma unroll
-                for (int c = 10; c <= 12; ++c) {
+                    for (int kk = 0; kk < G; ++kk) {
+                        const double zf = fma(ell[kk], 64.0, C7);
+                        ki[kk] = unsigned(__double2loint(zf));
+                        re[kk] = fma(zf - C7, -0.015625, ell[kk]);  // exact, |re| <= 1/128
+                        Tv[kk] = lds_exp_entry((ki[kk] << 3) & 0x1F8u);
+                    }
 #pragma unroll
-                    for (int kk = 0; kk < G; ++kk) pe[kk] = fma(pe[kk], re[kk], c_fm[c]);
-                }
+                    for (int kk = 0; kk < G; ++kk) pe[kk] = fma(re[kk], kExp2C0, c_fm[9]);
 #pragma unroll
-                for (int kk = 0; kk < G; ++kk) {
-                    const int j = j0 + kk;
-                    const int p = i + NT * j;
-                    const double qq = pe[kk] * re[kk];
-                    // 2^e, e = floor(n/64) for n = ki - 2^31: exactly 0 below 2^-1021, e clamped
-                    // at +1000; the 2^31 offset vanishes mod 2^32 in the exponent field
-                    const bool dead = ki[kk] < 0x80000000u - 65344u;
-                    const unsigned kc = min(ki[kk], 0x80000000u + 64063u);
-                    const double Ts =
-                        __hiloint2double(int((kc >> 6) << 20) + __double2hiint(Tv[kk]), __double2loint(Tv[kk]));
-                    const double E = dead ? 0.0 : fma(Ts, qq, Ts);
-                    if (FULL || p < R) {
-                        const double qn = qv[kk] * E;
-                        if constexpr (QREG) qr[j] = qn; else qrow[p] = qn;
-                        sum += qn;
-                        if constexpr (EAGER) {
-                            int r = idx[kk];
-                            r -= (r >= R) ? R : 0;
-                            const unsigned long long kq = argmax_key(qn, r);
-                            key = (r <= r_elig && kq > key) ? kq : key;
+                    for (int c = 10; c <= 12; ++c) {
+#pragma unroll
+                        for (int kk = 0; kk < G; ++kk) pe[kk] = fma(pe[kk], re[kk], c_fm[c]);
+                    }
+#pragma unroll
+                    for (int kk = 0; kk < G; ++kk) {
+                        const int j = j0 + kk;
+                        const int p = i + NT * j;
+                        const double qq = pe[kk] * re[kk];
+                        // 2^e, e = floor(n/64) for n = ki - 2^31: exactly 0 below 2^-1021, e clamped
+                        // at +1000; the 2^31 offset vanishes mod 2^32 in the exponent field
+                        const bool dead = ki[kk] < 0x80000000u - 65344u;
+                        const unsigned kc = min(ki[kk], 0x80000000u + 64063u);
+                        const double Ts = __hiloint2double(int((kc >> 6) << 20) + __double2hiint(Tv[kk]),
+                                                           __double2loint(Tv[kk]));
+                        const double E = dead ? 0.0 : fma(Ts, qq, Ts);
+                        if (FULL || p < R) {
+                            const double qn = qv[kk] * E;
+                            qrow[p] = qn;
+                            sum += qn;
+                            if constexpr (EAGER) {
+                                int r = idx[kk];
+                                r -= (r >= R) ? R : 0;
+                                const unsigned long long kq = argmax_key(qn, r);
+                                key = (r <= r_elig && kq > key) ? kq : key;
+                            }
                         }
                     }
                 }
-            }
-            // the three cells the tail needs (r = R-2, R-1, 0) are published by their owners
-            // (kB / kA are overwritten right after the barrier); kX = their q elements
-            const int par = tl & 1;
-            int kA, kB, k0;
-            if constexpr (ROT) {
-                kB = iB;                        // slot 0 of thread iB
-                kA = iB + 1;                    // slot 0 of thread iB+1, or slot 1 of thread 0
-                k0 = (iB == 0) ? R - 1 : iB - 1;  // slot 0 of thread iB-1, or slot J-1 of thread NT-1
-            } else {
-                kB = (tmod + 1 == R) ? 0 : tmod + 1;
-                kA = (kB + 1 == R) ? 0 : kB + 1;
-                k0 = tmod;
-            }
-            if constexpr (QREG) {
-                if ((kA % NT) == i) gs.spec[par][0] = (kA < NT) ? qr[0] : qr[1];
-                if (kB == i) gs.spec[par][1] = qr[0];
-                if ((k0 % NT) == i) gs.spec[par][2] = (k0 < NT) ? qr[0] : qr[J - 1];
-            } else {
+                // the three cells the tail needs (r = R-2, R-1, 0) are published by their owners
+                // (kB / kA are overwritten right after the barrier); kX = their q elements
+                const int par = tl & 1;
+                int kA, kB, k0;
+                if constexpr (ROT) {
+                    kB = iB;                          // slot 0 of thread iB
+                    kA = iB + 1;                      // slot 0 of thread iB+1, or slot 1 of thread 0
+                    k0 = (iB == 0) ? R - 1 : iB - 1;  // slot 0 of thread iB-1, or slot J-1 of thread NT-1
+                } else {
+                    kB = (tmod + 1 == R) ? 0 : tmod + 1;
+                    kA = (kB + 1 == R) ? 0 : kB + 1;
+                    k0 = tmod;
+                }
                 if ((kA % NT) == i) gs.spec[par][0] = qrow[kA];
                 if ((kB % NT) == i) gs.spec[par][1] = qrow[kB];
                 if ((k0 % NT) == i) gs.spec[par][2] = qrow[k0];
-            }
-            // ---- group sum (and, EAGER, argmax): the step's only barrier ----------------
+                // ---- group sum (and, EAGER, argmax): the step's only barrier ------------
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-            if constexpr (EAGER) key = warp_max_u64(key);
-            if constexpr (NT > 32) {
-                if (lane == 0) {
-                    gs.red2[par][w] = sum;
-                    if (EAGER) gs.red1[par][w] = key;
-                }
-                group_sync<NT>(g);
-                sum = gs.red2[par][0];
-#pragma unroll
-                for (int ww = 1; ww < NT / 32; ++ww) sum += gs.red2[par][ww];
-                if constexpr (EAGER) {
-#pragma unroll
-                    for (int ww = 0; ww < NT / 32; ++ww) {
-                        const unsigned long long o = gs.red1[par][ww];
-                        key = o > key ? o : key;
-                    }
-                }
-            } else {
-                group_sync<NT>(g);
-            }
-            // ---- the scalar tail (A5-A8): group-uniform, no transcendentals ---------------
-            const double Z = sum;
-            const double qA = gs.spec[par][0], qB = gs.spec[par][1], q0 = gs.spec[par][2];
-            const double Zd = merge ? Z : Z - P.omH * qB;       // normaliser of the new posterior
-            const double Zp = merge ? Z : Z - qB;               // p_new = pnum / Zp
-            const double pnum = (merge && R == 2) ? Z : q0;     // MERGE R = 2: p_new = 1
-            uint32_t fl = (t > 0 && pnum > P.theta * Zp) ? 1u : 0u;
-            if ((kB % NT) == i) {
-                if constexpr (QREG) qr[0] = P.hr * Z; else qrow[kB] = P.hr * Z;  // R_t(0) = H Z / Zd
-                if constexpr (ROT) {
-                    mu[0] = gs.mu0;  // the recycled cell is slot 0
-                    be[0] = gs.beta0;
-                    L[0] = gs.L0;
-                } else {
-                    set_stats<J>(mu, be, L, kB / NT, gs.mu0, gs.beta0, gs.L0);
-                }
-            }
-            if (merge && (kA % NT) == i) {  // bucket
-                if constexpr (QREG) {
-                    if (kA < NT) qr[0] = qA + qB; else qr[1] = qA + qB;
-                } else {
-                    qrow[kA] = qA + qB;
-                }
-            }
-            // ---- MAP run length r* (A7): eager (key reduced at the barrier) or on demand ----
-            int r_ex = -1;
-            double qex = 0.0;
-            if constexpr (EAGER) {
-                if (key != 0ull) {
-                    r_ex = key_r(key);
-                    qex = key_val(key);
-                }
-            } else if (fl & P.ev_mask) {  // group-uniform: an event at this step
-                unsigned long long kb = 0ull;
-#pragma unroll
-                for (int j = 0; j < J; ++j) {
-                    const int p = i + NT * j;
-                    if (FULL || p < R) {
-                        int r;
-                        if (ROT || TAB2) {
-                            r = ib - NT * j;
-                            r -= (r >= R) ? R : 0;
-                        } else {
-                            r = tmod - p;
-                            r += (r < 0) ? R : 0;
-                        }
-                        const unsigned long long kq = argmax_key(QREG ? qr[QREG ? j : 0] : qrow[p], r);  // own cells
-                        kb = (r <= r_elig && kq > kb) ? kq : kb;
-                    }
-                }
-                kb = warp_max_u64(kb);
+                for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+                if constexpr (EAGER) key = warp_max_u64(key);
                 if constexpr (NT > 32) {
-                    if (lane == 0) gs.red3[w] = kb;
+                    if (lane == 0) {
+                        gs.red2[par][w] = sum;
+                        if (EAGER) gs.red1[par][w] = key;
+                    }
                     group_sync<NT>(g);
+                    sum = gs.red2[par][0];
 #pragma unroll
-                    for (int ww = 0; ww < NT / 32; ++ww) {
-                        const unsigned long long o = gs.red3[ww];
-                        kb = o > kb ? o : kb;
+                    for (int ww = 1; ww < NT / 32; ++ww) sum += gs.red2[par][ww];
+                    if constexpr (EAGER) {
+#pragma unroll
+                        for (int ww = 0; ww < NT / 32; ++ww) {
+                            const unsigned long long o = gs.red1[par][ww];
+                            key = o > key ? o : key;
+                        }
                     }
-                    group_sync<NT>(g);  // red3 is reused at the next event step
-                }
-                if (kb != 0ull) {
-                    r_ex = key_r(kb);
-                    qex = key_val(kb);
-                }
-            }
-            if (EAGER || (fl & P.ev_mask)) {
-                int rstar;
-                if (merge) {
-                    // bucket (qA + qB) vs the best growth slot (ties -> the smaller run length)
-                    rstar = (r_ex < 0 || (qA + qB) > qex) ? R - 1 : r_ex + 1;
                 } else {
-                    rstar = r_ex + 1;
+                    group_sync<NT>(g);
                 }
-                if (EAGER && t > 0 && rstar < min(map_prev + 1, R - 1)) fl |= 2u;
-                map_prev = rstar;
-                if (i == 0 && P.out_map) P.out_map[s * P.ld_o + tl] = rstar;
-                if (fl & P.ev_mask) {
-                    if (i == 0 && ev_count < P.ev_cap) {
-                        EventRec ev;
-                        ev.t = t;
-                        ev.cp_index = t - rstar + 1;
-                        ev.flags = fl;
-                        ev.pad = 0;
-                        ev.p_new = pnum * fast_rcp(Zp);
-                        P.ev[s * P.ev_cap + ev_count] = ev;
+                // ---- the scalar tail (A5-A8): group-uniform, no transcendentals -----------
+                const double Z = sum;
+                const double qA = gs.spec[par][0], qB = gs.spec[par][1], q0 = gs.spec[par][2];
+                const double Zd = merge ? Z : Z - P.omH * qB;    // normaliser of the new posterior
+                const double Zp = merge ? Z : Z - qB;            // p_new = pnum / Zp
+                const double pnum = (merge && R == 2) ? Z : q0;  // MERGE R = 2: p_new = 1
+                uint32_t fl = (t > 0 && pnum > P.theta * Zp) ? 1u : 0u;
+                if ((kB % NT) == i) {
+                    qrow[kB] = P.hr * Z;  // R_t(0) = H Z / Zd
+                    if constexpr (ROT) {
+                        mu[0] = gs.mu0;  // the recycled cell is slot 0
+                        be[0] = gs.beta0;
+                        L[0] = gs.L0;
+                    } else {
+                        set_stats<J>(mu, be, L, kB / NT, gs.mu0, gs.beta0, gs.L0);
                     }
-                    ++ev_count;
                 }
-            }
-            if (i == 0) {
-                if (P.out_pnew) P.out_pnew[s * P.ld_o + tl] = pnum * fast_rcp(Zp);
-                if (P.out_logz) {  // kept mass (A4)
-                    const double lzd = fast_log2(Zd, kFmBase);
-                    P.out_logz[s * P.ld_o + tl] = fma(LN2, double(K0 + zexp) + (lzd - gs.lzd_prev), P.ln_omH);
-                    gs.lzd_prev = lzd;
-                }
-                gs.zd_prev = Zd;
-            }
-            zexp = ((__double2hiint(Zd) >> 20) & 0x7FF) - 1023;
-            tmod = (tmod + 1 == R) ? 0 : tmod + 1;
-            if constexpr (ROT) {
-                if (++iB == NT) {  // pB crosses a slot boundary: rotate slot j <- slot j+1
-                    iB = 0;
-                    phi = (phi + 1) & (J - 1);
-                    const double m0 = mu[0], b0 = be[0], l0r = L[0], qf = QREG ? qr[0] : qrow[i];
+                if (merge && (kA % NT) == i) qrow[kA] = qA + qB;  // bucket
+                // ---- MAP run length r* (A7): eager (key reduced at the barrier) or on demand --
+                int r_ex = -1;
+                double qex = 0.0;
+                if constexpr (EAGER) {
+                    if (key != 0ull) {
+                        r_ex = key_r(key);
+                        qex = key_val(key);
+                    }
+                } else if (fl & P.ev_mask) {  // group-uniform: an event at this step
+                    unsigned long long kb = 0ull;
 #pragma unroll
-                    for (int j = 0; j + 1 < J; ++j) {
-                        mu[j] = mu[j + 1];
-                        be[j] = be[j + 1];
-                        L[j] = L[j + 1];
-                        if constexpr (QREG) qr[j] = qr[j + 1]; else qrow[i + NT * j] = qrow[i + NT * (j + 1)];
+                    for (int j = 0; j < J; ++j) {
+                        const int p = i + NT * j;
+                        if (FULL || p < R) {
+                            int r;
+                            if (ROT || TAB2) {
+                                r = ib - NT * j;
+                                r -= (r >= R) ? R : 0;
+                            } else {
+                                r = tmod - p;
+                                r += (r < 0) ? R : 0;
+                            }
+                            const unsigned long long kq = argmax_key(qrow[p], r);  // own cells only
+                            kb = (r <= r_elig && kq > kb) ? kq : kb;
+                        }
                     }
-                    mu[J - 1] = m0;
-                    be[J - 1] = b0;
-                    L[J - 1] = l0r;
-                    if constexpr (QREG) qr[J - 1] = qf; else qrow[i + NT * (J - 1)] = qf;
+                    kb = warp_max_u64(kb);
+                    if constexpr (NT > 32) {
+                        if (lane == 0) gs.red3[w] = kb;
+                        group_sync<NT>(g);
+#pragma unroll
+                        for (int ww = 0; ww < NT / 32; ++ww) {
+                            const unsigned long long o = gs.red3[ww];
+                            kb = o > kb ? o : kb;
+                        }
+                        group_sync<NT>(g);  // red3 is reused at the next event step
+                    }
+                    if (kb != 0ull) {
+                        r_ex = key_r(kb);
+                        qex = key_val(kb);
+                    }
+                }
+                if (EAGER || (fl & P.ev_mask)) {
+                    int rstar;
+                    if (merge) {
+                        // bucket (qA + qB) vs the best growth slot (ties -> the smaller run length)
+                        rstar = (r_ex < 0 || (qA + qB) > qex) ? R - 1 : r_ex + 1;
+                    } else {
+                        rstar = r_ex + 1;
+                    }
+                    if (EAGER && t > 0 && rstar < min(map_prev + 1, R - 1)) fl |= 2u;
+                    map_prev = rstar;
+                    if (i == 0 && P.out_map) P.out_map[s * P.ld_o + tl] = rstar;
+                    if (fl & P.ev_mask) {
+                        if (i == 0 && ev_count < P.ev_cap) {
+                            EventRec ev;
+                            ev.t = t;
+                            ev.cp_index = t - rstar + 1;
+                            ev.flags = fl & P.ev_mask;  // the requested bits only (kernel-independent)
+                            ev.pad = 0;
+                            ev.p_new = pnum * fast_rcp(Zp);
+                            P.ev[s * P.ev_cap + ev_count] = ev;
+                        }
+                        ++ev_count;
+                    }
+                }
+                if (i == 0) {
+                    if (P.out_pnew) P.out_pnew[s * P.ld_o + tl] = pnum * fast_rcp(Zp);
+                    if (P.out_logz) {  // kept mass (A4)
+                        const double lzd = fast_log2(Zd, kFmBase);
+                        P.out_logz[s * P.ld_o + tl] =
+                            fma(LN2, double(K0 + zexp) + (lzd - gs.lzd_prev), P.ln_omH);
+                        gs.lzd_prev = lzd;
+                    }
+                    gs.zd_prev = Zd;
+                }
+                zexp = ((__double2hiint(Zd) >> 20) & 0x7FF) - 1023;
+                tmod = (tmod + 1 == R) ? 0 : tmod + 1;
+                if constexpr (ROT) {
+                    if (++iB == NT) {  // pB crosses a slot boundary: rotate slot j <- slot j+1
+                        iB = 0;
+                        phi = (phi + 1) & (J - 1);
+                        const double m0 = mu[0], b0 = be[0], l0r = L[0], qf = qrow[i];
+#pragma unroll
+                        for (int j = 0; j + 1 < J; ++j) {
+                            mu[j] = mu[j + 1];
+                            be[j] = be[j + 1];
+                            L[j] = L[j + 1];
+                            qrow[i + NT * j] = qrow[i + NT * (j + 1)];
+                        }
+                        mu[J - 1] = m0;
+                        be[J - 1] = b0;
+                        L[J - 1] = l0r;
+                        qrow[i + NT * (J - 1)] = qf;
+                    }
                 }
             }
         }
-    }
-    // ---- spill -------------------------------------------------------------
-    if (nonfinite) atomicOr(&gs.flags, 1);
-    group_sync<NT>(g);
+        // ---- spill -----------------------------------------------------------
+        if (nonfinite) atomicOr(&gs.flags, 1);
+        group_sync<NT>(g);
 #pragma unroll
-    for (int j = 0; j < J; ++j) {
-        const int p = ROT ? i + NT * ((j + phi) & (J - 1)) : i + NT * j;
-        const int e = ROT ? i + NT * j : p;
-        if (FULL || p < R) {
-            P.st_mu[sbase + p] = mu[j];
-            P.st_beta[sbase + p] = be[j];
-            P.st_q[sbase + p] = QREG ? qr[QREG ? j : 0] : qrow[e];
+        for (int j = 0; j < J; ++j) {
+            const int p = ROT ? i + NT * ((j + phi) & (J - 1)) : i + NT * j;
+            const int e = ROT ? i + NT * j : p;
+            if (FULL || p < R) {
+                P.st_mu[sbase + p] = mu[j];
+                P.st_beta[sbase + p] = be[j];
+                P.st_q[sbase + p] = qrow[e];
+            }
         }
-    }
-    if (i == 0) {
-        SeriesScalars sc;
-        sc.mu0 = gs.mu0;
-        sc.beta0 = gs.beta0;
-        sc.zd_prev = gs.zd_prev;
-        sc.map_prev = map_prev;
-        sc.ev_count = ev_count;
-        sc.flags = gs.flags;
-        sc.pad = 0;
-        sc.pad2 = 0.0;
-        P.scal[s] = sc;
-        if (sc.flags) atomicOr(P.err, unsigned(sc.flags));
+        if (i == 0) {
+            SeriesScalars sc;
+            sc.mu0 = gs.mu0;
+            sc.beta0 = gs.beta0;
+            sc.zd_prev = gs.zd_prev;
+            sc.map_prev = map_prev;
+            sc.ev_count = ev_count;
+            sc.flags = gs.flags;
+            sc.pad = 0;
+            sc.pad2 = 0.0;
+            P.scal[s] = sc;
+            if (sc.flags) atomicOr(P.err, unsigned(sc.flags));
+        }
+        group_sync<NT>(g);  // qrow / gs are reused by the next unit
     }
 }
 

@@ -10,14 +10,17 @@ namespace fbocd {
 template <int NT, int J, bool FULL, bool TAB2, int SPB, int MINB>
 static void make_variant(Variant* out) {
     Variant v;
-    v.fn = reinterpret_cast<const void*>(&bocd_update_kernel<NT, J, FULL, TAB2, false, SPB, MINB>);
-    v.fn_eager = reinterpret_cast<const void*>(&bocd_update_kernel<NT, J, FULL, TAB2, true, SPB, MINB>);
+    v.fn = reinterpret_cast<const void*>(&bocd_update_kernel<NT, J, FULL, TAB2, false, SPB, MINB, false>);
+    v.fn_eager = reinterpret_cast<const void*>(&bocd_update_kernel<NT, J, FULL, TAB2, true, SPB, MINB, false>);
+    v.fn_p = reinterpret_cast<const void*>(&bocd_update_kernel<NT, J, FULL, TAB2, false, SPB, MINB, true>);
+    v.fn_eager_p = reinterpret_cast<const void*>(&bocd_update_kernel<NT, J, FULL, TAB2, true, SPB, MINB, true>);
+    v.pref = kPrefOk<NT, J, FULL>;
     v.nt = NT;
     v.j = J;
     v.spb = SPB;
     v.full = FULL;
     v.tab2 = TAB2;
-    v.group_smem = sizeof(GroupSmem<NT>);  // + 2 R doubles of lp rows (group_bytes)
+    v.group_smem = sizeof(GroupSmem<NT>);  // + q row (+ PREF buffer): group_bytes
     *out = v;
 }
 
@@ -52,6 +55,13 @@ int select_variant(int R, Variant* out) {
     if (R <= 2048) { make_variant<256, 8, false, false, 1, 2>(out); return 0; }
     make_variant<512, 8, false, false, 1, 1>(out);
     return 0;
+}
+
+size_t variant_smem(const Variant& v, int R) {
+    const int rows = v.full ? R + v.nt : (v.tab2 ? 2 * R : R);  // table_entries
+    const size_t grp = v.group_smem + q_row_doubles(R) * sizeof(double) +
+                       (v.pref ? ((3 * size_t(R) * sizeof(double) + sizeof(SeriesScalars) + 15) & ~size_t(15)) : 0);
+    return kFmSmemBytes + table_bytes(rows) + size_t(v.spb) * grp;
 }
 
 // Test hook: elementwise fast_log2 / fast_exp2 over device arrays.

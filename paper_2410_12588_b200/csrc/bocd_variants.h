@@ -10,15 +10,20 @@ namespace fbocd {
 struct Variant {
     const void* fn = nullptr;        // __global__ void(KParams), MAP on demand
     const void* fn_eager = nullptr;  // MAP reduced every step
+    const void* fn_p = nullptr;        // persistent twins (streaming calls: few steps per call)
+    const void* fn_eager_p = nullptr;
     int nt = 0;                // threads per series group
     int j = 0;                 // cells per thread
     int spb = 0;               // series groups per CTA
     bool full = false;         // R == nt * j at compile time
     bool tab2 = false;         // doubled per-r tables
-    size_t group_smem = 0;     // bytes of per-group shared memory
+    size_t group_smem = 0;     // bytes of GroupSmem (the q row and the PREF buffer come on top)
+    bool pref = false;         // the persistent kernels prefetch the next unit's state (TMA)
 };
 
 int select_variant(int R, Variant* out);
+// dynamic shared memory of one CTA of variant v at ring size R
+size_t variant_smem(const Variant& v, int R);
 
 struct FastMathTables;
 int upload_fastmath_constants();  // once per device, before any kernel that uses fast_log2/exp2

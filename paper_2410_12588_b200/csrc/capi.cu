@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -27,6 +28,7 @@ struct falcon_bocd_s {
     falcon_bocd_config cfg{};
     fbocd::Variant var{};
     size_t smem = 0;
+    int64_t grid_cap = 0;  // co-resident CTAs (persistent grid)
     int64_t t = 0;  // observations absorbed
     double2* d_ca = nullptr;
     double* d_y = nullptr;
@@ -323,10 +325,7 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
         delete h;
         return fail(nullptr, FALCON_EINVAL, "no kernel variant for this R");
     }
-    // per-r table rows: FULL kernels index r and r + R < R + NT, generic TAB2 kernels r + R < 2R
-    const int tab_rows = h->var.full ? c.R + h->var.nt : (h->var.tab2 ? 2 * c.R : c.R);
-    h->smem = fbocd::kFmSmemBytes + fbocd::table_bytes(tab_rows) +
-              size_t(h->var.spb) * (h->var.group_smem + ((size_t(c.R) * sizeof(double) + 15) & ~size_t(15)));
+    h->smem = fbocd::variant_smem(h->var, c.R);
     auto bail = [&](int code) {
         g_create_err = h->err;
         falcon_bocd_destroy(h);
@@ -348,9 +347,16 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
         h->err = "cudaMemcpyToSymbol(c_fm) failed";
         return bail(FALCON_ECUDA);
     }
-    for (const void* fn : {h->var.fn, h->var.fn_eager}) {
+    for (const void* fn : {h->var.fn, h->var.fn_eager, h->var.fn_p, h->var.fn_eager_p}) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(h->smem));
         if (e != cudaSuccess) return bail(cuda_fail(h, e, "cudaFuncSetAttribute"));
+        int per_sm = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, h->var.nt * h->var.spb, h->smem);
+        if (e != cudaSuccess || per_sm < 1) return bail(cuda_fail(h, e != cudaSuccess ? e : cudaErrorInvalidConfiguration,
+                                                               "occupancy query"));
+        // persistent grid: as many CTAs as are co-resident (the kernel loops over series units)
+        const int64_t cap = int64_t(per_sm) * prop.multiProcessorCount;
+        h->grid_cap = h->grid_cap ? std::min(h->grid_cap, cap) : cap;
     }
 
     const int R = c.R;
@@ -416,6 +422,9 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
     return FALCON_OK;
 }
 
+// Calls of at most this many steps run the persistent kernels (bocd_kernel.cuh, PERSIST).
+constexpr int64_t kPersistMaxSteps = 64;
+
 static int launch_update(falcon_bocd_t h, const double* x_dev, int64_t ld, int64_t T,
                          int32_t* omap, double* opnew, double* ologz, int64_t ld_o, cudaStream_t st) {
     const falcon_bocd_config& c = h->cfg;
@@ -455,12 +464,17 @@ static int launch_update(falcon_bocd_t h, const double* x_dev, int64_t ld, int64
         P.out_logz = ologz ? ologz + done : nullptr;
         P.ld_o = ld_o;
         P.tma_ok = ((reinterpret_cast<uintptr_t>(P.x) & 15u) == 0) && ((ld & 1) == 0);
-        const int64_t grid = (c.n_series + h->var.spb - 1) / h->var.spb;
+        const int64_t units = (c.n_series + h->var.spb - 1) / h->var.spb;
+        // streaming calls (few steps): persistent grid, tables set up once per CTA and the next
+        // unit's state prefetched; long calls: one unit per CTA.  Identical arithmetic.
+        const bool persist = n <= kPersistMaxSteps && units > h->grid_cap;
+        const int64_t grid = persist ? h->grid_cap : units;
         void* args[] = {&P};
         // r* every step only when it is an output (per-step MAP, MAPRESET events); otherwise
         // the kernel reduces it on demand at the steps that report an event.
         const bool eager = (c.event_mask & FALCON_EV_MAPRESET) || omap;
-        cudaError_t e = cudaLaunchKernel(eager ? h->var.fn_eager : h->var.fn, dim3(unsigned(grid)),
+        const void* fn = persist ? (eager ? h->var.fn_eager_p : h->var.fn_p) : (eager ? h->var.fn_eager : h->var.fn);
+        cudaError_t e = cudaLaunchKernel(fn, dim3(unsigned(grid)),
                                          dim3(unsigned(h->var.nt * h->var.spb)), args, h->smem, st);
         if (e != cudaSuccess) return cuda_fail(h, e, "bocd_update_kernel launch");
         h->t += n;

@@ -56,7 +56,8 @@ def compare_steps(g_map, g_pnew, g_logz, res, theta, tol=TOL_LOG):
 def compare_events(gpu_events, res, theta, mask):
     """GPU events (structured array) vs oracle flags, outside exempt steps."""
     ex = exempt_steps(res.margin, res.p_new, theta)
-    want = {(s, t, c, f) for (s, t, c, f, _p) in res.events(mask) if not ex[s, t]}
+    # event records carry the requested flag bits only (include/falcon_bocd.h)
+    want = {(s, t, c, f & mask) for (s, t, c, f, _p) in res.events(mask) if not ex[s, t]}
     got = {(int(e["series"]), int(e["t"]), int(e["cp_index"]), int(e["flags"]))
            for e in gpu_events if not ex[int(e["series"]), int(e["t"])]}
     assert got == want, f"events differ: missing {sorted(want - got)[:5]}, extra {sorted(got - want)[:5]}"

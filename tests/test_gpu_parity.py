@@ -199,3 +199,34 @@ def test_event_overflow_warning():
     ev, dropped = b.changepoints()
     b.close()
     assert len(ev) == 3 and dropped  # DROP misfires MAPRESET (reading Q6): overflow reported
+
+
+def test_streaming_persistent_path_bit_exact(oracle_mod):
+    """Streaming calls (T <= 64 steps, more units than co-resident CTAs) run the persistent
+    kernels with TMA-prefetched state: same arithmetic as the one-unit-per-CTA kernels, so
+    one-column calls equal a single long call bit for bit, and sampled series match the oracle."""
+    cfg = tracegen.CONFIGS["C3"]
+    S, T = 1536, 96
+    spec = tracegen.make_spec(cfg, n_series=S)
+    x = tracegen.generate(spec, 0, S, 0, T)
+    a = _run_gpu(x, 1024, cfg.hazard, 0, prior_cov=0.3, ev_mask=1, cap=64)
+    b = _run_gpu(x, 1024, cfg.hazard, 0, prior_cov=0.3, ev_mask=1, cap=64, chunks=[1] * 40 + [56])
+    for k in ("map", "pnew", "logz", "logR", "mu", "beta"):
+        assert np.array_equal(a[k], b[k], equal_nan=True), k
+    assert np.array_equal(a["events"], b["events"])
+    sample = [0, 777, 1535]
+    res = _oracle(oracle_mod, x[sample], 1024, cfg.hazard, 0, prior_cov=0.3)
+    st = parity.compare_steps(b["map"][sample], b["pnew"][sample], b["logz"][sample], res, 0.9)
+    st["max_dlogR"] = parity.compare_logR(b["logR"][sample], res.logR_final)
+    parity.record("C3[0:1536,:96] R=1024 streaming (persistent) sampled", st)
+    # the on-demand-MAP (lazy) persistent kernel: no per-step outputs requested
+    xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    h = bocd.BocdBatch(S, R=1024, hazard=cfg.hazard, prior_first_obs=True, prior_cov=0.3,
+                       event_mask=1, event_capacity=64)
+    for t in range(T):
+        h.update_chunk(xd[:, t:t + 1])
+    logR = h.read_posterior()[0].cpu().numpy()
+    ev, _ = h.changepoints()
+    h.close()
+    assert np.array_equal(logR, a["logR"], equal_nan=True)
+    assert np.array_equal(ev, a["events"])
