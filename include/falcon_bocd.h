@@ -183,6 +183,65 @@ int falcon_bocd_predictive_constants(int32_t R, double kappa0, double alpha0, do
 int falcon_bocd_debug_fastmath(int32_t which, const double *in_dev, double *out_dev, int64_t n,
                                void *stream);
 
+/* ---------------------------------------------------------------------------
+ * Change-point verification and fail-slow pairing (§4.2
+ * "2) Change-point verification": a change point whose before/after mean
+ * iteration-time difference is less than 10% is a jitter).
+ * Readings V1-V5 (oracle/verify.py):
+ *   V1 boundary b = cp_index of the raw event; before = x[b-nb .. b-1], after =
+ *      x[b .. b+na-1], nb = min(window, b - t_lo), na = min(window, t_lo + T - b);
+ *   V2 nb == 0 or na == 0 -> FALCON_CP_INSUFFICIENT;
+ *   V3 |mean_after - mean_before| / mean_before < rel_threshold -> FALCON_CP_JITTER,
+ *      else FALCON_CP_DEGRADE (after > before) or FALCON_CP_RECOVER;
+ *   V4 pairing per series in time order: DEGRADE opens an event (onset b, baseline
+ *      mean_before, severity mean_after/mean_before), a further DEGRADE keeps it open
+ *      (severity = max(severity, mean_after/baseline)), RECOVER closes it (recovery b),
+ *      RECOVER while idle is ignored; an event still open at the end has recovery -1;
+ *   V5 means are fp64 sums in index order divided by the count (bit-identical to the
+ *      oracle).
+ * --------------------------------------------------------------------------- */
+enum { FALCON_CP_JITTER = 0, FALCON_CP_DEGRADE = 1, FALCON_CP_RECOVER = 2, FALCON_CP_INSUFFICIENT = 3 };
+
+typedef struct {
+    int64_t series;      /* global series id (as in falcon_bocd_event) */
+    int64_t t;           /* step the raw event was reported at */
+    int64_t cp_index;    /* boundary b */
+    int32_t status;      /* FALCON_CP_* */
+    int32_t n_before;    /* samples averaged on each side */
+    int32_t n_after;
+    int32_t reserved;
+    double mean_before;
+    double mean_after;
+} falcon_verified_cp;
+
+typedef struct {
+    int64_t series;      /* global series id */
+    int64_t onset;       /* boundary of the opening DEGRADE */
+    int64_t recovery;    /* boundary of the closing RECOVER, -1 while open */
+    double severity;     /* max mean_after / baseline over the event */
+} falcon_failslow_event;
+
+/* Verifies n_ev raw change points ev_dev (DEVICE, e.g. drained by
+ * falcon_bocd_changepoints into device memory; any order) against the observations
+ * x_dev (DEVICE, row-major [n_series][ld] fp64, row k = global series series_base + k,
+ * column j = global step t_lo + j, T columns valid).  Writes out_dev[k] (DEVICE) for
+ * each ev_dev[k].  window >= 1 (SPEC S:174 default 20), rel_threshold > 0 (0.10).
+ * An event whose series lies outside [series_base, series_base + n_series) is reported
+ * as FALCON_CP_INSUFFICIENT with n_before = n_after = 0.  Returns FALCON_EINVAL for bad
+ * arguments (nothing enqueued).  Stream-ordered, asynchronous. */
+int falcon_verify_changepoints(const double *x_dev, int64_t ld, int64_t n_series, int64_t series_base,
+                               int64_t t_lo, int64_t T, const falcon_bocd_event *ev_dev, int64_t n_ev,
+                               int32_t window, double rel_threshold, falcon_verified_cp *out_dev,
+                               void *stream);
+
+/* Pairs verified change points v_dev[n] (DEVICE, in (series, t) order as produced
+ * from a falcon_bocd_changepoints drain) into fail-slow events (V4): out_dev (DEVICE,
+ * capacity >= the number of DEGRADE records suffices) receives them in (series, onset)
+ * order and *n_out (HOST) their count.  Synchronises `stream`.  Returns FALCON_EINVAL
+ * if v_dev is not in (series, t) order or capacity is too small (*n_out = needed). */
+int falcon_pair_failslow(const falcon_verified_cp *v_dev, int64_t n, falcon_failslow_event *out_dev,
+                         int64_t capacity, int64_t *n_out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -87,6 +87,9 @@ def lib():
         "falcon_trace_generate": (ctypes.c_int, [ctypes.POINTER(TraceSpecC), _P, _i64, _i64, _i64,
                                                  _i64, _i64, _P]),
         "falcon_bocd_debug_fastmath": (ctypes.c_int, [_i32, _P, _P, _i64, _P]),
+        "falcon_verify_changepoints": (ctypes.c_int, [_P, _i64, _i64, _i64, _i64, _i64, _P, _i64, _i32,
+                                                      _f64, _P, _P]),
+        "falcon_pair_failslow": (ctypes.c_int, [_P, _i64, _P, _i64, ctypes.POINTER(_i64), _P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -100,7 +103,9 @@ EXPORTED = ["falcon_bocd_abi_version", "falcon_bocd_config_init", "falcon_bocd_c
             "falcon_bocd_update_chunk", "falcon_bocd_update_chunk_host", "falcon_bocd_changepoints",
             "falcon_bocd_pending_events", "falcon_bocd_read_posterior", "falcon_bocd_steps",
             "falcon_bocd_kernel_shape", "falcon_bocd_destroy", "falcon_bocd_last_error",
-            "falcon_bocd_predictive_constants", "falcon_trace_generate", "falcon_bocd_debug_fastmath"]
+            "falcon_bocd_predictive_constants", "falcon_trace_generate", "falcon_bocd_debug_fastmath",
+            "falcon_verify_changepoints", "falcon_pair_failslow"]
+CP_JITTER, CP_DEGRADE, CP_RECOVER, CP_INSUFFICIENT = 0, 1, 2, 3
 
 
 def check(code, handle=None):

@@ -20,6 +20,11 @@ def _ptr(t):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else None
 
 
+def _ld(x):
+    """Row stride of a 2-D row-major array (a single row may carry any stride)."""
+    return x.stride(0) if x.shape[0] > 1 else max(x.stride(0), x.shape[1])
+
+
 def _stream_ptr(stream):
     if stream is None:
         stream = torch.cuda.current_stream()
@@ -84,7 +89,7 @@ class BocdBatch:
                    torch.empty((self.n_series, T), dtype=torch.float64, device=x.device),
                    torch.empty((self.n_series, T), dtype=torch.float64, device=x.device))
             outs = N.StepOut(res[0].data_ptr(), res[1].data_ptr(), res[2].data_ptr(), T)
-        N.check(N.lib().falcon_bocd_update_chunk(self._h, _ptr(x), x.stride(0), T,
+        N.check(N.lib().falcon_bocd_update_chunk(self._h, _ptr(x), _ld(x), T,
                                                  ctypes.byref(outs) if outs else None,
                                                  _stream_ptr(stream)), self._h)
         return res
@@ -93,10 +98,10 @@ class BocdBatch:
         """Absorb HOST x[S][T] (pinned recommended); copies happen inside the library."""
         if isinstance(x, torch.Tensor):
             assert x.device.type == "cpu" and x.dtype == torch.float64 and x.stride(1) == 1
-            ptr, ld, T = x.data_ptr(), x.stride(0), x.shape[1]
+            ptr, ld, T = x.data_ptr(), _ld(x), x.shape[1]
         else:
             assert x.dtype == np.float64 and x.strides[1] == 8
-            ptr, ld, T = x.ctypes.data, x.strides[0] // 8, x.shape[1]
+            ptr, ld, T = x.ctypes.data, (x.strides[0] // 8 if x.shape[0] > 1 else x.shape[1]), x.shape[1]
         outs, res = None, None
         if outputs:
             res = (np.empty((self.n_series, T), np.int32), np.empty((self.n_series, T)),
@@ -164,6 +169,49 @@ class BocdBatch:
                 self._h = None
         except Exception:
             pass
+
+
+VERIFIED_DTYPE = np.dtype([("series", np.int64), ("t", np.int64), ("cp_index", np.int64), ("status", np.int32),
+                           ("n_before", np.int32), ("n_after", np.int32), ("reserved", np.int32),
+                           ("mean_before", np.float64), ("mean_after", np.float64)])
+FAILSLOW_DTYPE = np.dtype([("series", np.int64), ("onset", np.int64), ("recovery", np.int64),
+                           ("severity", np.float64)])
+
+
+def verify_changepoints(x, events, t_lo: int = 0, series_base: int = 0, window: int = 20,
+                        rel_threshold: float = 0.10, stream=None):
+    """Change-point verification (N1, falcon_verify_changepoints): x is a CUDA fp64 tensor
+    [n_series][T] (row k = global series series_base + k, column j = global step t_lo + j);
+    events a host EVENT_DTYPE array (e.g. from BocdBatch.changepoints()).  Returns a host
+    VERIFIED_DTYPE array, one record per event."""
+    assert x.is_cuda and x.dtype == torch.float64 and x.dim() == 2 and x.stride(1) == 1
+    ev = np.ascontiguousarray(events, dtype=EVENT_DTYPE)
+    n = len(ev)
+    if n == 0:
+        return np.empty(0, dtype=VERIFIED_DTYPE)
+    ev_d = torch.from_numpy(ev.view(np.uint8).reshape(n, EVENT_DTYPE.itemsize)).to(x.device)
+    out_d = torch.empty((n, VERIFIED_DTYPE.itemsize), dtype=torch.uint8, device=x.device)
+    N.check(N.lib().falcon_verify_changepoints(_ptr(x), _ld(x), x.shape[0], series_base, t_lo,
+                                               x.shape[1], _ptr(ev_d), n, window, rel_threshold,
+                                               _ptr(out_d), _stream_ptr(stream)))
+    return out_d.cpu().numpy().reshape(-1).view(VERIFIED_DTYPE).copy()
+
+
+def pair_failslow(verified, device=None, stream=None):
+    """Fail-slow pairing (N1, falcon_pair_failslow) of a VERIFIED_DTYPE array in (series, t)
+    order.  Returns a host FAILSLOW_DTYPE array in (series, onset) order."""
+    v = np.ascontiguousarray(verified, dtype=VERIFIED_DTYPE)
+    n = len(v)
+    if n == 0:
+        return np.empty(0, dtype=FAILSLOW_DTYPE)
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    v_d = torch.from_numpy(v.view(np.uint8).reshape(n, VERIFIED_DTYPE.itemsize)).to(dev)
+    cap = int((v["status"] == N.CP_DEGRADE).sum())
+    out_d = torch.empty((max(cap, 1), FAILSLOW_DTYPE.itemsize), dtype=torch.uint8, device=dev)
+    n_out = ctypes.c_int64()
+    N.check(N.lib().falcon_pair_failslow(_ptr(v_d), n, _ptr(out_d), cap, ctypes.byref(n_out),
+                                         _stream_ptr(stream)))
+    return out_d[: n_out.value].cpu().numpy().reshape(-1).view(FAILSLOW_DTYPE).copy()
 
 
 def predictive_constants(R: int, kappa0: float, alpha0: float):
