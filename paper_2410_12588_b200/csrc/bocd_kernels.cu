@@ -38,6 +38,7 @@ int select_variant(int R, Variant* out) {
         if (ev && strcmp(ev, "64x16s4") == 0) { make_variant<64, 16, true, true, 4, 1>(out); return 0; }
         if (ev && strcmp(ev, "128x8s2m1") == 0) { make_variant<128, 8, true, true, 2, 1>(out); return 0; }
         if (ev && strcmp(ev, "256x4s1m2") == 0) { make_variant<256, 4, true, true, 1, 2>(out); return 0; }
+        if (ev && strcmp(ev, "256x4s1m3") == 0) { make_variant<256, 4, true, true, 1, 3>(out); return 0; }
     }
     switch (R) {
         case 256: make_variant<32, 8, true, true, 8, 2>(out); return 0;
