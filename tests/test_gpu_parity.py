@@ -230,3 +230,17 @@ def test_streaming_persistent_path_bit_exact(oracle_mod):
     h.close()
     assert np.array_equal(logR, a["logR"], equal_nan=True)
     assert np.array_equal(ev, a["events"])
+
+
+def test_repeat_runs_bit_identical():
+    """Race detector of our own (compute-sanitizer is unavailable on this pool): the same
+    input twice through the resident and the persistent kernels gives identical bits."""
+    cfg = tracegen.CONFIGS["C3"]
+    S, T = 1536, 300
+    x = tracegen.generate(tracegen.make_spec(cfg, n_series=S), 0, S, 0, T)
+    for chunks in ([T], [1] * 20 + [280]):
+        runs = [_run_gpu(x, 1024, cfg.hazard, 0, prior_cov=0.3, ev_mask=3, cap=256, chunks=chunks)
+                for _ in range(2)]
+        for k in ("map", "pnew", "logz", "logR", "mu", "beta"):
+            assert np.array_equal(runs[0][k], runs[1][k], equal_nan=True), (chunks[:2], k)
+        assert np.array_equal(runs[0]["events"], runs[1]["events"])
