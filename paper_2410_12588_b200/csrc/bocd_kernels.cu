@@ -58,10 +58,11 @@ int select_variant(int R, Variant* out) {
     return 0;
 }
 
-size_t variant_smem(const Variant& v, int R) {
+size_t variant_smem(const Variant& v, int R, bool persistent) {
     const int rows = v.full ? R + v.nt : (v.tab2 ? 2 * R : R);  // table_entries
+    const bool pref = persistent && v.pref;  // only the persistent kernels carry the prefetch buffer
     const size_t grp = v.group_smem + q_row_doubles(R) * sizeof(double) +
-                       (v.pref ? ((3 * size_t(R) * sizeof(double) + sizeof(SeriesScalars) + 15) & ~size_t(15)) : 0);
+                       (pref ? ((3 * size_t(R) * sizeof(double) + sizeof(SeriesScalars) + 15) & ~size_t(15)) : 0);
     return kFmSmemBytes + table_bytes(rows) + size_t(v.spb) * grp;
 }
 

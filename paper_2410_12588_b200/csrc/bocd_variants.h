@@ -22,8 +22,8 @@ struct Variant {
 };
 
 int select_variant(int R, Variant* out);
-// dynamic shared memory of one CTA of variant v at ring size R
-size_t variant_smem(const Variant& v, int R);
+// dynamic shared memory of one CTA of variant v at ring size R (persistent or one-unit kernels)
+size_t variant_smem(const Variant& v, int R, bool persistent);
 
 struct FastMathTables;
 int upload_fastmath_constants();  // once per device, before any kernel that uses fast_log2/exp2

@@ -27,7 +27,8 @@ using fbocd::SeriesScalars;
 struct falcon_bocd_s {
     falcon_bocd_config cfg{};
     fbocd::Variant var{};
-    size_t smem = 0;
+    size_t smem = 0;    // dynamic shared memory of the one-unit-per-CTA kernels
+    size_t smem_p = 0;  // of the persistent kernels (+ the state prefetch buffers)
     int64_t grid_cap = 0;  // co-resident CTAs (persistent grid)
     int64_t t = 0;  // observations absorbed
     double2* d_ca = nullptr;
@@ -325,7 +326,8 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
         delete h;
         return fail(nullptr, FALCON_EINVAL, "no kernel variant for this R");
     }
-    h->smem = fbocd::variant_smem(h->var, c.R);
+    h->smem = fbocd::variant_smem(h->var, c.R, false);
+    h->smem_p = fbocd::variant_smem(h->var, c.R, true);
     auto bail = [&](int code) {
         g_create_err = h->err;
         falcon_bocd_destroy(h);
@@ -339,7 +341,7 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
         h->err = "device is not sm_100 class (this library is built for sm_100a only)";
         return bail(FALCON_ECUDA);
     }
-    if (h->smem > 227 * 1024) {
+    if (h->smem_p > 227 * 1024) {
         h->err = "shared memory footprint too large";
         return bail(FALCON_EINVAL);
     }
@@ -347,11 +349,15 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
         h->err = "cudaMemcpyToSymbol(c_fm) failed";
         return bail(FALCON_ECUDA);
     }
-    for (const void* fn : {h->var.fn, h->var.fn_eager, h->var.fn_p, h->var.fn_eager_p}) {
+    for (const void* fn : {h->var.fn, h->var.fn_eager}) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(h->smem));
         if (e != cudaSuccess) return bail(cuda_fail(h, e, "cudaFuncSetAttribute"));
+    }
+    for (const void* fn : {h->var.fn_p, h->var.fn_eager_p}) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(h->smem_p));
+        if (e != cudaSuccess) return bail(cuda_fail(h, e, "cudaFuncSetAttribute"));
         int per_sm = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, h->var.nt * h->var.spb, h->smem);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, h->var.nt * h->var.spb, h->smem_p);
         if (e != cudaSuccess || per_sm < 1) return bail(cuda_fail(h, e != cudaSuccess ? e : cudaErrorInvalidConfiguration,
                                                                "occupancy query"));
         // persistent grid: as many CTAs as are co-resident (the kernel loops over series units)
@@ -475,7 +481,8 @@ static int launch_update(falcon_bocd_t h, const double* x_dev, int64_t ld, int64
         const bool eager = (c.event_mask & FALCON_EV_MAPRESET) || omap;
         const void* fn = persist ? (eager ? h->var.fn_eager_p : h->var.fn_p) : (eager ? h->var.fn_eager : h->var.fn);
         cudaError_t e = cudaLaunchKernel(fn, dim3(unsigned(grid)),
-                                         dim3(unsigned(h->var.nt * h->var.spb)), args, h->smem, st);
+                                         dim3(unsigned(h->var.nt * h->var.spb)), args,
+                                         persist ? h->smem_p : h->smem, st);
         if (e != cudaSuccess) return cuda_fail(h, e, "bocd_update_kernel launch");
         h->t += n;
         done += n;
