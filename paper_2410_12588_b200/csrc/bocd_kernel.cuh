@@ -58,6 +58,10 @@ constexpr int kTile = 256;  // x steps per shared-memory tile (2 KB)
 #define FALCON_BOCD_KG 4
 #endif
 constexpr int kG = FALCON_BOCD_KG;  // cells per interleaved group (ILP)
+#ifndef FALCON_BOCD_STEP_UNROLL
+#define FALCON_BOCD_STEP_UNROLL 1
+#endif
+constexpr int kStepUnroll = FALCON_BOCD_STEP_UNROLL;  // steps per unrolled loop body
 
 struct SeriesScalars {  // per-series state carried between calls (HBM), 48 B
     double mu0, beta0;  // prior (set from x_0 when prior_first_obs)
@@ -338,6 +342,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     __syncthreads();
     const int ntiles = (P.T + kTile - 1) / kTile;
     const bool merge = (P.mode == 0);
+    const bool any_out = P.out_map || P.out_pnew || P.out_logz;  // per-step outputs requested
     // argmax-eligible run lengths: MERGE r <= R-3 (slot R-1 is the bucket), DROP r <= R-2
     const int r_elig = merge ? R - 3 : R - 2;
     unsigned xphase = 0u;  // parity of the two x-tile mbarriers (bit b: mbar[b])
@@ -466,6 +471,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 gs.kbuf[buf][q] = __double2int_rn(fmin(fmax(l0, -1048576.0), 1048576.0));
             }
             group_sync<NT>(g);
+#pragma unroll kStepUnroll
             for (int q = 0; q < n; ++q) {
                 const int tl = base + q;
                 const int64_t t = P.t0 + tl;
@@ -630,98 +636,99 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 const double Zp = merge ? Z : Z - qB;            // p_new = pnum / Zp
                 const double pnum = (merge && R == 2) ? Z : q0;  // MERGE R = 2: p_new = 1
                 uint32_t fl = (t > 0 && pnum > P.theta * Zp) ? 1u : 0u;
-                if ((kB % NT) == i) {
-                    qrow[kB] = P.hr * Z;  // R_t(0) = H Z / Zd
-                    if constexpr (ROT) {
-                        mu[0] = gs.mu0;  // the recycled cell is slot 0
-                        be[0] = gs.beta0;
-                        L[0] = gs.L0;
-                    } else {
-                        set_stats<J>(mu, be, L, kB / NT, gs.mu0, gs.beta0, gs.L0);
-                    }
+                // common path: branch-free (owner writes predicated) so that, with the step
+                // loop unrolled by two, the next step's cell work can overlap this tail
+                const bool own = (kB % NT) == i;
+                if (own) qrow[kB] = P.hr * Z;  // R_t(0) = H Z / Zd
+                if constexpr (ROT) {
+                    const double m0 = gs.mu0, b0 = gs.beta0, l0p = gs.L0;  // the recycled cell is slot 0
+                    mu[0] = own ? m0 : mu[0];
+                    be[0] = own ? b0 : be[0];
+                    L[0] = own ? l0p : L[0];
+                } else if (own) {
+                    set_stats<J>(mu, be, L, kB / NT, gs.mu0, gs.beta0, gs.L0);
                 }
                 if (merge && (kA % NT) == i) qrow[kA] = qA + qB;  // bucket
-                // ---- MAP run length r* (A7): eager (key reduced at the barrier) or on demand --
-                int r_ex = -1;
-                double qex = 0.0;
-                if constexpr (EAGER) {
-                    if (key != 0ull) {
-                        r_ex = key_r(key);
-                        qex = key_val(key);
-                    }
-                } else if (fl & P.ev_mask) {  // group-uniform: an event at this step
-                    unsigned long long kb = 0ull;
+                if (i == 0) gs.zd_prev = Zd;
+                const bool rot = ROT && (iB + 1 == NT);  // pB crosses a slot boundary
+                // ---- rare path (group-uniform): MAP run length r* (A7), events (A8), per-step
+                // outputs, the slot rotation ---------------------------------------------
+                if (EAGER || (fl & P.ev_mask) || any_out || rot) {
+                    int r_ex = -1;
+                    double qex = 0.0;
+                    if constexpr (EAGER) {
+                        if (key != 0ull) {
+                            r_ex = key_r(key);
+                            qex = key_val(key);
+                        }
+                    } else if (fl & P.ev_mask) {  // on demand: an event at this step
+                        unsigned long long kb = 0ull;
 #pragma unroll
-                    for (int j = 0; j < J; ++j) {
-                        const int p = i + NT * j;
-                        if (FULL || p < R) {
-                            int r;
-                            if (ROT || TAB2) {
-                                r = ib - NT * j;
-                                r -= (r >= R) ? R : 0;
-                            } else {
-                                r = tmod - p;
-                                r += (r < 0) ? R : 0;
+                        for (int j = 0; j < J; ++j) {
+                            const int p = i + NT * j;
+                            if (FULL || p < R) {
+                                int r;
+                                if (ROT || TAB2) {
+                                    r = ib - NT * j;
+                                    r -= (r >= R) ? R : 0;
+                                } else {
+                                    r = tmod - p;
+                                    r += (r < 0) ? R : 0;
+                                }
+                                const unsigned long long kq = argmax_key(qrow[p], r);  // own cells only
+                                kb = (r <= r_elig && kq > kb) ? kq : kb;
                             }
-                            const unsigned long long kq = argmax_key(qrow[p], r);  // own cells only
-                            kb = (r <= r_elig && kq > kb) ? kq : kb;
                         }
-                    }
-                    kb = warp_max_u64(kb);
-                    if constexpr (NT > 32) {
-                        if (lane == 0) gs.red3[w] = kb;
-                        group_sync<NT>(g);
+                        kb = warp_max_u64(kb);
+                        if constexpr (NT > 32) {
+                            if (lane == 0) gs.red3[w] = kb;
+                            group_sync<NT>(g);
 #pragma unroll
-                        for (int ww = 0; ww < NT / 32; ++ww) {
-                            const unsigned long long o = gs.red3[ww];
-                            kb = o > kb ? o : kb;
+                            for (int ww = 0; ww < NT / 32; ++ww) {
+                                const unsigned long long o = gs.red3[ww];
+                                kb = o > kb ? o : kb;
+                            }
+                            group_sync<NT>(g);  // red3 is reused at the next event step
                         }
-                        group_sync<NT>(g);  // red3 is reused at the next event step
-                    }
-                    if (kb != 0ull) {
-                        r_ex = key_r(kb);
-                        qex = key_val(kb);
-                    }
-                }
-                if (EAGER || (fl & P.ev_mask)) {
-                    int rstar;
-                    if (merge) {
-                        // bucket (qA + qB) vs the best growth slot (ties -> the smaller run length)
-                        rstar = (r_ex < 0 || (qA + qB) > qex) ? R - 1 : r_ex + 1;
-                    } else {
-                        rstar = r_ex + 1;
-                    }
-                    if (EAGER && t > 0 && rstar < min(map_prev + 1, R - 1)) fl |= 2u;
-                    map_prev = rstar;
-                    if (i == 0 && P.out_map) P.out_map[s * P.ld_o + tl] = rstar;
-                    if (fl & P.ev_mask) {
-                        if (i == 0 && ev_count < P.ev_cap) {
-                            EventRec ev;
-                            ev.t = t;
-                            ev.cp_index = t - rstar + 1;
-                            ev.flags = fl & P.ev_mask;  // the requested bits only (kernel-independent)
-                            ev.pad = 0;
-                            ev.p_new = pnum * fast_rcp(Zp);
-                            P.ev[s * P.ev_cap + ev_count] = ev;
+                        if (kb != 0ull) {
+                            r_ex = key_r(kb);
+                            qex = key_val(kb);
                         }
-                        ++ev_count;
                     }
-                }
-                if (i == 0) {
-                    if (P.out_pnew) P.out_pnew[s * P.ld_o + tl] = pnum * fast_rcp(Zp);
-                    if (P.out_logz) {  // kept mass (A4)
-                        const double lzd = fast_log2(Zd, kFmBase);
-                        P.out_logz[s * P.ld_o + tl] =
-                            fma(LN2, double(K0 + zexp) + (lzd - gs.lzd_prev), P.ln_omH);
-                        gs.lzd_prev = lzd;
+                    if (EAGER || (fl & P.ev_mask)) {
+                        int rstar;
+                        if (merge) {
+                            // bucket (qA + qB) vs the best growth slot (ties -> the smaller run length)
+                            rstar = (r_ex < 0 || (qA + qB) > qex) ? R - 1 : r_ex + 1;
+                        } else {
+                            rstar = r_ex + 1;
+                        }
+                        if (EAGER && t > 0 && rstar < min(map_prev + 1, R - 1)) fl |= 2u;
+                        map_prev = rstar;
+                        if (i == 0 && P.out_map) P.out_map[s * P.ld_o + tl] = rstar;
+                        if (fl & P.ev_mask) {
+                            if (i == 0 && ev_count < P.ev_cap) {
+                                EventRec ev;
+                                ev.t = t;
+                                ev.cp_index = t - rstar + 1;
+                                ev.flags = fl & P.ev_mask;  // the requested bits only (kernel-independent)
+                                ev.pad = 0;
+                                ev.p_new = pnum * fast_rcp(Zp);
+                                P.ev[s * P.ev_cap + ev_count] = ev;
+                            }
+                            ++ev_count;
+                        }
                     }
-                    gs.zd_prev = Zd;
-                }
-                zexp = ((__double2hiint(Zd) >> 20) & 0x7FF) - 1023;
-                tmod = (tmod + 1 == R) ? 0 : tmod + 1;
-                if constexpr (ROT) {
-                    if (++iB == NT) {  // pB crosses a slot boundary: rotate slot j <- slot j+1
-                        iB = 0;
+                    if (i == 0) {
+                        if (P.out_pnew) P.out_pnew[s * P.ld_o + tl] = pnum * fast_rcp(Zp);
+                        if (P.out_logz) {  // kept mass (A4)
+                            const double lzd = fast_log2(Zd, kFmBase);
+                            P.out_logz[s * P.ld_o + tl] =
+                                fma(LN2, double(K0 + zexp) + (lzd - gs.lzd_prev), P.ln_omH);
+                            gs.lzd_prev = lzd;
+                        }
+                    }
+                    if (rot) {  // rotate slot j <- slot j+1
                         phi = (phi + 1) & (J - 1);
                         const double m0 = mu[0], b0 = be[0], l0r = L[0], qf = qrow[i];
 #pragma unroll
@@ -737,6 +744,9 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                         qrow[i + NT * (J - 1)] = qf;
                     }
                 }
+                zexp = ((__double2hiint(Zd) >> 20) & 0x7FF) - 1023;
+                tmod = (tmod + 1 == R) ? 0 : tmod + 1;
+                if constexpr (ROT) iB = rot ? 0 : iB + 1;
             }
         }
         // ---- spill -----------------------------------------------------------
