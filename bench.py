@@ -117,6 +117,15 @@ class ClockSampler:
                 "samples": len(sm), "power_w_max": max(pw) if pw else None}
 
 
+def host_cores() -> int:
+    """Cores this process may run on (torchrun sets OMP_NUM_THREADS=1 per rank; the oracle
+    legs ask for every core explicitly)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
 def cpu_baseline_run(cfg, spec, n_series, T_s, s_offset=0):
     """The fp64 oracle as it stands, on this host's cores, over a bounded sample."""
     import oracle
@@ -124,7 +133,7 @@ def cpu_baseline_run(cfg, spec, n_series, T_s, s_offset=0):
     x = tracegen.generate(spec, s_offset, n_series, 0, T_s)
     t0 = time.perf_counter()
     oracle.run(x, cfg.R, cfg.hazard, cfg.kappa0, cfg.alpha0, prior_first_obs=True,
-               prior_cov=cfg.prior_cov, n_threads=0)
+               prior_cov=cfg.prior_cov, n_threads=host_cores())
     dt = time.perf_counter() - t0
     return n_series * T_s / dt, dt
 
@@ -134,11 +143,10 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    import oracle
     from paper_2410_12588_b200 import tracegen
     cfg = tracegen.CONFIGS[args.config]
     spec = tracegen.make_spec(cfg, n_series=cfg.n_series)
-    cores = oracle.max_threads()
+    cores = host_cores()
     n_s = max(1, min(cfg.n_series // max(1, args.steps + args.warmup), 4 * cores))
     T_s = min(cfg.T, args.ref_steps)
     times = []
@@ -301,8 +309,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        import oracle
-        cores = oracle.max_threads()
+        cores = host_cores()
         n_s = 32 * cores
         v, dt = cpu_baseline_run(cfg, spec, n_s, args.cpu_sample_steps)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
