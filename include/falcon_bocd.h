@@ -242,6 +242,22 @@ int falcon_verify_changepoints(const double *x_dev, int64_t ld, int64_t n_series
 int falcon_pair_failslow(const falcon_verified_cp *v_dev, int64_t n, falcon_failslow_event *out_dev,
                          int64_t capacity, int64_t *n_out, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * Suspicious-group classification (§4.3 "Profiling",
+ * "communication groups with data transfer time longer than 1.1x median
+ * value are classified as suspicious"; SPEC.md classify_groups S:202-210).
+ * Batched: n_batches independent profiling rounds of n_groups transfer times each.
+ * --------------------------------------------------------------------------- */
+
+/* times_dev: DEVICE fp64 [n_batches][ld] (ld >= n_groups), finite values; for each batch b:
+ *   median_dev[b] = the median of times[b][0..n_groups) (mean of the two middle values
+ *                   for an even count), DEVICE fp64 [n_batches] (may be NULL);
+ *   flags_dev[b * n_groups + k] = times[b][k] > factor * median  (strict; DEVICE uint8).
+ * One CTA per batch (shared-memory bitonic sort), 1 <= n_groups <= 8192, factor > 0
+ * (1.1).  Returns FALCON_EINVAL for bad arguments.  Stream-ordered, asynchronous. */
+int falcon_classify_groups(const double *times_dev, int64_t n_batches, int32_t n_groups, int64_t ld,
+                           double factor, uint8_t *flags_dev, double *median_dev, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

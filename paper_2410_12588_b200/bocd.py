@@ -214,6 +214,19 @@ def pair_failslow(verified, device=None, stream=None):
     return out_d[: n_out.value].cpu().numpy().reshape(-1).view(FAILSLOW_DTYPE).copy()
 
 
+def classify_groups(times, factor: float = 1.1, stream=None):
+    """Suspicious-group classification (N4, falcon_classify_groups): times is a CUDA fp64
+    tensor [n_batches][n_groups] of per-group transfer times.  Returns (suspicious: bool
+    tensor [n_batches][n_groups], median: fp64 tensor [n_batches]) on the device."""
+    assert times.is_cuda and times.dtype == torch.float64 and times.dim() == 2 and times.stride(1) == 1
+    B, G_ = times.shape
+    flags = torch.empty((B, G_), dtype=torch.uint8, device=times.device)
+    med = torch.empty(B, dtype=torch.float64, device=times.device)
+    N.check(N.lib().falcon_classify_groups(_ptr(times), B, G_, _ld(times), factor, _ptr(flags), _ptr(med),
+                                           _stream_ptr(stream)))
+    return flags.bool(), med
+
+
 def predictive_constants(R: int, kappa0: float, alpha0: float):
     """Host-only table (c_r, alpha_r, g_r, 1/(kappa_r+1)) used by the kernels."""
     out = [np.empty(R) for _ in range(4)]
