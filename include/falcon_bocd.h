@@ -258,6 +258,31 @@ int falcon_pair_failslow(const falcon_verified_cp *v_dev, int64_t n, falcon_fail
 int falcon_classify_groups(const double *times_dev, int64_t n_batches, int32_t n_groups, int64_t ld,
                            double factor, uint8_t *flags_dev, double *median_dev, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * ACF period detection and iteration times (§4.2 "Iteration time
+ * analysis"):  ACF(X)_k = sum_{t=1}^{L-k} (X_t - mu)(X_{t+k} - mu) /
+ * sum_{t=1}^{L} (X_t - mu)^2 with mu the mean of X, Period = argmin_k (ACF_k >= M),
+ * M = 0.95; the iteration time is the time between a call and its occurrence one period
+ * earlier (anchors = the first call of each period block).  Readings
+ * (DESIGN.md §3): the window is the whole sequence given; zero variance -> ACF 0, no period.
+ * --------------------------------------------------------------------------- */
+
+/* codes_dev: DEVICE int32 [n_series][ld] call-signature codes, L per series (2 <= L <= 8192,
+ * 1 <= k_max < L).  period_dev (DEVICE int32 [n_series]) receives the smallest k in
+ * [1, k_max] with ACF_k >= M, or 0; acf_dev (DEVICE fp64 [n_series][k_max], may be NULL)
+ * the ACF values.  One CTA per series; mu, the centred codes and the lag sums in fp64.
+ * Stream-ordered, asynchronous. */
+int falcon_detect_period(const int32_t *codes_dev, int64_t n_series, int32_t L, int64_t ld, int32_t k_max,
+                         double M, double *acf_dev, int32_t *period_dev, void *stream);
+
+/* ts_dev: DEVICE fp64 [n_series][ld] call timestamps (n per series); period_dev as above.
+ * out_dev (DEVICE fp64 [n_series][ld_out]) receives, per series, the iteration times
+ * ts[(i+1) P] - ts[i P] for i < (n - 1) / P, and n_out_dev (DEVICE int32 [n_series]) their
+ * count (0 where P = 0); ld_out >= n - 1.  Stream-ordered, asynchronous. */
+int falcon_iteration_times(const double *ts_dev, int64_t n_series, int32_t n, int64_t ld,
+                           const int32_t *period_dev, double *out_dev, int64_t ld_out, int32_t *n_out_dev,
+                           void *stream);
+
 #ifdef __cplusplus
 }
 #endif

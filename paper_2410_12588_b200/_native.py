@@ -91,6 +91,8 @@ def lib():
                                                       _f64, _P, _P]),
         "falcon_pair_failslow": (ctypes.c_int, [_P, _i64, _P, _i64, ctypes.POINTER(_i64), _P]),
         "falcon_classify_groups": (ctypes.c_int, [_P, _i64, _i32, _i64, _f64, _P, _P, _P]),
+        "falcon_detect_period": (ctypes.c_int, [_P, _i64, _i32, _i64, _i32, _f64, _P, _P, _P]),
+        "falcon_iteration_times": (ctypes.c_int, [_P, _i64, _i32, _i64, _P, _P, _i64, _P, _P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -105,7 +107,8 @@ EXPORTED = ["falcon_bocd_abi_version", "falcon_bocd_config_init", "falcon_bocd_c
             "falcon_bocd_pending_events", "falcon_bocd_read_posterior", "falcon_bocd_steps",
             "falcon_bocd_kernel_shape", "falcon_bocd_destroy", "falcon_bocd_last_error",
             "falcon_bocd_predictive_constants", "falcon_trace_generate", "falcon_bocd_debug_fastmath",
-            "falcon_verify_changepoints", "falcon_pair_failslow", "falcon_classify_groups"]
+            "falcon_verify_changepoints", "falcon_pair_failslow", "falcon_classify_groups",
+            "falcon_detect_period", "falcon_iteration_times"]
 CP_JITTER, CP_DEGRADE, CP_RECOVER, CP_INSUFFICIENT = 0, 1, 2, 3
 
 

@@ -227,6 +227,31 @@ def classify_groups(times, factor: float = 1.1, stream=None):
     return flags.bool(), med
 
 
+def detect_period(codes, k_max: int, M: float = 0.95, with_acf: bool = False, stream=None):
+    """ACF period detection (N2, falcon_detect_period): codes is a CUDA int32 tensor [S][L].
+    Returns period (int32 [S], 0 = none) and, with_acf, the ACF [S][k_max] (device tensors)."""
+    assert codes.is_cuda and codes.dtype == torch.int32 and codes.dim() == 2 and codes.stride(1) == 1
+    S, L = codes.shape
+    period = torch.empty(S, dtype=torch.int32, device=codes.device)
+    acf = torch.empty((S, k_max), dtype=torch.float64, device=codes.device) if with_acf else None
+    N.check(N.lib().falcon_detect_period(_ptr(codes), S, L, _ld(codes), k_max, M, _ptr(acf), _ptr(period),
+                                         _stream_ptr(stream)))
+    return (period, acf) if with_acf else period
+
+
+def iteration_times(ts, period, stream=None):
+    """Iteration times from call timestamps (N2, falcon_iteration_times): ts CUDA fp64 [S][n],
+    period int32 [S].  Returns (times fp64 [S][n-1], counts int32 [S]); row s is valid up to
+    counts[s]."""
+    assert ts.is_cuda and ts.dtype == torch.float64 and ts.dim() == 2 and ts.stride(1) == 1
+    S, n = ts.shape
+    out = torch.zeros((S, max(n - 1, 1)), dtype=torch.float64, device=ts.device)
+    cnt = torch.empty(S, dtype=torch.int32, device=ts.device)
+    N.check(N.lib().falcon_iteration_times(_ptr(ts), S, n, _ld(ts), _ptr(period.to(torch.int32).contiguous()),
+                                           _ptr(out), out.stride(0), _ptr(cnt), _stream_ptr(stream)))
+    return out, cnt
+
+
 def predictive_constants(R: int, kappa0: float, alpha0: float):
     """Host-only table (c_r, alpha_r, g_r, 1/(kappa_r+1)) used by the kernels."""
     out = [np.empty(R) for _ in range(4)]

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libfalcon_bocd.so")
-SOURCES = ["capi.cu", "bocd_kernels.cu", "tracegen.cu", "verify.cu", "groups.cu"]
+SOURCES = ["capi.cu", "bocd_kernels.cu", "tracegen.cu", "verify.cu", "groups.cu", "acf.cu"]
 HEADERS = ["bocd_kernel.cuh", "bocd_variants.h", "fastmath.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
