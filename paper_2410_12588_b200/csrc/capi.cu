@@ -222,6 +222,10 @@ int check_sticky(falcon_bocd_t h, cudaStream_t st) {
         h->poisoned = true;
         return fail(h, FALCON_ENONFINITE, "non-finite or non-positive prior (beta0 <= 0, or first observation 0)");
     }
+    if (e & 4u) {  // the kernel's entry check of its shared-memory layout (bocd_kernel.cuh, kFmBase)
+        h->poisoned = true;
+        return fail(h, FALCON_ECUDA, "internal: dynamic shared memory not at the expected address");
+    }
     return FALCON_OK;
 }
 
@@ -698,8 +702,8 @@ int falcon_bocd_destroy(falcon_bocd_t h) {
         if (cudaDeviceSynchronize() != cudaSuccess) rc = FALCON_ECUDA;
         if (rc == FALCON_OK && h->d_err) {
             unsigned e = 0;
-            if (cudaMemcpy(&e, h->d_err, sizeof(unsigned), cudaMemcpyDeviceToHost) == cudaSuccess && (e & 3u))
-                rc = FALCON_ENONFINITE;
+            if (cudaMemcpy(&e, h->d_err, sizeof(unsigned), cudaMemcpyDeviceToHost) == cudaSuccess && (e & 7u))
+                rc = (e & 3u) ? FALCON_ENONFINITE : FALCON_ECUDA;
         }
     }
     cudaGetLastError();
