@@ -34,14 +34,15 @@ METRIC = "BOCD series·timesteps/sec (R=1024, fp64) at 1/2/4/8 B200; % roofline"
 UNIT = "series*steps/s"
 # FP64-pipe work per cell (one run length, one step): DESIGN.md §6.
 #   The formulation's arithmetic per cell, counted as FP64-pipe instructions:
-#   NIG update 4 (d, mu', x - mu' folded with 1/2, beta'), lg beta' 9 (table-driven
-#   fast_log2), Student-t predictive 3, 2^(l - N) 9 (table-driven fast_exp2 with the
-#   row shift folded into its rounding constant), joint + evidence sum 2  =  27.
+#   NIG update 4 (d, mu', x - mu' folded with 1/2, beta'), lg beta' 8 (table-driven
+#   fast_log2: 256-entry table, degree-4 polynomial), Student-t predictive 3, 2^(l - N) 9
+#   (table-driven fast_exp2 with the row shift folded into its rounding constant),
+#   joint + evidence sum 2  =  26.
 #   Per-step work (group reduction, scalar tail, the tile's prior references) is not
-#   counted, so roofline.frac <= the measured FP64-pipe utilisation (ncu: 28.7 FP64
+#   counted, so roofline.frac <= the measured FP64-pipe utilisation (ncu: FP64
 #   instructions per cell executed, profiles/r01_ncu_top_kernel.txt).  For context the
 #   same cell with libdevice log/exp (30 + 18 FP64 instructions, cuobjdump, P0) is 60.
-FP64_INSTR_PER_CELL = 27
+FP64_INSTR_PER_CELL = 26
 FP64_INSTR_PER_CELL_LIBDEVICE = 60
 # FP64 pipe peak: 148 SMs x 64 FP64 lanes/clk x 1965 MHz (sm_max_mhz, MEASURED_PEAKS.json);
 # P0 measured 58.9 DFMA/clk/SM sustained at 1965 MHz (profiles/r01_p0_fp64_peaks.json).

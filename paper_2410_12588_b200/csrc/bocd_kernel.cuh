@@ -279,14 +279,14 @@ __host__ __device__ constexpr int table_entries(int R) {
 constexpr unsigned kDynBase = 0x400u;
 constexpr unsigned kFmBase = 0x800u;
 
-__device__ __forceinline__ double2 lds_log_entry(unsigned off) {  // off = (index << 4), index < 128
+__device__ __forceinline__ double2 lds_log_entry(unsigned off) {  // off = (index << 4), index < 256
     double2 v;
     asm("ld.shared.v2.f64 {%0, %1}, [%2+2048];" : "=d"(v.x), "=d"(v.y) : "r"(off));
     return v;
 }
 __device__ __forceinline__ double lds_exp_entry(unsigned off) {  // off = (index << 3), index < 64
     double v;
-    asm("ld.shared.f64 %0, [%1+4096];" : "=d"(v) : "r"(off));
+    asm("ld.shared.f64 %0, [%1+6144];" : "=d"(v) : "r"(off));  // exptab at kFmBase + 4096
     return v;
 }
 
@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
 #pragma unroll
                     for (int kk = 0; kk < G; ++kk) {
                         tb[kk] = unsigned(__double2hiint(bn[kk])) + 0x00196000u;
-                        lt[kk] = lds_log_entry((tb[kk] >> 9) & 0x7F0u);
+                        lt[kk] = lds_log_entry((tb[kk] >> 8) & 0xFF0u);
                     }
 #pragma unroll
                     for (int kk = 0; kk < G; ++kk) {
@@ -535,7 +535,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
 #pragma unroll
                     for (int kk = 0; kk < G; ++kk) pl[kk] = fma(rl[kk], kLog2C0, c_fm[1]);
 #pragma unroll
-                    for (int c = 2; c <= 5; ++c) {
+                    for (int c = 2; c <= 4; ++c) {
 #pragma unroll
                         for (int kk = 0; kk < G; ++kk) pl[kk] = fma(pl[kk], rl[kk], c_fm[c]);
                     }

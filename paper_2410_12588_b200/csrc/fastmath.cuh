@@ -9,12 +9,13 @@
 // own control-flow region; these spend 9 FP64 instructions each, no branches.
 //
 // log2: b = 2^k z, z in [0.70703125, 1.4140625) (integer split of the bit
-//       pattern); z lies in one of 128 sub-intervals i with precomputed
-//       invc_i ~ 1/c_i and l_i = -log2(invc_i) (long double on the host);
-//       r = z invc_i - 1 is one FMA (exact product, one rounding), |r| < 0.0040,
-//       log2 b = k + l_i + log2(1 + r),  log2(1 + r) = r P(r), P the degree-5
-//       Taylor polynomial of log1p(r)/(r ln 2) (truncation < 3e-18).
-//       9 FP64 + ~7 integer ops.  Valid for 2^-1000 < b < 2^1000 (the 2^-k
+//       pattern); z lies in one of 256 sub-intervals i (width 1/512 below 1, 1/256
+//       above) with precomputed invc_i ~ 1/c_i and l_i = -log2(invc_i) (long double
+//       on the host); r = z invc_i - 1 is one FMA (exact product, one rounding),
+//       |r| < 0.00196, log2 b = k + l_i + log2(1 + r),  log2(1 + r) = r P(r), P the
+//       degree-4 Chebyshev interpolant of log1p(r)/(r ln 2) on |r| <= 0.001954
+//       (max |error| of r P(r) 8.4e-19, 50-digit mpmath).
+//       8 FP64 + ~7 integer ops.  Valid for 2^-1000 < b < 2^1000 (the 2^-k
 //       scaling is folded into invc_i).
 // exp2: d clamped to >= -1021 on the integer pipe (2^-1021 is irrelevant next to
 //       the max term 1), d = (64 k + j)/64 + r exactly, |r| <= 1/128,
@@ -29,7 +30,7 @@
 
 namespace fbocd {
 
-constexpr int kLogTab = 128;
+constexpr int kLogTab = 256;
 constexpr int kExpTab = 64;
 constexpr double LN2 = 0.6931471805599453;
 constexpr double INV_LN2 = 1.4426950408889634;
@@ -39,17 +40,17 @@ struct FastMathTables {
     double exptab[kExpTab];   // 2^(j/64)
 };
 
-// z-interval of index i: i < 75 -> [c0 + i/256, +1/256), else [1 + (i-75)/128, +1/128)
+// z-interval of index i: i < 150 -> [c0 + i/512, +1/512), else [1 + (i-150)/256, +1/256)
 inline void fill_fastmath_tables(FastMathTables* t) {
     const long double c0 = 0.70703125L;
     for (int i = 0; i < kLogTab; ++i) {
         long double lo, w;
-        if (i < 75) {
-            lo = c0 + (long double)i / 256.0L;
-            w = 1.0L / 256.0L;
+        if (i < 150) {
+            lo = c0 + (long double)i / 512.0L;
+            w = 1.0L / 512.0L;
         } else {
-            lo = 1.0L + (long double)(i - 75) / 128.0L;
-            w = 1.0L / 128.0L;
+            lo = 1.0L + (long double)(i - 150) / 256.0L;
+            w = 1.0L / 256.0L;
         }
         const long double c = lo + 0.5L * w;
         const double invc = (double)(1.0L / c);
@@ -60,9 +61,10 @@ inline void fill_fastmath_tables(FastMathTables* t) {
 }
 
 // The tables live in DYNAMIC shared memory at a 2048-B aligned address fmb (logtab at
-// fmb, exptab at fmb + 2048), so a lookup address is (index bits) | fmb: one LOP3, no
-// add.  A kernel reserves kFmSmemBytes at the start of its dynamic shared memory
-// (alignment slack included) and calls fm_setup once (then a CTA barrier).
+// fmb, exptab at fmb + 4096); a lookup address is (index bits) + base (the BOCD kernel
+// uses the compile-time base as an LDS immediate).  A kernel reserves kFmSmemBytes at the
+// start of its dynamic shared memory (alignment slack included) and calls fm_setup once
+// (then a CTA barrier).
 constexpr unsigned kFmSmemBytes = 2048u + unsigned(sizeof(FastMathTables));
 
 // Polynomial / conversion constants in constant memory, uploaded at handle creation
@@ -74,11 +76,11 @@ static __constant__ double c_fm[16];
 // them as 32-bit immediates (no register or uniform-register operand): the rounding
 // (relative 7e-8) is weighted by r^6 < 5e-15 (log2) and r^5 < 3e-11 (exp2), i.e. below
 // 1e-20 absolute.
-constexpr double kLog2C0 = -0.2404491901397705;   // 0xbfcec70a00000000 ~ c_fm[0]
+constexpr double kLog2C0 = 0.2885398864746094;    // 0x3fd2777000000000 ~ c_fm[0]
 constexpr double kExp2C0 = 0.0013333559036254883;  // 0x3f55d88000000000 ~ c_fm[8]
 static const double kFastMathConstants[16] = {
-    -0.2404491734814939,   0.28853900817779266,  -0.36067376022224085, 0.4808983469629878,   // log2 P
-    -0.7213475204444817,   1.4426950408889634,   4503599627371520.0,   6755399441055744.0,   // .., 1/ln2, 2^52+1024, 1.5*2^52
+    0.2885399918194671,    -0.36067490780407263, 0.48089834696204886,  -0.7213475204433863,  // log2 P (r^4 .. r^1)
+    1.4426950408889634,    0.0,                  4503599627371520.0,   6755399441055744.0,   // r^0, -, 2^52+1024, 1.5*2^52
     0.0013333558146428443, 0.009618129107628477, 0.05550410866482158,  0.24022650695910072,  // exp2 poly
     0.6931471805599453,    64.0,                 -0.015625,            0.0};
 
@@ -110,8 +112,8 @@ __device__ __forceinline__ double lds_f64(unsigned a) {
 
 __device__ __forceinline__ double fast_log2(double x, unsigned fmb) {
     const unsigned tb = unsigned(__double2hiint(x)) + 0x00196000u;  // (hi - 0x3FE6A000) + (1024 << 20)
-    // entry (tb >> 13) & 127 (top 7 mantissa bits of ix - OFF), as a byte offset
-    const double2 t = lds_v2f64(((tb >> 9) & 0x7F0u) | fmb);
+    // entry (tb >> 12) & 255 (top 8 mantissa bits of ix - OFF), as a byte offset
+    const double2 t = lds_v2f64(((tb >> 8) & 0xFF0u) + fmb);
     // r = z * invc - 1 with z = x / 2^k: the exact power-of-two scaling is folded into invc
     const double invs =
         __hiloint2double(__double2hiint(t.x) + 0x40000000 - int(tb & 0xFFF00000u), __double2loint(t.x));
@@ -123,7 +125,6 @@ __device__ __forceinline__ double fast_log2(double x, unsigned fmb) {
     p = fma(p, r, c_fm[2]);
     p = fma(p, r, c_fm[3]);
     p = fma(p, r, c_fm[4]);
-    p = fma(p, r, c_fm[5]);
     return fma(r, p, kt);
 }
 
@@ -141,7 +142,7 @@ __device__ __forceinline__ double fast_exp2(double x, unsigned fmb) {
     p = fma(p, r, c_fm[11]);
     p = fma(p, r, c_fm[12]);
     const double q = p * r;
-    const double T = lds_f64(((ki << 3) & 0x1F8u) | (fmb + 2048u));
+    const double T = lds_f64(((ki << 3) & 0x1F8u) + (fmb + 4096u));
     int th;  // high word of T * 2^(ki >> 6): one IMAD
     asm("mad.lo.s32 %0, %1, 1048576, %2;" : "=r"(th) : "r"(int(ki) >> 6), "r"(__double2hiint(T)));
     const double Ts = __hiloint2double(th, __double2loint(T));
