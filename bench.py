@@ -33,16 +33,19 @@ if ROOT not in sys.path:
 METRIC = "BOCD series·timesteps/sec (R=1024, fp64) at 1/2/4/8 B200; % roofline"
 UNIT = "series*steps/s"
 # FP64-pipe work per cell (one run length, one step): DESIGN.md §6.
-#   The formulation's arithmetic per cell, counted as FP64-pipe instructions:
-#   NIG update 4 (d, mu', x - mu' folded with 1/2, beta'), lg beta' 8 (table-driven
-#   fast_log2: 256-entry table, degree-4 polynomial), Student-t predictive 3, 2^(l - N) 9
-#   (table-driven fast_exp2 with the row shift folded into its rounding constant),
-#   joint + evidence sum 2  =  26.
-#   Per-step work (group reduction, scalar tail, the tile's prior references) is not
-#   counted, so roofline.frac <= the measured FP64-pipe utilisation (ncu: FP64
-#   instructions per cell executed, profiles/r01_ncu_top_kernel.txt).  For context the
-#   same cell with libdevice log/exp (30 + 18 FP64 instructions, cuobjdump, P0) is 60.
+#   ALGORITHMIC work = the textbook recursion of PAPER App. A per cell, counted
+#   as FP64-pipe instructions with this library's table-driven transcendentals: NIG update 4
+#   (d, mu', x - mu' folded with 1/2, beta'), lg beta' 8 (fast_log2: 256-entry table,
+#   degree-4 polynomial), Student-t predictive 3, 2^(l - N) 9 (fast_exp2, the reference
+#   folded into its rounding constant), joint + evidence sum 2  =  26.  It is fixed across
+#   kernel formulations (comparable between rounds).  The current kernel evaluates the same
+#   recursion in the log-joint form (bocd_kernel.cuh: the predictive ratio telescopes into
+#   the NIG marginal likelihood) with 24 FP64 instructions per cell: "frac_executed" reports
+#   the fraction on that basis.  Per-step work (group reduction, scalar tail, the tile's prior
+#   references) is counted in neither.  For context the textbook cell with libdevice log/exp
+#   (30 + 18 FP64 instructions, cuobjdump, P0) is 60.
 FP64_INSTR_PER_CELL = 26
+FP64_INSTR_PER_CELL_EXECUTED = 24
 FP64_INSTR_PER_CELL_LIBDEVICE = 60
 # FP64 pipe peak: 148 SMs x 64 FP64 lanes/clk x 1965 MHz (sm_max_mhz, MEASURED_PEAKS.json);
 # P0 measured 58.9 DFMA/clk/SM sustained at 1965 MHz (profiles/r01_p0_fp64_peaks.json).
@@ -347,6 +350,8 @@ def main():
                          "kernel": "bocd_update_kernel<128,8,FULL,ROT>",
                          "kernel_ms_avg": k_avg, "kernel_share_of_step": k_share,
                          "work_per_cell": FP64_INSTR_PER_CELL,
+                         "frac_executed": FP64_INSTR_PER_CELL_EXECUTED * cells_per_launch
+                         / (k_avg * 1e-3) / peak,
                          "frac_vs_libdevice_work": FP64_INSTR_PER_CELL_LIBDEVICE * cells_per_launch
                          / (k_avg * 1e-3) / peak,
                          "peak_basis": f"{SMS} SMs x {FP64_PER_CLK_SM} FP64/clk x {sm_max:.0f} MHz (derived)"},

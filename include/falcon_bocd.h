@@ -106,9 +106,10 @@ typedef struct {
  * mu0 = 0, beta0 = 1, threshold 0.9, MERGE, EV_PROB, capacity 64, device 0). */
 int falcon_bocd_config_init(falcon_bocd_config *cfg);
 
-/* Allocates the handle: per-series state (3 x R fp64 per series: mu, beta,
- * unnormalised log posterior), the per-R predictive constant table and the
- * event buffers on cfg->device.  The state starts at the prior (no data).
+/* Allocates the handle: per-series state (3 x R fp64 per series: mu, beta and
+ * the log-joint offset of every run-length cell, plus one pending weight per
+ * thread of the kernel's series group), the per-R marginal-likelihood constant
+ * table and the event buffers on cfg->device.  The state starts at the prior (no data).
  * Returns FALCON_EINVAL on a bad config, FALCON_ENOMEM if device memory runs out. */
 int falcon_bocd_create(const falcon_bocd_config *cfg, falcon_bocd_t *out);
 

@@ -7,42 +7,52 @@
 // BEFORE x_t is absorbed, so growth r -> r+1 (App. A)
 // moves no data, and the position that truncation at R recycles (r = R-1) is
 // exactly the one that becomes the new change-point cell.  Per-r constants of
-// the Student-t predictive come from a shared-memory table indexed by r.
+// the NIG marginal likelihood come from a shared-memory table indexed by r.
 //
-// The recursion runs in the PROBABILITY domain: the row q is the run-length
-// posterior up to one per-series factor, R_t(r) = q_r (1-H) / Zd_t, so a step
-// needs ONE group reduction (the evidence Z) and a scalar tail without
-// transcendentals.  Predictive densities are evaluated in base-2 log units with
-// branch-free table-driven log2 / exp2 (fastmath.cuh), and every cell is
-// exponentiated against a per-step integer reference N_t = K0_t + z_{t-1}:
-//   K0_t = round(l0_t), l0_t the prior predictive of x_t (log2; the change-point
-//          cell's density, so Z >= H 2^(l0-K0-z) never underflows), computed for a
-//          whole x tile at once;
-//   z_{t-1} = the binary exponent of Zd_{t-1}, which renormalises the row by an
-//          exact power of two instead of a multiply per cell.
-// N_t enters the exp2 range reduction as an exact integer shift of its rounding
-// constant, so the per-cell cost of both is zero.  All fp64, no fast-math.
-// Per step:
+// LOG-JOINT representation.  A cell whose segment has absorbed n observations
+// holds (mu_n, beta_n) and one number a: its joint mass Pr(r_t = n, x_{0..t})
+// (up to the per-series normaliser) is
+//     q = 2^(a + G_n - alpha_n lg beta_n - Dc_t)                         (lg = log2)
+// where G_n + alpha0 lg beta0 - alpha_n lg beta_n is the log2 NIG marginal
+// likelihood of the segment (G_n = lg[Gamma(alpha_n)/Gamma(alpha0)] + 1/2 lg(kappa0/kappa_n)
+// - n/2 lg(2 pi) from a host table; kappa_n = kappa0 + n, alpha_n = alpha0 + n/2), a
+// fixes the segment's prior mass when it was created, and Dc_t is a per-series
+// integer frame.  The product of Student-t predictives of P:1345 telescopes into
+// this ratio of marginals, so a step needs, per cell, the NIG update, ONE log2
+// (lg beta') and ONE exp2; no per-cell multiply by the previous mass and no
+// posterior row in shared memory.
+//   Dc_t = Dc_{t-1} + N_t, N_t = K0_t + z_{t-1}: K0_t = round(l0_t), l0_t the prior
+//          predictive of x_t (the change-point cell's density, computed for a whole
+//          x tile at once), z_{t-1} = the binary exponent of Zd_{t-1}; so the cells of
+//          step t are exponentiated against the reference 2^(Dc_t) and Z stays O(1).
+//          Dc enters the exp2 range reduction as an exact integer shift of its
+//          rounding constant (zero per-cell cost).  At every global step that is a
+//          multiple of kRebase the frame is rebased (a -= Dc, Dc = 0): a fixed global
+//          schedule, so results do not depend on how the data is split into calls.
+// Per step and cell (r = the cell's run length before x_t; n = r + 1 after):
 //   A1  NIG update            mu' = mu + d y_r,  beta' = beta + d (x - mu')/2   (d = x - mu,
 //                             y_r = 1/(kappa_r+1): d (x - mu')/2 = kappa_r d^2 / (2(kappa_r+1)))
-//   A2  Student-t predictive  l_r = c_r/ln2 + alpha_r (lg beta - lg beta') - 1/2 lg beta'  (lg = log2;
-//                             = [c_r - 1/2 log beta - (alpha_r+1/2) log1p(kappa d^2/(2 beta (kappa+1)))]/ln2)
-//   A3  joint                 q'_r = q_r 2^(l_r - N_t)        (= R_{t-1}(r) pred_r x (step constant))
+//   A2  log2 marginal         l = (a + G_n) - alpha_n lg beta'   (the Student-t predictive of
+//                             P:1333/P:1345 is 2^(l - l_prev), implicit)
+//   A3  joint                 q' = 2^(l - Dc_t)  (fast exp2, Dc_t in the rounding constant)
 //   A4  evidence              Z = sum_r q'_r  (per-thread sums, xor butterfly, fixed-order
 //                             cross-warp sum: deterministic);
-//                             log Z_t = ln2 (K0_t + z_{t-1} + lg Zd_t - lg Zd_{t-1}) + ln(1-H)
-//   A5  normalisation         Zd = Z (MERGE) or Z - (1-H) q'_{R-1} (DROP); slot r+1 <- q'_r
-//   A6  change point / MERGE  new CP cell (recycled position): q = H Z/(1-H), prior statistics;
-//                             MERGE bucket: q = q'_{R-2} + q'_{R-1};  DROP: q'_{R-1} dropped
+//                             log Z_t = ln2 (N_t + lg Zd_t - lg Zd_{t-1}) + ln(1-H)
+//   A5  normalisation         Zd = Z (MERGE) or Z - (1-H) q'_{R-1} (DROP); R_t(r+1) = (1-H) q'_r / Zd
+//   A6  change point / MERGE  the recycled cell (r = R-1) becomes the new change-point cell:
+//                             prior statistics, a = lg(H Z/(1-H)) + alpha0 lg beta0 + Dc_t
+//                             (R_t(0) = H Z / Zd); MERGE: the cell reaching r = R-1 takes the
+//                             truncated cell's mass, a = lg(q'_{R-2} + q'_{R-1}) - (G - alpha lg beta')
+//                             + Dc_t;  DROP: q'_{R-1} is dropped
 //   A7  decision, MAP         p_new = R_t(1)/(1-R_t(0)) = q'_0/Z (MERGE) or q'_0/(Z - q'_{R-1}) (DROP);
 //                             r* = argmax over the growth slots (+ bucket), reduced every step when
 //                             the caller asks for per-step MAP / MAPRESET events, else on demand at
-//                             the steps that report an event
-// q lives in a per-series shared-memory row; mu, beta, lg beta live in registers
-// for the whole call; x is staged in double-buffered shared-memory tiles by 1-D
-// TMA bulk copies (cp.async.bulk + mbarrier); state is spilled to HBM once per call.
-// The cell loop is written stage-major over groups of kG cells (every stage of a
-// group before the next stage) so the dependent FP64 chains of kG cells interleave.
+//                             the steps that report an event (q' recomputed from the registers)
+// mu, beta, a live in registers for the whole call; x is staged in double-buffered
+// shared-memory tiles by 1-D TMA bulk copies (cp.async.bulk + mbarrier); state is
+// spilled to HBM once per call.  The cell loop is written stage-major over groups of
+// kG cells (every stage of a group before the next stage) so the dependent FP64
+// chains of kG cells interleave.
 #pragma once
 
 #include <climits>
@@ -53,7 +63,8 @@
 
 namespace fbocd {
 
-constexpr int kTile = 256;  // x steps per shared-memory tile (2 KB)
+constexpr int kTile = 256;     // x steps per shared-memory tile (2 KB)
+constexpr int kRebase = 256;   // generic kernels: global steps between frame rebases (ROT: every NT)
 #ifndef FALCON_BOCD_KG
 #define FALCON_BOCD_KG 4
 #endif
@@ -62,14 +73,16 @@ constexpr int kG = FALCON_BOCD_KG;  // cells per interleaved group (ILP)
 #define FALCON_BOCD_STEP_UNROLL 1
 #endif
 constexpr int kStepUnroll = FALCON_BOCD_STEP_UNROLL;  // steps per unrolled loop body
+// K0_t = round(l0_t) is clamped to +-kK0Max so that |N_t| < 2^16 and 64 Dc stays below 2^31
+constexpr double kK0Max = 32768.0;
 
 struct SeriesScalars {  // per-series state carried between calls (HBM), 48 B
     double mu0, beta0;  // prior (set from x_0 when prior_first_obs)
     double zd_prev;     // Zd_{t-1}: R_{t-1}(r) = q_r (1-H) / Zd_{t-1}  (1-H before the first step)
     int32_t map_prev;   // r*_{t-1}
     int32_t ev_count;   // events appended since the last drain (may exceed capacity)
-    int32_t flags;      // bit0: non-finite observation seen; bit1: bad prior
-    int32_t pad;
+    int32_t flags;      // bit0: non-finite observation seen; bit1: bad prior; bit2: smem layout
+    int32_t dc;         // Dc_{t-1}: integer frame of the cells' a values since the last rebase
     double pad2;
 };
 
@@ -90,12 +103,13 @@ struct KParams {
     int prior_first_obs;
     uint32_t ev_mask;
     int ev_cap;
-    const double2* tab_ca;     // [R] {c_r / ln2, alpha_r}
+    const double2* tab_ca;     // [R] row r: {G_{r+1}, alpha_{r+1}}
     const double* tab_y;       // [R] y_r = 1/(kappa_r+1)
     const FastMathTables* fm;  // log2 / exp2 tables
     double* st_mu;             // [S][R] position order
     double* st_beta;
-    double* st_q;
+    double* st_a;
+    double* st_w;              // [S][NT] pending slot-0 weights (FULL kernels)
     SeriesScalars* scal;  // [S]
     EventRec* ev;         // [S][ev_cap]
     unsigned* err;        // sticky device error bits
@@ -119,10 +133,16 @@ struct __align__(16) GroupSmem {
     double red2[2][NT / 32 > 0 ? NT / 32 : 1];
     unsigned long long red1[2][NT / 32 > 0 ? NT / 32 : 1];  // EAGER argmax keys
     unsigned long long red3[NT / 32 > 0 ? NT / 32 : 1];     // on-demand argmax (event steps)
-    double spec[2][4];                                       // q' of the cells r = R-2, R-1, 0
+    // generic kernels: q' of the cells r = R-2, R-1, 0 and G - alpha lg beta' of r = R-2;
+    // ROT kernels: e0 / l0 hold q' / lg beta' of every thread's slot 0, entry NT = slot 1 of
+    // thread 0, entry NT+1 (e0) = slot J-1 of thread NT-1 (the cells the tail needs)
+    double spec[2][4];
+    double e0[2][NT + 2];
+    double l0[2][NT + 1];
     double mu0, beta0, L0, zd_prev;  // zd_prev: kept current by thread 0 every step
     double lzd_prev;                 // lg Zd_{t-1} (log-evidence output, thread 0)
-    int map_prev, ev_count, flags, pad;
+    double aprior;                   // alpha0 lg beta0
+    int map_prev, ev_count, flags, dc0;  // dc0: Dc_{t-1} at the start of the call
     unsigned long long mbar[2];  // x tiles
     unsigned long long mbar_st;  // prefetched state of the next unit (PREF kernels)
 };
@@ -211,48 +231,51 @@ __device__ __forceinline__ bool tile_tma_ok(const KParams& P, int k) {
     return P.tma_ok && ((n & 1) == 0);
 }
 
-// Shared memory of one CTA: tables, then per group: GroupSmem + the q row [R].
+// Shared memory of one CTA: tables, then per group: GroupSmem (+ PREF buffer).
 // TAB2: the per-r tables are stored twice (entries r and r+R) so the ring index
 // (t - p) mod R becomes (t - p + R) with no masking and compile-time offsets per cell.
-__host__ __device__ constexpr size_t q_row_doubles(int R) { return (size_t(R) + 1) & ~size_t(1); }  // 16-B rows
-// per group: GroupSmem, the q row, and (PREF) the prefetch buffer [mu R][beta R][q R][scalars]
+// per group: GroupSmem and (PREF) the prefetch buffer [mu R][beta R][a R][scalars]
 template <int NT, bool PREF>
 __host__ __device__ constexpr size_t group_bytes(int R) {
-    return sizeof(GroupSmem<NT>) + q_row_doubles(R) * sizeof(double) +
+    return sizeof(GroupSmem<NT>) +
            (PREF ? ((3 * size_t(R) * sizeof(double) + sizeof(SeriesScalars) + 15) & ~size_t(15)) : 0);
 }
-// bytes of the per-r tables ({c_r/ln2, alpha_r} and y_r) for `entries` table rows
+// bytes of the per-r tables ({G_{r+1}, alpha_{r+1}} and y_r) for `entries` table rows
 __host__ __device__ constexpr size_t table_bytes(int entries) {
     return (size_t(entries) * (sizeof(double2) + sizeof(double)) + 15) & ~size_t(15);
 }
 
-// Resets one cell's NIG statistics to the prior (called by the owning thread only;
-// j is uniform within the thread, so this is a plain jump table).
+// Writes v into register slot j of a (a runtime slot index: a plain jump table).
 template <int J>
-__device__ __forceinline__ void set_stats(double (&mu)[J], double (&be)[J], double (&L)[J], int j, double m,
-                                          double b, double l) {
-#define FBOCD_SETS(k)          \
+__device__ __forceinline__ void set_slot(double (&a)[J], int j, double v) {
+#define FBOCD_SET1(k)          \
     case k:                    \
-        if constexpr (J > k) { \
-            mu[k] = m;         \
-            be[k] = b;         \
-            L[k] = l;          \
-        }                      \
+        if constexpr (J > k) a[k] = v; \
         break;
-    switch (j) { FBOCD_SETS(0) FBOCD_SETS(1) FBOCD_SETS(2) FBOCD_SETS(3) FBOCD_SETS(4) FBOCD_SETS(5) FBOCD_SETS(6) FBOCD_SETS(7)
-                 FBOCD_SETS(8) FBOCD_SETS(9) FBOCD_SETS(10) FBOCD_SETS(11) FBOCD_SETS(12) FBOCD_SETS(13) FBOCD_SETS(14) FBOCD_SETS(15) }
-#undef FBOCD_SETS
+    switch (j) { FBOCD_SET1(0) FBOCD_SET1(1) FBOCD_SET1(2) FBOCD_SET1(3) FBOCD_SET1(4) FBOCD_SET1(5) FBOCD_SET1(6) FBOCD_SET1(7)
+                 FBOCD_SET1(8) FBOCD_SET1(9) FBOCD_SET1(10) FBOCD_SET1(11) FBOCD_SET1(12) FBOCD_SET1(13) FBOCD_SET1(14) FBOCD_SET1(15) }
+#undef FBOCD_SET1
 }
 
-// Student-t predictive (A1 + A2) of the prior at x, log2 units: the tile's
-// exponent references K0_t = round(l0_t).
-__device__ __forceinline__ double prior_l2(double x, double mu0, double be0, double L0, double2 ca0, double y0,
+// log2 of v >= 0 for the per-step scalars (new change-point mass, MERGE bucket):
+// 0 -> -inf; arguments outside fast_log2's range (2^-1000, 2^1000) are scaled by 2^-+600.
+__device__ __forceinline__ double safe_log2(double v) {
+    const bool tiny = v < 0x1p-900;
+    const bool huge = v > 0x1p+900;
+    const double s = tiny ? v * 0x1p+600 : (huge ? v * 0x1p-600 : v);
+    const double l = fast_log2(s, 0x800u) + (tiny ? -600.0 : (huge ? 600.0 : 0.0));
+    return v > 0.0 ? l : -__longlong_as_double(0x7FF0000000000000ll);
+}
+
+// Prior predictive of x (A1 + A2 of the prior, log2 units): the tile's exponent
+// references K0_t = round(l0_t).  ca0 = {G_1, alpha_1}, ap = alpha0 lg beta0.
+__device__ __forceinline__ double prior_l2(double x, double mu0, double be0, double ap, double2 ca0, double y0,
                                            unsigned fmb) {
     const double d = x - mu0;
     const double mun = fma(d, y0, mu0);
     const double bn = fma(d, fma(mun, -0.5, 0.5 * x), be0);
     const double Ln = fast_log2(bn, fmb);
-    return fma(-0.5, Ln, fma(ca0.y, L0 - Ln, ca0.x));
+    return fma(-ca0.y, Ln, ca0.x + ap);
 }
 
 // ---------------------------------------------------------------------------
@@ -261,12 +284,12 @@ __device__ __forceinline__ double prior_l2(double x, double mu0, double be0, dou
 //          slot <-> position map by one slot every NT steps (slot j of thread i
 //          holds position i + NT*((j + phi) mod J), phi = pB / NT for the
 //          position pB the step recycles), so the recycled cell is always slot 0:
-//          its prior reset is a compile-time register write, and every table /
-//          row offset of a slot is a compile-time constant.
+//          its prior reset is a compile-time register write, and every table
+//          offset of a slot is a compile-time constant.
 //   TAB2 : doubled per-r tables (generic R <= 2048);
 //   EAGER: the MAP run length r* is reduced every step (per-step MAP output or
-//          MAPRESET events requested); otherwise it is reduced on demand, from the
-//          step's q row in shared memory, only at steps that report an event.
+//          MAPRESET events requested); otherwise it is reduced on demand, from
+//          q' recomputed out of the registers, only at steps that report an event.
 // ---------------------------------------------------------------------------
 template <int NT, int J, bool FULL, bool TAB2>
 __host__ __device__ constexpr int table_entries(int R) {
@@ -278,16 +301,63 @@ __host__ __device__ constexpr int table_entries(int R) {
 // the fast-math tables sit at the compile-time address kFmBase (checked at entry).
 constexpr unsigned kDynBase = 0x400u;
 constexpr unsigned kFmBase = 0x800u;
+// The exp2 table replicated 16 times, entry j of copy c at kExpRepBase + 128 j + 8 c: lane L
+// reads copy L mod 16, so the 32 lanes of a warp hit 32 distinct banks whatever their
+// indices (2 wavefronts per warp-wide 8-B lookup, no bank conflicts).  The per-r tables
+// start after it: kBocdFmBytes of the dynamic window hold the fast-math tables.
+constexpr unsigned kExpRepBase = 0x2000u;
+// The log2 table (16-B entries) replicated kLogRep times the same way (entry i of copy c at
+// kLogRepBase + 16 (kLogRep i + c), lane L reads copy L mod kLogRep): kLogRep = 8 makes the
+// 4 wavefronts of a warp-wide 16-B lookup conflict-free, but measured slower at R = 1024
+// (82.9 vs 82.0 ms per C3 call; 4 copies 84.5 ms): off by default (tuning knob).
+#ifndef FALCON_BOCD_LOGREP
+#define FALCON_BOCD_LOGREP 1
+#endif
+constexpr int kLogRep = FALCON_BOCD_LOGREP;
+constexpr int kLogRepShift = kLogRep == 8 ? 5 : kLogRep == 4 ? 6 : kLogRep == 2 ? 7 : 8;
+static_assert(kLogRep == 1 || kLogRep == 2 || kLogRep == 4 || kLogRep == 8, "kLogRep: 1, 2, 4 or 8");
+constexpr unsigned kLogRepBase = 0x4000u;
+constexpr unsigned kBocdFmBytes = (kLogRep > 1 ? kLogRepBase + 4096u * kLogRep : kExpRepBase + 8192u) - kDynBase;
+static_assert(kLogRepBase == 16384u && kFmBase + kFmSmemBytes - 2048u <= kExpRepBase, "fast-math tables overlap the replicated exp2 table");
 
-__device__ __forceinline__ double2 lds_log_entry(unsigned off) {  // off = (index << 4), index < 256
+// log2 table entry for tb = hi(x) + 0x00196000: index (tb >> 12) & 255; llb = 16 (lane mod kLogRep)
+__device__ __forceinline__ double2 lds_log_entry(unsigned tb, unsigned llb) {
     double2 v;
-    asm("ld.shared.v2.f64 {%0, %1}, [%2+2048];" : "=d"(v.x), "=d"(v.y) : "r"(off));
+    if constexpr (kLogRep > 1) {
+        asm("ld.shared.v2.f64 {%0, %1}, [%2+16384];"
+            : "=d"(v.x), "=d"(v.y)
+            : "r"(((tb >> kLogRepShift) & (0xFF0u * kLogRep)) | llb));  // kLogRepBase
+    } else {
+        asm("ld.shared.v2.f64 {%0, %1}, [%2+2048];" : "=d"(v.x), "=d"(v.y) : "r"((tb >> 8) & 0xFF0u));
+    }
     return v;
 }
-__device__ __forceinline__ double lds_exp_entry(unsigned off) {  // off = (index << 3), index < 64
+// replicated exp2 table: address = ((ki << 7) & 0x1F80) | lb, lb = kExpRepBase + 8 (lane & 15)
+__device__ __forceinline__ double lds_exp_entry(unsigned ki, unsigned lb) {
     double v;
-    asm("ld.shared.f64 %0, [%1+6144];" : "=d"(v) : "r"(off));  // exptab at kFmBase + 4096
+    asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(((ki << 7) & 0x1F80u) | lb));
     return v;
+}
+
+// exp2 of a cell: q' = 2^(ell - Dc) with C7 = 1.5 2^52 + 2^31 - 64 Dc (fast_exp2 of
+// fastmath.cuh with the frame folded into the rounding constant).  Exactly 0 below
+// 2^-1021 (also for ell = -inf), exponent clamped at +1000.  The cell
+// loop evaluates the same operations stage by stage; the on-demand MAP recomputation
+// calls this and must agree bit for bit.
+__device__ __forceinline__ double cell_exp2(double ell, double C7, unsigned lb) {
+    const double zf = fma(ell, 64.0, C7);
+    const unsigned ki = unsigned(__double2loint(zf));
+    const double re = fma(zf - C7, -0.015625, ell);
+    const double T = lds_exp_entry(ki, lb);
+    double p = fma(re, kExp2C0, c_fm[9]);
+    p = fma(p, re, c_fm[10]);
+    p = fma(p, re, c_fm[11]);
+    p = fma(p, re, c_fm[12]);
+    const double qq = p * re;
+    const bool dead = ki < 0x80000000u - 65344u;
+    const unsigned kc = min(ki, 0x80000000u + 64063u);
+    const double Ts = __hiloint2double(int(kc * 16384u) + __double2hiint(T), __double2loint(T));
+    return dead ? 0.0 : fma(Ts, qq, Ts);
 }
 
 // PREF is used for power-of-two R up to 1024, where the buffer (24 B x R per series) fits
@@ -297,7 +367,7 @@ constexpr bool kPrefOk = FULL && NT * J <= 1024;
 
 // Persistent kernel: each CTA loops over work units of SPB series (unit u = series
 // [u*SPB, u*SPB + SPB)), u = blockIdx.x, blockIdx.x + gridDim.x, ...  Tables are set up
-// once per CTA.  PREF: the state rows (mu, beta, q) and scalars of the group's NEXT unit
+// once per CTA.  PREF: the state rows (mu, beta, a) and scalars of the group's NEXT unit
 // are prefetched into shared memory by 1-D TMA bulk copies while the current unit computes
 // (streaming calls with a few steps per call are then bound by HBM, not by load latency).
 template <int NT, int J, bool FULL, bool TAB2, bool EAGER, int SPB, int MINB, bool PERSIST>
@@ -309,11 +379,11 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     constexpr bool ROT = FULL;
     const int R = FULL ? NT * J : P.R;
     const int RT = table_entries<NT, J, FULL, TAB2>(R);
-    // dynamic shared memory: [fast-math tables (aligned in kFmSmemBytes)][per-r tables][groups]
+    // dynamic shared memory: [fast-math tables + replicated exp2 table (kBocdFmBytes)][per-r tables][groups]
     unsigned char* const smem = smem_raw;
-    double2* s_ca = reinterpret_cast<double2*>(smem + kFmSmemBytes);
+    double2* s_ca = reinterpret_cast<double2*>(smem + kBocdFmBytes);
     double* s_y = reinterpret_cast<double*>(s_ca + RT);
-    unsigned char* gbase = smem + kFmSmemBytes + table_bytes(RT);
+    unsigned char* gbase = smem + kBocdFmBytes + table_bytes(RT);
 
     for (int k = threadIdx.x; k < RT; k += blockDim.x) {
         const int r = k < R ? k : k - R;
@@ -321,16 +391,23 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         s_y[k] = P.tab_y[r];
     }
     const bool fm_ok = smem_addr(smem_raw) == kDynBase && fm_setup(smem_raw, P.fm) == kFmBase;
+    {
+        double* rep = reinterpret_cast<double*>(smem_raw + (kExpRepBase - kDynBase));
+        for (int k = threadIdx.x; k < kExpTab * 16; k += blockDim.x) rep[k] = P.fm->exptab[k >> 4];
+    }
+    if constexpr (kLogRep > 1) {
+        double2* rep = reinterpret_cast<double2*>(smem_raw + (kLogRepBase - kDynBase));
+        for (int k = threadIdx.x; k < kLogTab * kLogRep; k += blockDim.x) rep[k] = P.fm->logtab[k / kLogRep];
+    }
+    const unsigned lb = kExpRepBase + 8u * (threadIdx.x & 15u);
+    const unsigned llb = 16u * (threadIdx.x & unsigned(kLogRep - 1));
     const int g = threadIdx.x / NT;
     const int i = threadIdx.x % NT;
     const int lane = threadIdx.x & 31;
     const int w = i >> 5;
     GroupSmem<NT>& gs = *reinterpret_cast<GroupSmem<NT>*>(gbase + size_t(g) * group_bytes<NT, PREF>(R));
-    // the series' unnormalised run-length posterior q: FULL in slot order (element
-    // i + NT*j = slot j of thread i), else in ring-position order
-    double* qrow = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(&gs) + sizeof(GroupSmem<NT>));
-    // PREF: the prefetched next-unit state [mu R][beta R][q R][SeriesScalars], position order
-    double* const pf = qrow + q_row_doubles(R);
+    // PREF: the prefetched next-unit state [mu R][beta R][a R][SeriesScalars], position order
+    double* const pf = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(&gs) + sizeof(GroupSmem<NT>));
     SeriesScalars* const pf_sc = reinterpret_cast<SeriesScalars*>(pf + 3 * size_t(R));
     const int64_t nunits = (P.S + SPB - 1) / SPB;
     if (i == 0) {
@@ -345,6 +422,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     const bool any_out = P.out_map || P.out_pnew || P.out_logz;  // per-step outputs requested
     // argmax-eligible run lengths: MERGE r <= R-3 (slot R-1 is the bucket), DROP r <= R-2
     const int r_elig = merge ? R - 3 : R - 2;
+    const double ninf = -__longlong_as_double(0x7FF0000000000000ll);
     unsigned xphase = 0u;  // parity of the two x-tile mbarriers (bit b: mbar[b])
     unsigned sphase = 0u;  // parity of the state mbarrier
     auto issue_state = [&](int64_t sn) {  // thread 0 of the group: next unit's state -> pf
@@ -354,7 +432,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         const size_t rb = size_t(R) * sizeof(double);
         tma_load_1d(pf, P.st_mu + sn * R, unsigned(rb), &gs.mbar_st);
         tma_load_1d(pf + R, P.st_beta + sn * R, unsigned(rb), &gs.mbar_st);
-        tma_load_1d(pf + 2 * size_t(R), P.st_q + sn * R, unsigned(rb), &gs.mbar_st);
+        tma_load_1d(pf + 2 * size_t(R), P.st_a + sn * R, unsigned(rb), &gs.mbar_st);
         tma_load_1d(pf_sc, P.scal + sn, unsigned(sizeof(SeriesScalars)), &gs.mbar_st);
     };
     if constexpr (PREF) {
@@ -370,7 +448,10 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         if (i == 0 && ntiles > 0 && tile_tma_ok(P, 0)) issue_tile_tma<NT>(gs, xrow, 0, P.T);
 
         // ---- load or initialise the state --------------------------------
-        double mu[J], be[J], L[J];
+        double mu[J], be[J], a[J];
+        // ROT: pending weight of slot 0 (the mass of a new change-point / bucket cell, kept as a
+        // factor of its q' until the next rotation step folds it into a)
+        double wq = 1.0;
         const int64_t sbase = s * int64_t(R);
         if constexpr (PREF) {
             if (P.t0 > 0) {
@@ -388,21 +469,25 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 }
                 sc.zd_prev = P.omH;  // R_{-1} = [1, 0, ...] = q (1-H)/Zd
                 sc.map_prev = 0;
+                sc.dc = 0;
             }
             const bool ok = sc.beta0 >= 2.2250738585072014e-308 && sc.beta0 < 1e300 && isfinite(sc.mu0);
             gs.mu0 = sc.mu0;
             gs.beta0 = ok ? sc.beta0 : 1.0;
             gs.L0 = fast_log2(gs.beta0, kFmBase);
+            gs.aprior = P.alpha0 * gs.L0;
             gs.zd_prev = sc.zd_prev;
             gs.map_prev = sc.map_prev;
             gs.ev_count = sc.ev_count;
             gs.flags = sc.flags | (ok ? 0 : 2) | (fm_ok ? 0 : 4);
+            gs.dc0 = sc.dc;
         }
         group_sync<NT>(g);
         // the prior and the rarely used per-series scalars stay in shared memory (gs) so
         // that the step loop keeps its registers for the cells
         int zexp = ((__double2hiint(gs.zd_prev) >> 20) & 0x7FF) - 1023;  // binary exponent of Zd_{t-1}
         int map_prev = gs.map_prev, ev_count = gs.ev_count;
+        int dc = gs.dc0;  // Dc_{t-1}
         // ring bookkeeping.  FULL: the recycled position pB = (t+1) mod R = NT*phi + iB;
         // generic: tmod = t mod R.
         int tmod = int(P.t0 % R);
@@ -415,30 +500,30 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
 #pragma unroll
         for (int j = 0; j < J; ++j) {
             const int p = ROT ? i + NT * ((j + phi) & (J - 1)) : i + NT * j;  // position of slot j
-            const int e = ROT ? i + NT * j : p;                                // its q element
             if (FULL || p < R) {
                 if (P.t0 == 0) {
                     mu[j] = gs.mu0;
                     be[j] = gs.beta0;
-                    L[j] = gs.L0;
-                    qrow[e] = (p == 0) ? 1.0 : 0.0;  // before x_0 a segment starts w.p. 1 (Q8)
+                    a[j] = (p == 0) ? gs.aprior : ninf;  // before x_0 a segment starts w.p. 1 (Q8)
                 } else {
                     if constexpr (PREF) {
                         mu[j] = pf[p];
                         be[j] = pf[R + p];
-                        qrow[e] = pf[2 * R + p];
+                        a[j] = pf[2 * R + p];
                     } else {
                         mu[j] = P.st_mu[sbase + p];
                         be[j] = P.st_beta[sbase + p];
-                        qrow[e] = P.st_q[sbase + p];
+                        a[j] = P.st_a[sbase + p];
                     }
-                    L[j] = fast_log2(be[j], kFmBase);
                 }
             } else {
                 mu[j] = gs.mu0;
                 be[j] = gs.beta0;
-                L[j] = gs.L0;
+                a[j] = ninf;
             }
+        }
+        if constexpr (ROT) {
+            if (P.t0 > 0) wq = P.st_w[s * NT + i];
         }
         if constexpr (PREF) {
             // pf is free once every thread of the group has read it: prefetch the next unit
@@ -467,24 +552,48 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             for (int q = i; q < n; q += NT) {
                 const double xq = gs.xbuf[buf][q];
                 if (!isfinite(xq)) nonfinite = true;
-                const double l0 = prior_l2(xq, gs.mu0, gs.beta0, gs.L0, s_ca[0], s_y[0], kFmBase);
-                gs.kbuf[buf][q] = __double2int_rn(fmin(fmax(l0, -1048576.0), 1048576.0));
+                const double l0 = prior_l2(xq, gs.mu0, gs.beta0, gs.aprior, s_ca[0], s_y[0], kFmBase);
+                gs.kbuf[buf][q] = __double2int_rn(fmin(fmax(l0, -kK0Max), kK0Max));
             }
             group_sync<NT>(g);
+            // ROT: the tile's steps run in segments that end at a rotation step (iB = NT-1); the
+            // slot rotation, the fold of the pending weights and the frame rebase run between
+            // segments (register permutations outside the step loop: no copies inside it)
+            for (int q = 0; q < n;) {
+            const int qe = ROT ? min(n, q + (NT - iB)) : n;
 #pragma unroll kStepUnroll
-            for (int q = 0; q < n; ++q) {
+            for (; q < qe; ++q) {
                 const int tl = base + q;
                 const int64_t t = P.t0 + tl;
                 const double x = gs.xbuf[buf][q];
                 const double hx = 0.5 * x;
                 const int K0 = gs.kbuf[buf][q];
-                // exp2 rounding constant 1.5*2^52 + 2^31 - 64 N_t: zf = fma(l, 64, C7) holds
-                // round(64 l) - 64 N_t + 2^31 in its low word (exact integers below 2^52)
-                const double C7 = __hiloint2double(0x43380000, int(0x80000000u - unsigned(K0 + zexp) * 64u));
+                if (!ROT && (unsigned(t) & (kRebase - 1)) == 0u) {  // generic: rebase at t % kRebase == 0
+                    const double dcd = double(dc);
+#pragma unroll
+                    for (int j = 0; j < J; ++j) a[j] -= dcd;
+                    dc = 0;
+                }
+                dc += K0 + zexp;  // Dc_t = Dc_{t-1} + N_t
+                // exp2 rounding constant 1.5*2^52 + 2^31 - 64 Dc_t: zf = fma(l, 64, C7) holds
+                // round(64 l) - 64 Dc_t + 2^31 in its low word (exact integers below 2^52)
+                const double C7 = __hiloint2double(0x43380000, int(0x80000000u - unsigned(dc) * 64u));
                 // ---- A1-A4 for the J cells (groups of G, every stage across the group) ----
                 // table index of slot j: ib - NT*j  (= r or r + R).  FULL: r of slot j is
                 // (pB - 1 - p) mod R = (iB - 1 - i - NT j) mod R.
                 const int ib = ROT ? iB - 1 - i + R : tmod - i + R;
+                // the cells the tail needs (r = R-2 -> qA, R-1 -> qB, 0 -> q0) and their owners
+                int kA, kB, k0;
+                if constexpr (ROT) {
+                    kB = iB;                          // slot 0 of thread iB
+                    kA = iB + 1;                      // slot 0 of thread iB+1, or slot 1 of thread 0
+                    k0 = (iB == 0) ? R - 1 : iB - 1;  // slot 0 of thread iB-1, or slot J-1 of thread NT-1
+                } else {
+                    kB = (tmod + 1 == R) ? 0 : tmod + 1;
+                    kA = (kB + 1 == R) ? 0 : kB + 1;
+                    k0 = tmod;
+                }
+                const int par = tl & 1;
                 double sum = 0.0;
                 unsigned long long key = 0ull;
 #pragma unroll
@@ -492,9 +601,9 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     constexpr int G = (J < kG) ? J : kG;
                     int idx[G];
                     double2 ca[G];
-                    double yv[G], qv[G], d[G], bn[G];
+                    double yv[G], d[G], bn[G];
 #pragma unroll
-                    for (int kk = 0; kk < G; ++kk) {  // table + row loads
+                    for (int kk = 0; kk < G; ++kk) {  // table loads
                         const int j = j0 + kk;
                         const int p = i + NT * j;
                         if (ROT || TAB2) {
@@ -506,7 +615,6 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                         if (!FULL && p >= R) idx[kk] = 0;  // masked cell: any valid entry
                         ca[kk] = s_ca[idx[kk]];
                         yv[kk] = s_y[idx[kk]];
-                        qv[kk] = (FULL || p < R) ? qrow[p] : 0.0;
                     }
                     // A1: NIG update
 #pragma unroll
@@ -514,7 +622,10 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
 #pragma unroll
                     for (int kk = 0; kk < G; ++kk) mu[j0 + kk] = fma(d[kk], yv[kk], mu[j0 + kk]);
 #pragma unroll
-                    for (int kk = 0; kk < G; ++kk) bn[kk] = fma(d[kk], fma(mu[j0 + kk], -0.5, hx), be[j0 + kk]);
+                    for (int kk = 0; kk < G; ++kk) {
+                        bn[kk] = fma(d[kk], fma(mu[j0 + kk], -0.5, hx), be[j0 + kk]);
+                        be[j0 + kk] = bn[kk];
+                    }
                     // A2: lg beta' (fast_log2 of fastmath.cuh, stage by stage)
                     unsigned tb[G];
                     double2 lt[G];
@@ -522,7 +633,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
 #pragma unroll
                     for (int kk = 0; kk < G; ++kk) {
                         tb[kk] = unsigned(__double2hiint(bn[kk])) + 0x00196000u;
-                        lt[kk] = lds_log_entry((tb[kk] >> 8) & 0xFF0u);
+                        lt[kk] = lds_log_entry(tb[kk], llb);
                     }
 #pragma unroll
                     for (int kk = 0; kk < G; ++kk) {
@@ -544,11 +655,15 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     for (int kk = 0; kk < G; ++kk) {
                         const int j = j0 + kk;
                         const double Ln = fma(rl[kk], pl[kk], kt[kk]);
-                        ell[kk] = fma(-0.5, Ln, fma(ca[kk].y, L[j] - Ln, ca[kk].x));
-                        L[j] = Ln;
-                        be[j] = bn[kk];
+                        ell[kk] = fma(-ca[kk].y, Ln, a[j] + ca[kk].x);
+                        if constexpr (ROT) {  // lg beta' of slot 0 (and slot 1 of thread 0) for the bucket
+                            if (j == 0) gs.l0[par][i] = Ln;
+                            if (J > 1 && j == 1 && i == 0) gs.l0[par][NT] = Ln;
+                        } else {
+                            if (merge && i + NT * j == kA) gs.spec[par][3] = fma(-ca[kk].y, Ln, ca[kk].x);
+                        }
                     }
-                    // A3: q' = q 2^(l - N_t)  (fast_exp2 with the shifted rounding constant)
+                    // A3: q' = 2^(l - Dc_t)  (cell_exp2, stage by stage)
                     double re[G], pe[G], Tv[G];
                     unsigned ki[G];
 #pragma unroll
@@ -556,7 +671,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                         const double zf = fma(ell[kk], 64.0, C7);
                         ki[kk] = unsigned(__double2loint(zf));
                         re[kk] = fma(zf - C7, -0.015625, ell[kk]);  // exact, |re| <= 1/128
-                        Tv[kk] = lds_exp_entry((ki[kk] << 3) & 0x1F8u);
+                        Tv[kk] = lds_exp_entry(ki[kk], lb);
                     }
 #pragma unroll
                     for (int kk = 0; kk < G; ++kk) pe[kk] = fma(re[kk], kExp2C0, c_fm[9]);
@@ -571,41 +686,34 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                         const int p = i + NT * j;
                         const double qq = pe[kk] * re[kk];
                         // 2^e, e = floor(n/64) for n = ki - 2^31: exactly 0 below 2^-1021, e clamped
-                        // at +1000; the 2^31 offset vanishes mod 2^32 in the exponent field
+                        // at +1000; hi word = kc * 2^14 + hi(T'_j) (fastmath.cuh)
                         const bool dead = ki[kk] < 0x80000000u - 65344u;
                         const unsigned kc = min(ki[kk], 0x80000000u + 64063u);
-                        const double Ts = __hiloint2double(int((kc >> 6) << 20) + __double2hiint(Tv[kk]),
+                        const double Ts = __hiloint2double(int(kc * 16384u) + __double2hiint(Tv[kk]),
                                                            __double2loint(Tv[kk]));
-                        const double E = dead ? 0.0 : fma(Ts, qq, Ts);
+                        double E = dead ? 0.0 : fma(Ts, qq, Ts);
+                        if (ROT && j == 0) E *= wq;  // slot 0's pending weight (new CP / bucket mass)
                         if (FULL || p < R) {
-                            const double qn = qv[kk] * E;
-                            qrow[p] = qn;
-                            sum += qn;
+                            sum += E;
                             if constexpr (EAGER) {
                                 int r = idx[kk];
                                 r -= (r >= R) ? R : 0;
-                                const unsigned long long kq = argmax_key(qn, r);
+                                const unsigned long long kq = argmax_key(E, r);
                                 key = (r <= r_elig && kq > key) ? kq : key;
+                            }
+                            // the tail's cells, published by their owners
+                            if constexpr (ROT) {
+                                if (j == 0) gs.e0[par][i] = E;
+                                if (J > 1 && j == 1 && i == 0) gs.e0[par][NT] = E;
+                                if (j == J - 1 && i == NT - 1) gs.e0[par][NT + 1] = E;
+                            } else {
+                                if (p == kA) gs.spec[par][0] = E;
+                                if (p == kB) gs.spec[par][1] = E;
+                                if (p == k0) gs.spec[par][2] = E;
                             }
                         }
                     }
                 }
-                // the three cells the tail needs (r = R-2, R-1, 0) are published by their owners
-                // (kB / kA are overwritten right after the barrier); kX = their q elements
-                const int par = tl & 1;
-                int kA, kB, k0;
-                if constexpr (ROT) {
-                    kB = iB;                          // slot 0 of thread iB
-                    kA = iB + 1;                      // slot 0 of thread iB+1, or slot 1 of thread 0
-                    k0 = (iB == 0) ? R - 1 : iB - 1;  // slot 0 of thread iB-1, or slot J-1 of thread NT-1
-                } else {
-                    kB = (tmod + 1 == R) ? 0 : tmod + 1;
-                    kA = (kB + 1 == R) ? 0 : kB + 1;
-                    k0 = tmod;
-                }
-                if ((kA % NT) == i) gs.spec[par][0] = qrow[kA];
-                if ((kB % NT) == i) gs.spec[par][1] = qrow[kB];
-                if ((k0 % NT) == i) gs.spec[par][2] = qrow[k0];
                 // ---- group sum (and, EAGER, argmax): the step's only barrier ------------
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
@@ -631,29 +739,58 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 }
                 // ---- the scalar tail (A5-A8): group-uniform, no transcendentals -----------
                 const double Z = sum;
-                const double qA = gs.spec[par][0], qB = gs.spec[par][1], q0 = gs.spec[par][2];
+                double qA, qB, q0;
+                if constexpr (ROT) {
+                    qB = gs.e0[par][iB];
+                    qA = gs.e0[par][iB + 1];
+                    q0 = gs.e0[par][iB == 0 ? NT + 1 : iB - 1];
+                } else {
+                    qA = gs.spec[par][0];
+                    qB = gs.spec[par][1];
+                    q0 = gs.spec[par][2];
+                }
                 const double Zd = merge ? Z : Z - P.omH * qB;    // normaliser of the new posterior
                 const double Zp = merge ? Z : Z - qB;            // p_new = pnum / Zp
                 const double pnum = (merge && R == 2) ? Z : q0;  // MERGE R = 2: p_new = 1
                 uint32_t fl = (t > 0 && pnum > P.theta * Zp) ? 1u : 0u;
-                // common path: branch-free (owner writes predicated) so that, with the step
-                // loop unrolled by two, the next step's cell work can overlap this tail
-                const bool own = (kB % NT) == i;
-                if (own) qrow[kB] = P.hr * Z;  // R_t(0) = H Z / Zd
+                // A6: the new change-point cell (owner of kB) and the MERGE bucket (owner of kA).
+                // ROT: branch-free; the new mass is the slot-0 pending weight wq (no log on the
+                // step's critical path), folded into a at the next rotation step.  Generic: one
+                // divergent block for the one or two owner lanes (one shared log2 pass).
                 if constexpr (ROT) {
-                    const double m0 = gs.mu0, b0 = gs.beta0, l0p = gs.L0;  // the recycled cell is slot 0
-                    mu[0] = own ? m0 : mu[0];
-                    be[0] = own ? b0 : be[0];
-                    L[0] = own ? l0p : L[0];
-                } else if (own) {
-                    set_stats<J>(mu, be, L, kB / NT, gs.mu0, gs.beta0, gs.L0);
+                    const bool ownB = (i == iB);
+                    const bool ownA = merge && (i == iB + 1);  // iB = NT-1: thread 0, slot 1 (rotation)
+                    const double dcd = double(dc);
+                    const double2 cA = s_ca[R - 2];  // G_{R-1} - alpha_{R-1} lg beta' of cell kA
+                    const double offA = fma(-cA.y, gs.l0[par][iB + 1], cA.x);
+                    const double m0 = gs.mu0, b0 = gs.beta0;
+                    const double aB = gs.aprior + dcd, aA = dcd - offA;
+                    const double wB = P.hr * Z, wA = qA + qB;
+                    mu[0] = ownB ? m0 : mu[0];
+                    be[0] = ownB ? b0 : be[0];
+                    a[0] = ownB ? aB : (ownA ? aA : a[0]);
+                    wq = ownB ? wB : (ownA ? wA : wq);
+                } else {
+                const bool ownB = (unsigned(kB) % NT) == unsigned(i);
+                const bool ownA = merge && ((unsigned(kA) % NT) == unsigned(i));
+                if (ownB || ownA) {
+                    const double lv = safe_log2(ownB ? P.hr * Z : qA + qB);
+                    if (ownB) {  // R_t(0) = H Z / Zd: mass hr Z in this step's frame, prior statistics
+                        const double anew = (lv + gs.aprior) + double(dc);
+                        const int jb = kB / NT;
+                        set_slot<J>(mu, jb, gs.mu0);
+                        set_slot<J>(be, jb, gs.beta0);
+                        set_slot<J>(a, jb, anew);
+                    } else {  // bucket: q'_{R-2} + q'_{R-1} with the window statistics of cell kA
+                        const double anew = (lv - gs.spec[par][3]) + double(dc);  // spec[3] = G - alpha lg beta'
+                        set_slot<J>(a, kA / NT, anew);
+                    }
                 }
-                if (merge && (kA % NT) == i) qrow[kA] = qA + qB;  // bucket
+                }
                 if (i == 0) gs.zd_prev = Zd;
-                const bool rot = ROT && (iB + 1 == NT);  // pB crosses a slot boundary
                 // ---- rare path (group-uniform): MAP run length r* (A7), events (A8), per-step
-                // outputs, the slot rotation ---------------------------------------------
-                if (EAGER || (fl & P.ev_mask) || any_out || rot) {
+                // outputs ----------------------------------------------------------------
+                if (EAGER || (fl & P.ev_mask) || any_out) {
                     int r_ex = -1;
                     double qex = 0.0;
                     if constexpr (EAGER) {
@@ -663,20 +800,35 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                         }
                     } else if (fl & P.ev_mask) {  // on demand: an event at this step
                         unsigned long long kb = 0ull;
-#pragma unroll
+                        // one cell at a time (runtime slot index, register arrays read by selects):
+                        // the recomputation must not raise the register pressure of the step loop
+#pragma unroll 1
                         for (int j = 0; j < J; ++j) {
                             const int p = i + NT * j;
                             if (FULL || p < R) {
-                                int r;
+                                int r, id;
                                 if (ROT || TAB2) {
-                                    r = ib - NT * j;
-                                    r -= (r >= R) ? R : 0;
+                                    id = ib - NT * j;
+                                    r = id - ((id >= R) ? R : 0);
                                 } else {
                                     r = tmod - p;
                                     r += (r < 0) ? R : 0;
+                                    id = r;
                                 }
-                                const unsigned long long kq = argmax_key(qrow[p], r);  // own cells only
-                                kb = (r <= r_elig && kq > kb) ? kq : kb;
+                                if (r <= r_elig) {  // the eligible cells kept their a and beta'
+                                    double bj = be[0], aj = a[0];
+#pragma unroll
+                                    for (int jj = 1; jj < J; ++jj) {
+                                        bj = (jj == j) ? be[jj] : bj;
+                                        aj = (jj == j) ? a[jj] : aj;
+                                    }
+                                    const double2 c2 = s_ca[id];
+                                    const double Ln = fast_log2(bj, kFmBase);
+                                    double E = cell_exp2(fma(-c2.y, Ln, aj + c2.x), C7, lb);
+                                    if (ROT && j == 0) E *= wq;
+                                    const unsigned long long kq = argmax_key(E, r);
+                                    kb = kq > kb ? kq : kb;
+                                }
                             }
                         }
                         kb = warp_max_u64(kb);
@@ -728,25 +880,41 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                             gs.lzd_prev = lzd;
                         }
                     }
-                    if (rot) {  // rotate slot j <- slot j+1
-                        phi = (phi + 1) & (J - 1);
-                        const double m0 = mu[0], b0 = be[0], l0r = L[0], qf = qrow[i];
-#pragma unroll
-                        for (int j = 0; j + 1 < J; ++j) {
-                            mu[j] = mu[j + 1];
-                            be[j] = be[j + 1];
-                            L[j] = L[j + 1];
-                            qrow[i + NT * j] = qrow[i + NT * (j + 1)];
-                        }
-                        mu[J - 1] = m0;
-                        be[J - 1] = b0;
-                        L[J - 1] = l0r;
-                        qrow[i + NT * (J - 1)] = qf;
-                    }
                 }
                 zexp = ((__double2hiint(Zd) >> 20) & 0x7FF) - 1023;
                 tmod = (tmod + 1 == R) ? 0 : tmod + 1;
-                if constexpr (ROT) iB = rot ? 0 : iB + 1;
+                if constexpr (ROT) ++iB;
+            }
+            if (ROT && iB == NT) {  // the segment ended at a rotation step (group-uniform)
+                const int par = (base + q - 1) & 1;  // that step's publication buffers
+                // fold every pending weight into its cell, rebase the frame (a fixed global
+                // schedule: every NT steps), then thread 0's bucket cell (slot 1 -> slot 0 after
+                // the rotation) takes its weight q'_{R-2} + q'_{R-1}
+                const double dcd = double(dc);
+                a[0] += safe_log2(wq);
+                wq = 1.0;
+#pragma unroll
+                for (int j = 0; j < J; ++j) a[j] -= dcd;
+                dc = 0;
+                if (merge && i == 0 && J > 1) {
+                    const double2 cA = s_ca[R - 2];
+                    a[1] = -fma(-cA.y, gs.l0[par][NT], cA.x);
+                    wq = gs.e0[par][NT] + gs.e0[par][NT - 1];
+                }
+                // rotate slot j <- slot j+1
+                phi = (phi + 1) & (J - 1);
+                const double m0 = mu[0], b0 = be[0], a0 = a[0];
+#pragma unroll
+                for (int j = 0; j + 1 < J; ++j) {
+                    mu[j] = mu[j + 1];
+                    be[j] = be[j + 1];
+                    a[j] = a[j + 1];
+                }
+                mu[J - 1] = m0;
+                be[J - 1] = b0;
+                a[J - 1] = a0;
+                iB = 0;
+            }
             }
         }
         // ---- spill -----------------------------------------------------------
@@ -755,13 +923,13 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
 #pragma unroll
         for (int j = 0; j < J; ++j) {
             const int p = ROT ? i + NT * ((j + phi) & (J - 1)) : i + NT * j;
-            const int e = ROT ? i + NT * j : p;
             if (FULL || p < R) {
                 P.st_mu[sbase + p] = mu[j];
                 P.st_beta[sbase + p] = be[j];
-                P.st_q[sbase + p] = qrow[e];
+                P.st_a[sbase + p] = a[j];
             }
         }
+        if constexpr (ROT) P.st_w[s * NT + i] = wq;
         if (i == 0) {
             SeriesScalars sc;
             sc.mu0 = gs.mu0;
@@ -770,12 +938,12 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             sc.map_prev = map_prev;
             sc.ev_count = ev_count;
             sc.flags = gs.flags;
-            sc.pad = 0;
+            sc.dc = dc;
             sc.pad2 = 0.0;
             P.scal[s] = sc;
             if (sc.flags) atomicOr(P.err, unsigned(sc.flags));
         }
-        group_sync<NT>(g);  // qrow / gs are reused by the next unit
+        group_sync<NT>(g);  // gs is reused by the next unit
     }
 }
 

@@ -20,7 +20,7 @@ static void make_variant(Variant* out) {
     v.spb = SPB;
     v.full = FULL;
     v.tab2 = TAB2;
-    v.group_smem = sizeof(GroupSmem<NT>);  // + q row (+ PREF buffer): group_bytes
+    v.group_smem = sizeof(GroupSmem<NT>);  // (+ PREF buffer): group_bytes
     *out = v;
 }
 
@@ -61,9 +61,9 @@ int select_variant(int R, Variant* out) {
 size_t variant_smem(const Variant& v, int R, bool persistent) {
     const int rows = v.full ? R + v.nt : (v.tab2 ? 2 * R : R);  // table_entries
     const bool pref = persistent && v.pref;  // only the persistent kernels carry the prefetch buffer
-    const size_t grp = v.group_smem + q_row_doubles(R) * sizeof(double) +
+    const size_t grp = v.group_smem +
                        (pref ? ((3 * size_t(R) * sizeof(double) + sizeof(SeriesScalars) + 15) & ~size_t(15)) : 0);
-    return kFmSmemBytes + table_bytes(rows) + size_t(v.spb) * grp;
+    return kBocdFmBytes + table_bytes(rows) + size_t(v.spb) * grp;
 }
 
 // Test hook: elementwise fast_log2 / fast_exp2 over device arrays.

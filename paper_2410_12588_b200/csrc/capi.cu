@@ -1,8 +1,8 @@
 // capi.cu — host runtime and C ABI of libfalcon_bocd.so (include/falcon_bocd.h).
 //
-// Owns: the per-R predictive constant table (long double on the host, rounded
-// once), the per-series state (mu, beta, unnormalised log posterior v in ring
-// position order, plus SeriesScalars), the per-series event buffers, the
+// Owns: the per-R marginal-likelihood constant table (long double on the host,
+// rounded once), the per-series state (mu, beta and the log-joint offset a of
+// every cell in ring position order, plus SeriesScalars; bocd_kernel.cuh), the per-series event buffers, the
 // host-staging buffers of update_chunk_host, and the drain / posterior-gather
 // kernels.  Every computing entry point launches CUDA kernels; there is no CPU
 // fallback.
@@ -36,7 +36,8 @@ struct falcon_bocd_s {
     fbocd::FastMathTables* d_fm = nullptr;
     double* d_mu = nullptr;
     double* d_beta = nullptr;
-    double* d_v = nullptr;
+    double* d_a = nullptr;  // log-joint offsets a [S][R] (bocd_kernel.cuh)
+    double* d_w = nullptr;  // pending slot-0 weights [S][NT] (FULL kernels; 1 = none)
     SeriesScalars* d_scal = nullptr;
     EventRec* d_ev = nullptr;
     unsigned* d_err = nullptr;
@@ -106,22 +107,29 @@ __global__ void init_scalars_kernel(SeriesScalars* scal, const double* mu0, cons
         sc.map_prev = 0;
         sc.ev_count = 0;
         sc.flags = 0;
-        sc.pad = 0;
+        sc.dc = 0;
         sc.pad2 = 0.0;
         scal[s] = sc;
     }
 }
 
-__global__ void init_state_kernel(double* mu, double* beta, double* q, const SeriesScalars* scal, int64_t S,
-                                  int R) {
+// Before x_0 a segment starts with probability one (Q8): the cell at position 0 has
+// q = 2^(a - alpha0 lg beta0) = 1, every other cell is impossible (a = -inf).
+__global__ void init_state_kernel(double* mu, double* beta, double* a, const SeriesScalars* scal, int64_t S,
+                                  int R, double alpha0) {
     const int64_t n = S * int64_t(R);
     for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
         const int64_t s = k / R;
         const int p = int(k - s * R);
         mu[k] = scal[s].mu0;
         beta[k] = scal[s].beta0;
-        q[k] = (p == 0) ? 1.0 : 0.0;
+        a[k] = (p == 0) ? alpha0 * log2(scal[s].beta0) : -INFINITY;
     }
+}
+
+__global__ void fill_kernel(double* v, int64_t n, double value) {
+    for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x)
+        v[k] = value;
 }
 
 // Exclusive scan of min(count, cap) over series (single CTA), total + overflow flag in meta.
@@ -185,19 +193,31 @@ __global__ void drain_gather_kernel(SeriesScalars* scal, const EventRec* ev, int
     if (reset && lane == 0) scal[s].ev_count = 0;
 }
 
-// Ring position order -> run-length order; R_t(r) = q_r (1-H) / Zd_t.
-__global__ void posterior_kernel(const double* mu, const double* beta, const double* q,
-                                 const SeriesScalars* scal, int64_t s0, int64_t count, int R, int64_t t,
-                                 double omH, double* logR_out, double* mu_out, double* beta_out) {
+// Ring position order -> run-length order; R_t(r) = q_r (1-H) / Zd_t with the cell's
+// q_r = w 2^(a + G_r - alpha_r lg beta - Dc) (bocd_kernel.cuh), G_r / alpha_r from the
+// kernel table (row r-1 = {G_r, alpha_r}; G_0 = 0, alpha_0 = alpha0).  FULL kernels (w != null):
+// the pending weight w of thread i applies to its slot 0, position i + NT phi.
+__global__ void posterior_kernel(const double* mu, const double* beta, const double* a, const double* w, int nt,
+                                 const double2* ca, double alpha0, const SeriesScalars* scal, int64_t s0,
+                                 int64_t count, int R, int64_t t, double omH, double* logR_out, double* mu_out,
+                                 double* beta_out) {
     const int64_t n = count * int64_t(R);
     const int tm = int(t % R);
+    const int phi = w ? ((tm + 1 == R) ? 0 : tm + 1) / nt : 0;
     for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
         const int64_t i = k / R;
         const int r = int(k - i * R);
         int p = tm - r;
         if (p < 0) p += R;
         const int64_t src = (s0 + i) * int64_t(R) + p;
-        if (logR_out) logR_out[k] = log(q[src] * (omH / scal[s0 + i].zd_prev));
+        if (logR_out) {
+            const SeriesScalars& sc = scal[s0 + i];
+            const double G = r ? ca[r - 1].x : 0.0;
+            const double al = r ? ca[r - 1].y : alpha0;
+            double lq = (a[src] + G) - al * log2(beta[src]) - double(sc.dc);
+            if (w && p / nt == phi) lq += log2(w[(s0 + i) * nt + p % nt]);
+            logR_out[k] = 0.6931471805599453 * lq + log(omH / sc.zd_prev);
+        }
         if (mu_out) mu_out[k] = mu[src];
         if (beta_out) beta_out[k] = beta[src];
     }
@@ -374,14 +394,18 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
     falcon_bocd_predictive_constants(R, c.kappa0, c.alpha0, tc.data(), ta.data(), tg.data(), tk.data());
     std::vector<double2> ca(R);
     {
-        // base-2 units: the device table holds c_r / ln2 (bocd_kernel.cuh, A2)
+        // base-2 units: row r holds {G_{r+1}, alpha_{r+1}} with G_n the data-independent part
+        // of the log2 NIG marginal likelihood of n observations (bocd_kernel.cuh, A2),
+        // G_{r+1} = G_r + c_r / ln2 (c_r: the Student-t constant), G_0 = 0
         const long double inv_ln2 = 1.442695040888963407359924681001892137L;
         long double D = lgammal((long double)c.alpha0 + 0.5L) - lgammal((long double)c.alpha0);
         const long double two_pi = 6.283185307179586476925286766559005768L;
+        long double G = 0.0L;
         for (int r = 0; r < R; ++r) {
             const long double kap = (long double)c.kappa0 + r;
             const long double cr = D - 0.5L * logl(two_pi * (kap + 1.0L) / kap);
-            ca[r] = make_double2((double)(cr * inv_ln2), ta[r]);
+            G += cr * inv_ln2;
+            ca[r] = make_double2((double)G, (double)((long double)c.alpha0 + 0.5L * (r + 1)));
             D = logl((long double)c.alpha0 + 0.5L * r) - D;
         }
     }
@@ -403,7 +427,8 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
     ALLOC(h->d_fm, sizeof(fbocd::FastMathTables));
     ALLOC(h->d_mu, SR * sizeof(double));
     ALLOC(h->d_beta, SR * sizeof(double));
-    ALLOC(h->d_v, SR * sizeof(double));
+    ALLOC(h->d_a, SR * sizeof(double));
+    ALLOC(h->d_w, size_t(S) * h->var.nt * sizeof(double));
     ALLOC(h->d_scal, S * sizeof(SeriesScalars));
     ALLOC(h->d_ev, size_t(S) * c.event_capacity * sizeof(EventRec));
     ALLOC(h->d_err, sizeof(unsigned));
@@ -421,7 +446,9 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
     if (e3 == cudaSuccess) e3 = cudaMemset(h->d_err, 0, sizeof(unsigned));
     if (e3 == cudaSuccess) {
         init_scalars_kernel<<<grid_for(S, 256), 256>>>(h->d_scal, dmu0, dbeta0, S, 1.0 - c.hazard);
-        init_state_kernel<<<grid_for(int64_t(SR), 256), 256>>>(h->d_mu, h->d_beta, h->d_v, h->d_scal, S, R);
+        init_state_kernel<<<grid_for(int64_t(SR), 256), 256>>>(h->d_mu, h->d_beta, h->d_a, h->d_scal, S, R,
+                                                               c.alpha0);
+        fill_kernel<<<grid_for(S * h->var.nt, 256), 256>>>(h->d_w, S * h->var.nt, 1.0);
         e3 = cudaGetLastError();
     }
     if (e3 == cudaSuccess) e3 = cudaDeviceSynchronize();
@@ -461,7 +488,8 @@ static int launch_update(falcon_bocd_t h, const double* x_dev, int64_t ld, int64
         P.fm = h->d_fm;
         P.st_mu = h->d_mu;
         P.st_beta = h->d_beta;
-        P.st_q = h->d_v;
+        P.st_a = h->d_a;
+        P.st_w = h->d_w;
         P.scal = h->d_scal;
         P.ev = h->d_ev;
         P.err = h->d_err;
@@ -669,8 +697,11 @@ int falcon_bocd_read_posterior(falcon_bocd_t h, int64_t s0, int64_t count, doubl
         if (!outs[k]) continue;
         dst[k] = is_device_ptr(outs[k]) ? outs[k] : tmp + k * n;
     }
-    posterior_kernel<<<grid_for(int64_t(n), 256), 256, 0, st>>>(h->d_mu, h->d_beta, h->d_v, h->d_scal, s0, count, R,
-                                                                h->t, 1.0 - h->cfg.hazard, dst[0], dst[1], dst[2]);
+    posterior_kernel<<<grid_for(int64_t(n), 256), 256, 0, st>>>(h->d_mu, h->d_beta, h->d_a,
+                                                                h->var.full ? h->d_w : nullptr, h->var.nt,
+                                                                h->d_ca, h->cfg.alpha0,
+                                                                h->d_scal, s0, count, R, h->t, 1.0 - h->cfg.hazard,
+                                                                dst[0], dst[1], dst[2]);
     cudaError_t e = cudaGetLastError();
     for (int k = 0; k < 3 && e == cudaSuccess; ++k)
         if (outs[k] && dst[k] != outs[k])
@@ -707,7 +738,7 @@ int falcon_bocd_destroy(falcon_bocd_t h) {
         }
     }
     cudaGetLastError();
-    void* ptrs[] = {h->d_ca, h->d_y, h->d_fm, h->d_mu, h->d_beta, h->d_v, h->d_scal, h->d_ev, h->d_err, h->d_off,
+    void* ptrs[] = {h->d_ca, h->d_y, h->d_fm, h->d_mu, h->d_beta, h->d_a, h->d_w, h->d_scal, h->d_ev, h->d_err, h->d_off,
                     h->d_meta, h->d_evout, h->d_stage[0], h->d_stage[1], h->d_omap, h->d_opnew, h->d_ologz};
     for (void* p : ptrs)
         if (p) cudaFree(p);

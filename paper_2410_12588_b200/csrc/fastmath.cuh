@@ -21,11 +21,15 @@
 //       the max term 1), d = (64 k + j)/64 + r exactly, |r| <= 1/128,
 //       2^d = 2^k T_j (1 + q(r)), T_j = 2^(j/64) from a 64-entry table, q the
 //       degree-5 Taylor polynomial of 2^r - 1 (truncation < 4e-17).  9 FP64 ops.
+//       The table stores T'_j = T_j with (j << 14) subtracted from its high word, so
+//       the high word of 2^k T_j is ONE integer multiply-add of the rounded argument
+//       n = 64 k + j: n * 2^14 + hi(T'_j) = (k << 20) + hi(T_j)  (mod 2^32).
 // Both tables live in shared memory.  Accuracy is tested against numpy/mpmath
 // through the falcon_bocd_debug_fastmath hook (tests/test_gpu_fastmath.py).
 #pragma once
 
 #include <cstdint>
+#include <cstring>
 #include <cuda_runtime.h>
 
 namespace fbocd {
@@ -37,7 +41,7 @@ constexpr double INV_LN2 = 1.4426950408889634;
 
 struct FastMathTables {
     double2 logtab[kLogTab];  // {invc_i, -log2(invc_i)}
-    double exptab[kExpTab];   // 2^(j/64)
+    double exptab[kExpTab];   // 2^(j/64), high word minus (j << 14) (see exp2 above)
 };
 
 // z-interval of index i: i < 150 -> [c0 + i/512, +1/512), else [1 + (i-150)/256, +1/256)
@@ -57,7 +61,14 @@ inline void fill_fastmath_tables(FastMathTables* t) {
         t->logtab[i].x = invc;
         t->logtab[i].y = (double)(-log2l((long double)invc));
     }
-    for (int j = 0; j < kExpTab; ++j) t->exptab[j] = (double)exp2l((long double)j / 64.0L);
+    for (int j = 0; j < kExpTab; ++j) {
+        const double v = (double)exp2l((long double)j / 64.0L);
+        uint64_t b;
+        static_assert(sizeof(b) == sizeof(v), "double is 64-bit");
+        std::memcpy(&b, &v, sizeof(b));
+        b -= uint64_t(uint32_t(j) << 14) << 32;  // pre-compensate the index bits (hi word)
+        std::memcpy(&t->exptab[j], &b, sizeof(b));
+    }
 }
 
 // The tables live in DYNAMIC shared memory at a 2048-B aligned address fmb (logtab at
@@ -143,8 +154,8 @@ __device__ __forceinline__ double fast_exp2(double x, unsigned fmb) {
     p = fma(p, r, c_fm[12]);
     const double q = p * r;
     const double T = lds_f64(((ki << 3) & 0x1F8u) + (fmb + 4096u));
-    int th;  // high word of T * 2^(ki >> 6): one IMAD
-    asm("mad.lo.s32 %0, %1, 1048576, %2;" : "=r"(th) : "r"(int(ki) >> 6), "r"(__double2hiint(T)));
+    int th;  // high word of T_j * 2^(ki >> 6) = ki * 2^14 + hi(T'_j): one IMAD
+    asm("mad.lo.s32 %0, %1, 16384, %2;" : "=r"(th) : "r"(ki), "r"(__double2hiint(T)));
     const double Ts = __hiloint2double(th, __double2loint(T));
     return fma(Ts, q, Ts);
 }
