@@ -14,7 +14,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libfalcon_bocd.so")
 SOURCES = ["capi.cu", "bocd_kernels.cu", "tracegen.cu", "verify.cu", "groups.cu", "acf.cu"]
-HEADERS = ["bocd_kernel.cuh", "bocd_variants.h", "fastmath.cuh"]
+HEADERS = ["bocd_kernel.cuh", "bocd_variants.h", "fastmath.cuh", "cellmath.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", f"-I{os.path.join(ROOT, 'include')}"]

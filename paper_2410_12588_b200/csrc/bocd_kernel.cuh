@@ -59,6 +59,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "cellmath.cuh"
 #include "fastmath.cuh"
 
 namespace fbocd {
@@ -73,8 +74,9 @@ constexpr int kG = FALCON_BOCD_KG;  // cells per interleaved group (ILP)
 #define FALCON_BOCD_STEP_UNROLL 1
 #endif
 constexpr int kStepUnroll = FALCON_BOCD_STEP_UNROLL;  // steps per unrolled loop body
-// K0_t = round(l0_t) is clamped to +-kK0Max so that |N_t| < 2^16 and 64 Dc stays below 2^31
-constexpr double kK0Max = 32768.0;
+// K0_t = round(l0_t) is clamped to +-kK0Max so that |N_t| < 2^14 and 256 Dc stays below 2^31
+// (at most 512 steps between rebases)
+constexpr double kK0Max = 8192.0;
 
 struct SeriesScalars {  // per-series state carried between calls (HBM), 48 B
     double mu0, beta0;  // prior (set from x_0 when prior_first_obs)
@@ -105,7 +107,8 @@ struct KParams {
     int ev_cap;
     const double2* tab_ca;     // [R] row r: {G_{r+1}, alpha_{r+1}}
     const double* tab_y;       // [R] y_r = 1/(kappa_r+1)
-    const FastMathTables* fm;  // log2 / exp2 tables
+    const FastMathTables* fm;  // log2 / exp2 tables (per-step scalars)
+    const CellTables* ct;      // the cell loop's log2 / exp2 tables (cellmath.cuh)
     double* st_mu;             // [S][R] position order
     double* st_beta;
     double* st_a;
@@ -301,62 +304,33 @@ __host__ __device__ constexpr int table_entries(int R) {
 // the fast-math tables sit at the compile-time address kFmBase (checked at entry).
 constexpr unsigned kDynBase = 0x400u;
 constexpr unsigned kFmBase = 0x800u;
-// The exp2 table replicated 16 times, entry j of copy c at kExpRepBase + 128 j + 8 c: lane L
-// reads copy L mod 16, so the 32 lanes of a warp hit 32 distinct banks whatever their
-// indices (2 wavefronts per warp-wide 8-B lookup, no bank conflicts).  The per-r tables
-// start after it: kBocdFmBytes of the dynamic window hold the fast-math tables.
-constexpr unsigned kExpRepBase = 0x2000u;
-// The log2 table (16-B entries) replicated kLogRep times the same way (entry i of copy c at
-// kLogRepBase + 16 (kLogRep i + c), lane L reads copy L mod kLogRep): kLogRep = 8 makes the
-// 4 wavefronts of a warp-wide 16-B lookup conflict-free, but measured slower at R = 1024
-// (82.9 vs 82.0 ms per C3 call; 4 copies 84.5 ms): off by default (tuning knob).
-#ifndef FALCON_BOCD_LOGREP
-#define FALCON_BOCD_LOGREP 1
-#endif
-constexpr int kLogRep = FALCON_BOCD_LOGREP;
-constexpr int kLogRepShift = kLogRep == 8 ? 5 : kLogRep == 4 ? 6 : kLogRep == 2 ? 7 : 8;
-static_assert(kLogRep == 1 || kLogRep == 2 || kLogRep == 4 || kLogRep == 8, "kLogRep: 1, 2, 4 or 8");
-constexpr unsigned kLogRepBase = 0x4000u;
-constexpr unsigned kBocdFmBytes = (kLogRep > 1 ? kLogRepBase + 4096u * kLogRep : kExpRepBase + 8192u) - kDynBase;
-static_assert(kLogRepBase == 16384u && kFmBase + kFmSmemBytes - 2048u <= kExpRepBase, "fast-math tables overlap the replicated exp2 table");
-
-// log2 table entry for tb = hi(x) + 0x00196000: index (tb >> 12) & 255; llb = 16 (lane mod kLogRep)
-__device__ __forceinline__ double2 lds_log_entry(unsigned tb, unsigned llb) {
-    double2 v;
-    if constexpr (kLogRep > 1) {
-        asm("ld.shared.v2.f64 {%0, %1}, [%2+16384];"
-            : "=d"(v.x), "=d"(v.y)
-            : "r"(((tb >> kLogRepShift) & (0xFF0u * kLogRep)) | llb));  // kLogRepBase
-    } else {
-        asm("ld.shared.v2.f64 {%0, %1}, [%2+2048];" : "=d"(v.x), "=d"(v.y) : "r"((tb >> 8) & 0xFF0u));
-    }
-    return v;
+// The cell loop's tables (cellmath.cuh) follow the fast-math tables at compile-time
+// addresses; the per-r tables start after them.  EC: copies of the exp2 table (16, conflict-
+// free, for the R <= 1024 FULL kernels; 8 otherwise, where the per-r tables are larger).
+__host__ __device__ constexpr int cell_ec(bool full, int r_full) { return (full && r_full <= 1024) ? 16 : 8; }
+__host__ __device__ constexpr unsigned bocd_fm_bytes(int ec) {
+    return (ec == 16 ? cell_tables_end<16>() : cell_tables_end<8>()) - kDynBase;
 }
-// replicated exp2 table: address = ((ki << 7) & 0x1F80) | lb, lb = kExpRepBase + 8 (lane & 15)
-__device__ __forceinline__ double lds_exp_entry(unsigned ki, unsigned lb) {
-    double v;
-    asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(((ki << 7) & 0x1F80u) | lb));
-    return v;
-}
+static_assert(kFmBase + kFmSmemBytes - 2048u <= kCellExpBase, "fast-math tables overlap the cell tables");
 
-// exp2 of a cell: q' = 2^(ell - Dc) with C7 = 1.5 2^52 + 2^31 - 64 Dc (fast_exp2 of
-// fastmath.cuh with the frame folded into the rounding constant).  Exactly 0 below
-// 2^-1021 (also for ell = -inf), exponent clamped at +1000.  The cell
-// loop evaluates the same operations stage by stage; the on-demand MAP recomputation
-// calls this and must agree bit for bit.
-__device__ __forceinline__ double cell_exp2(double ell, double C7, unsigned lb) {
-    const double zf = fma(ell, 64.0, C7);
+// exp2 of a cell: q' = 2^(ell - Dc) with C7 = 1.5 2^52 + 2^31 - 256 Dc (cellmath.cuh's
+// reduction with the frame folded into the rounding constant).  Exactly 0 below 2^-1021
+// (also for ell = -inf), exponent clamped at +1000.  The cell loop evaluates
+// the same operations stage by stage; the on-demand MAP recomputation calls this and must
+// agree bit for bit.
+template <int EC>
+__device__ __forceinline__ double cell_exp2(double ell, double C7, unsigned lbe) {
+    const double zf = fma(ell, 256.0, C7);
     const unsigned ki = unsigned(__double2loint(zf));
-    const double re = fma(zf - C7, -0.015625, ell);
-    const double T = lds_exp_entry(ki, lb);
-    double p = fma(re, kExp2C0, c_fm[9]);
-    p = fma(p, re, c_fm[10]);
-    p = fma(p, re, c_fm[11]);
-    p = fma(p, re, c_fm[12]);
+    const double re = fma(zf - C7, -0.00390625, ell);
+    const double T = cell_exp_entry<EC>(ki, lbe);
+    double p = fma(re, kCellExpQ3, c_cell[11]);
+    p = fma(p, re, c_cell[10]);
+    p = fma(p, re, c_cell[9]);
     const double qq = p * re;
-    const bool dead = ki < 0x80000000u - 65344u;
-    const unsigned kc = min(ki, 0x80000000u + 64063u);
-    const double Ts = __hiloint2double(int(kc * 16384u) + __double2hiint(T), __double2loint(T));
+    const bool dead = ki < 0x80000000u - 261376u;
+    const unsigned kc = min(ki, 0x80000000u + 256255u);
+    const double Ts = __hiloint2double(int(kc * 4096u) + __double2hiint(T), __double2loint(T));
     return dead ? 0.0 : fma(Ts, qq, Ts);
 }
 
@@ -377,13 +351,14 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     constexpr bool PREF = PERSIST && kPrefOk<NT, J, FULL>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr bool ROT = FULL;
+    constexpr int EC = cell_ec(FULL, NT * J);
     const int R = FULL ? NT * J : P.R;
     const int RT = table_entries<NT, J, FULL, TAB2>(R);
-    // dynamic shared memory: [fast-math tables + replicated exp2 table (kBocdFmBytes)][per-r tables][groups]
+    // dynamic shared memory: [fast-math tables, cell tables (bocd_fm_bytes)][per-r tables][groups]
     unsigned char* const smem = smem_raw;
-    double2* s_ca = reinterpret_cast<double2*>(smem + kBocdFmBytes);
+    double2* s_ca = reinterpret_cast<double2*>(smem + bocd_fm_bytes(EC));
     double* s_y = reinterpret_cast<double*>(s_ca + RT);
-    unsigned char* gbase = smem + kBocdFmBytes + table_bytes(RT);
+    unsigned char* gbase = smem + bocd_fm_bytes(EC) + table_bytes(RT);
 
     for (int k = threadIdx.x; k < RT; k += blockDim.x) {
         const int r = k < R ? k : k - R;
@@ -392,15 +367,12 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     }
     const bool fm_ok = smem_addr(smem_raw) == kDynBase && fm_setup(smem_raw, P.fm) == kFmBase;
     {
-        double* rep = reinterpret_cast<double*>(smem_raw + (kExpRepBase - kDynBase));
-        for (int k = threadIdx.x; k < kExpTab * 16; k += blockDim.x) rep[k] = P.fm->exptab[k >> 4];
+        double* ex = reinterpret_cast<double*>(smem_raw + (kCellExpBase - kDynBase));
+        for (int k = threadIdx.x; k < kCellExpTab * EC; k += blockDim.x) ex[k] = P.ct->exptab[k / EC];
+        double2* lg = reinterpret_cast<double2*>(smem_raw + (cell_log_base<EC>() - kDynBase));
+        for (int k = threadIdx.x; k < (1 << kCellLB); k += blockDim.x) lg[k] = P.ct->logtab[k];
     }
-    if constexpr (kLogRep > 1) {
-        double2* rep = reinterpret_cast<double2*>(smem_raw + (kLogRepBase - kDynBase));
-        for (int k = threadIdx.x; k < kLogTab * kLogRep; k += blockDim.x) rep[k] = P.fm->logtab[k / kLogRep];
-    }
-    const unsigned lb = kExpRepBase + 8u * (threadIdx.x & 15u);
-    const unsigned llb = 16u * (threadIdx.x & unsigned(kLogRep - 1));
+    const unsigned lb = 8u * (threadIdx.x & unsigned(EC - 1));  // exp2 table copy of this lane
     const int g = threadIdx.x / NT;
     const int i = threadIdx.x % NT;
     const int lane = threadIdx.x & 31;
@@ -575,9 +547,9 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     dc = 0;
                 }
                 dc += K0 + zexp;  // Dc_t = Dc_{t-1} + N_t
-                // exp2 rounding constant 1.5*2^52 + 2^31 - 64 Dc_t: zf = fma(l, 64, C7) holds
-                // round(64 l) - 64 Dc_t + 2^31 in its low word (exact integers below 2^52)
-                const double C7 = __hiloint2double(0x43380000, int(0x80000000u - unsigned(dc) * 64u));
+                // exp2 rounding constant 1.5*2^52 + 2^31 - 256 Dc_t: zf = fma(l, 256, C7) holds
+                // round(256 l) - 256 Dc_t + 2^31 in its low word (exact integers below 2^52)
+                const double C7 = __hiloint2double(0x43380000, int(0x80000000u - unsigned(dc) * 256u));
                 // ---- A1-A4 for the J cells (groups of G, every stage across the group) ----
                 // table index of slot j: ib - NT*j  (= r or r + R).  FULL: r of slot j is
                 // (pB - 1 - p) mod R = (iB - 1 - i - NT j) mod R.
@@ -626,29 +598,31 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                         bn[kk] = fma(d[kk], fma(mu[j0 + kk], -0.5, hx), be[j0 + kk]);
                         be[j0 + kk] = bn[kk];
                     }
-                    // A2: lg beta' (fast_log2 of fastmath.cuh, stage by stage)
+                    // A2: lg beta' (cell_log2 of cellmath.cuh, stage by stage)
                     unsigned tb[G];
                     double2 lt[G];
                     double rl[G], kt[G], pl[G];
 #pragma unroll
                     for (int kk = 0; kk < G; ++kk) {
-                        tb[kk] = unsigned(__double2hiint(bn[kk])) + 0x00196000u;
-                        lt[kk] = lds_log_entry(tb[kk], llb);
+                        tb[kk] = unsigned(__double2hiint(bn[kk]));
+                        lt[kk] = cell_log_entry<EC>(tb[kk]);
                     }
 #pragma unroll
                     for (int kk = 0; kk < G; ++kk) {
-                        const double invs = __hiloint2double(__double2hiint(lt[kk].x) + 0x40000000 -
-                                                                 int(tb[kk] & 0xFFF00000u),
+                        const double invs = __hiloint2double(__double2hiint(lt[kk].x) + 0x3FF00000 -
+                                                                 int(tb[kk] & 0x7FF00000u),
                                                              __double2loint(lt[kk].x));
                         rl[kk] = fma(bn[kk], invs, -1.0);
-                        kt[kk] = (__hiloint2double(0x43300000, int(tb[kk] >> 20)) - c_fm[6]) + lt[kk].y;
+                        kt[kk] = (__hiloint2double(0x43300000, int(tb[kk] >> 20)) - 4503599627371519.0) + lt[kk].y;
                     }
+                    {
+                        constexpr int o = 3 * (kCellLB - 8);
 #pragma unroll
-                    for (int kk = 0; kk < G; ++kk) pl[kk] = fma(rl[kk], kLog2C0, c_fm[1]);
+                        for (int kk = 0; kk < G; ++kk) pl[kk] = fma(rl[kk], kCellLogP3, c_cell[o + 2]);
 #pragma unroll
-                    for (int c = 2; c <= 4; ++c) {
+                        for (int kk = 0; kk < G; ++kk) pl[kk] = fma(pl[kk], rl[kk], c_cell[o + 1]);
 #pragma unroll
-                        for (int kk = 0; kk < G; ++kk) pl[kk] = fma(pl[kk], rl[kk], c_fm[c]);
+                        for (int kk = 0; kk < G; ++kk) pl[kk] = fma(pl[kk], rl[kk], c_cell[o]);
                     }
                     double ell[G];
 #pragma unroll
@@ -668,28 +642,27 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     unsigned ki[G];
 #pragma unroll
                     for (int kk = 0; kk < G; ++kk) {
-                        const double zf = fma(ell[kk], 64.0, C7);
+                        const double zf = fma(ell[kk], 256.0, C7);
                         ki[kk] = unsigned(__double2loint(zf));
-                        re[kk] = fma(zf - C7, -0.015625, ell[kk]);  // exact, |re| <= 1/128
-                        Tv[kk] = lds_exp_entry(ki[kk], lb);
+                        re[kk] = fma(zf - C7, -0.00390625, ell[kk]);  // exact, |re| <= 2^-9
+                        Tv[kk] = cell_exp_entry<EC>(ki[kk], lb);
                     }
 #pragma unroll
-                    for (int kk = 0; kk < G; ++kk) pe[kk] = fma(re[kk], kExp2C0, c_fm[9]);
+                    for (int kk = 0; kk < G; ++kk) pe[kk] = fma(re[kk], kCellExpQ3, c_cell[11]);
 #pragma unroll
-                    for (int c = 10; c <= 12; ++c) {
+                    for (int kk = 0; kk < G; ++kk) pe[kk] = fma(pe[kk], re[kk], c_cell[10]);
 #pragma unroll
-                        for (int kk = 0; kk < G; ++kk) pe[kk] = fma(pe[kk], re[kk], c_fm[c]);
-                    }
+                    for (int kk = 0; kk < G; ++kk) pe[kk] = fma(pe[kk], re[kk], c_cell[9]);
 #pragma unroll
                     for (int kk = 0; kk < G; ++kk) {
                         const int j = j0 + kk;
                         const int p = i + NT * j;
                         const double qq = pe[kk] * re[kk];
-                        // 2^e, e = floor(n/64) for n = ki - 2^31: exactly 0 below 2^-1021, e clamped
-                        // at +1000; hi word = kc * 2^14 + hi(T'_j) (fastmath.cuh)
-                        const bool dead = ki[kk] < 0x80000000u - 65344u;
-                        const unsigned kc = min(ki[kk], 0x80000000u + 64063u);
-                        const double Ts = __hiloint2double(int(kc * 16384u) + __double2hiint(Tv[kk]),
+                        // 2^e, e = floor(n/256) for n = ki - 2^31: exactly 0 below 2^-1021, e clamped
+                        // at +1000; hi word = kc * 2^12 + hi(T'_j) (cellmath.cuh)
+                        const bool dead = ki[kk] < 0x80000000u - 261376u;
+                        const unsigned kc = min(ki[kk], 0x80000000u + 256255u);
+                        const double Ts = __hiloint2double(int(kc * 4096u) + __double2hiint(Tv[kk]),
                                                            __double2loint(Tv[kk]));
                         double E = dead ? 0.0 : fma(Ts, qq, Ts);
                         if (ROT && j == 0) E *= wq;  // slot 0's pending weight (new CP / bucket mass)
@@ -823,8 +796,8 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                                         aj = (jj == j) ? a[jj] : aj;
                                     }
                                     const double2 c2 = s_ca[id];
-                                    const double Ln = fast_log2(bj, kFmBase);
-                                    double E = cell_exp2(fma(-c2.y, Ln, aj + c2.x), C7, lb);
+                                    const double Ln = cell_log2<EC>(bj);
+                                    double E = cell_exp2<EC>(fma(-c2.y, Ln, aj + c2.x), C7, lb);
                                     if (ROT && j == 0) E *= wq;
                                     const unsigned long long kq = argmax_key(E, r);
                                     kb = kq > kb ? kq : kb;

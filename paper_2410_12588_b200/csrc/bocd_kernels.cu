@@ -63,31 +63,52 @@ size_t variant_smem(const Variant& v, int R, bool persistent) {
     const bool pref = persistent && v.pref;  // only the persistent kernels carry the prefetch buffer
     const size_t grp = v.group_smem +
                        (pref ? ((3 * size_t(R) * sizeof(double) + sizeof(SeriesScalars) + 15) & ~size_t(15)) : 0);
-    return kBocdFmBytes + table_bytes(rows) + size_t(v.spb) * grp;
+    return bocd_fm_bytes(cell_ec(v.full, v.nt * v.j)) + table_bytes(rows) + size_t(v.spb) * grp;
 }
 
-// Test hook: elementwise fast_log2 / fast_exp2 over device arrays.
+// Test hook: elementwise fast_log2 / fast_exp2 (which 0 / 1) and the cell loop's cell_log2 /
+// cell_exp2 (which 2 / 3; tables at the BOCD kernel's addresses) over device arrays.
 __global__ void fastmath_probe_kernel(int which, const double* in, double* out, int64_t n,
-                                      const FastMathTables* tab) {
+                                      const FastMathTables* tab, const CellTables* ct) {
     extern __shared__ __align__(16) unsigned char dyn[];
     const unsigned fmb = fm_setup(dyn, tab);
+    const bool at_base = smem_addr(dyn) == kDynBase && fmb == kFmBase;
+    double* ex = reinterpret_cast<double*>(dyn + (kCellExpBase - kDynBase));
+    for (int k = threadIdx.x; k < kCellExpTab * 16; k += blockDim.x) ex[k] = ct->exptab[k >> 4];
+    double2* lg = reinterpret_cast<double2*>(dyn + (cell_log_base<16>() - kDynBase));
+    for (int k = threadIdx.x; k < (1 << kCellLB); k += blockDim.x) lg[k] = ct->logtab[k];
     __syncthreads();
-    for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x)
-        out[k] = which == 0 ? fast_log2(in[k], fmb) : fast_exp2(in[k], fmb);
+    const double C7 = __hiloint2double(0x43380000, int(0x80000000u));  // Dc = 0
+    const unsigned lbe = 8u * (threadIdx.x & 15u);
+    for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
+        double v;
+        switch (which) {
+            case 0: v = fast_log2(in[k], fmb); break;
+            case 1: v = fast_exp2(in[k], fmb); break;
+            case 2: v = cell_log2<16>(in[k]); break;
+            default: v = cell_exp2<16>(in[k], C7, lbe); break;
+        }
+        out[k] = at_base ? v : __longlong_as_double(0x7FF8000000000000ll);  // NaN: layout check failed
+    }
 }
 
 int launch_fastmath_probe(int which, const double* in, double* out, int64_t n, const FastMathTables* tab,
-                          cudaStream_t st) {
+                          const CellTables* ct, cudaStream_t st) {
     int64_t blocks = (n + 255) / 256;
     if (blocks > 4096) blocks = 4096;
     if (blocks < 1) blocks = 1;
-    fastmath_probe_kernel<<<unsigned(blocks), 256, kFmSmemBytes, st>>>(which, in, out, n, tab);
+    const size_t smem = bocd_fm_bytes(16);
+    if (cudaFuncSetAttribute(fastmath_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
+        cudaSuccess)
+        return -1;
+    fastmath_probe_kernel<<<unsigned(blocks), 256, smem, st>>>(which, in, out, n, tab, ct);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 // The constant bank is per translation unit: this is the copy the kernels above read.
 int upload_fastmath_constants() {
-    return cudaMemcpyToSymbol(c_fm, kFastMathConstants, sizeof(kFastMathConstants)) == cudaSuccess ? 0 : -1;
+    if (cudaMemcpyToSymbol(c_fm, kFastMathConstants, sizeof(kFastMathConstants)) != cudaSuccess) return -1;
+    return cudaMemcpyToSymbol(c_cell, kCellConstants, sizeof(kCellConstants)) == cudaSuccess ? 0 : -1;
 }
 
 }  // namespace fbocd

@@ -26,8 +26,9 @@ int select_variant(int R, Variant* out);
 size_t variant_smem(const Variant& v, int R, bool persistent);
 
 struct FastMathTables;
+struct CellTables;
 int upload_fastmath_constants();  // once per device, before any kernel that uses fast_log2/exp2
 int launch_fastmath_probe(int which, const double* in, double* out, int64_t n, const FastMathTables* tab,
-                          cudaStream_t st);
+                          const CellTables* ct, cudaStream_t st);
 
 }  // namespace fbocd

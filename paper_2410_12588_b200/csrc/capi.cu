@@ -34,6 +34,7 @@ struct falcon_bocd_s {
     double2* d_ca = nullptr;
     double* d_y = nullptr;
     fbocd::FastMathTables* d_fm = nullptr;
+    fbocd::CellTables* d_ct = nullptr;
     double* d_mu = nullptr;
     double* d_beta = nullptr;
     double* d_a = nullptr;  // log-joint offsets a [S][R] (bocd_kernel.cuh)
@@ -411,6 +412,8 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
     }
     fbocd::FastMathTables fmt;
     fbocd::fill_fastmath_tables(&fmt);
+    std::vector<fbocd::CellTables> cellt(1);
+    fbocd::fill_cell_tables(cellt.data());
     const size_t SR = size_t(S) * size_t(R);
     double *dmu0 = nullptr, *dbeta0 = nullptr;
 #define ALLOC(ptr, bytes)                                                   \
@@ -425,6 +428,7 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
     ALLOC(h->d_ca, R * sizeof(double2));
     ALLOC(h->d_y, R * sizeof(double));
     ALLOC(h->d_fm, sizeof(fbocd::FastMathTables));
+    ALLOC(h->d_ct, sizeof(fbocd::CellTables));
     ALLOC(h->d_mu, SR * sizeof(double));
     ALLOC(h->d_beta, SR * sizeof(double));
     ALLOC(h->d_a, SR * sizeof(double));
@@ -441,6 +445,7 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
     if (e3 == cudaSuccess) e3 = cudaMemcpy(h->d_ca, ca.data(), R * sizeof(double2), cudaMemcpyHostToDevice);
     if (e3 == cudaSuccess) e3 = cudaMemcpy(h->d_y, tk.data(), R * sizeof(double), cudaMemcpyHostToDevice);
     if (e3 == cudaSuccess) e3 = cudaMemcpy(h->d_fm, &fmt, sizeof(fmt), cudaMemcpyHostToDevice);
+    if (e3 == cudaSuccess) e3 = cudaMemcpy(h->d_ct, cellt.data(), sizeof(fbocd::CellTables), cudaMemcpyHostToDevice);
     if (e3 == cudaSuccess) e3 = cudaMemcpy(dmu0, mu0.data(), S * sizeof(double), cudaMemcpyHostToDevice);
     if (e3 == cudaSuccess) e3 = cudaMemcpy(dbeta0, beta0.data(), S * sizeof(double), cudaMemcpyHostToDevice);
     if (e3 == cudaSuccess) e3 = cudaMemset(h->d_err, 0, sizeof(unsigned));
@@ -486,6 +491,7 @@ static int launch_update(falcon_bocd_t h, const double* x_dev, int64_t ld, int64
         P.tab_ca = h->d_ca;
         P.tab_y = h->d_y;
         P.fm = h->d_fm;
+        P.ct = h->d_ct;
         P.st_mu = h->d_mu;
         P.st_beta = h->d_beta;
         P.st_a = h->d_a;
@@ -738,7 +744,7 @@ int falcon_bocd_destroy(falcon_bocd_t h) {
         }
     }
     cudaGetLastError();
-    void* ptrs[] = {h->d_ca, h->d_y, h->d_fm, h->d_mu, h->d_beta, h->d_a, h->d_w, h->d_scal, h->d_ev, h->d_err, h->d_off,
+    void* ptrs[] = {h->d_ca, h->d_y, h->d_fm, h->d_ct, h->d_mu, h->d_beta, h->d_a, h->d_w, h->d_scal, h->d_ev, h->d_err, h->d_off,
                     h->d_meta, h->d_evout, h->d_stage[0], h->d_stage[1], h->d_omap, h->d_opnew, h->d_ologz};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -754,18 +760,28 @@ int falcon_bocd_destroy(falcon_bocd_t h) {
 const char* falcon_bocd_last_error(falcon_bocd_t h) { return h ? h->err.c_str() : g_create_err.c_str(); }
 
 int falcon_bocd_debug_fastmath(int32_t which, const double* in_dev, double* out_dev, int64_t n, void* stream) {
-    if ((which != 0 && which != 1) || n < 0 || (n > 0 && (!in_dev || !out_dev))) return FALCON_EINVAL;
+    if (which < 0 || which > 3 || n < 0 || (n > 0 && (!in_dev || !out_dev))) return FALCON_EINVAL;
     if (n == 0) return FALCON_OK;
     fbocd::FastMathTables fmt;
     fbocd::fill_fastmath_tables(&fmt);
+    std::vector<fbocd::CellTables> cellt(1);
+    fbocd::fill_cell_tables(cellt.data());
     fbocd::FastMathTables* d = nullptr;
+    fbocd::CellTables* dc = nullptr;
     cudaStream_t st = (cudaStream_t)stream;
     if (fbocd::upload_fastmath_constants() != 0) return FALCON_ECUDA;
     if (cudaMalloc((void**)&d, sizeof(fmt)) != cudaSuccess) return FALCON_ENOMEM;
+    if (cudaMalloc((void**)&dc, sizeof(fbocd::CellTables)) != cudaSuccess) {
+        cudaFree(d);
+        return FALCON_ENOMEM;
+    }
     cudaError_t e = cudaMemcpyAsync(d, &fmt, sizeof(fmt), cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess && fbocd::launch_fastmath_probe(which, in_dev, out_dev, n, d, st) != 0) e = cudaErrorLaunchFailure;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dc, cellt.data(), sizeof(fbocd::CellTables), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && fbocd::launch_fastmath_probe(which, in_dev, out_dev, n, d, dc, st) != 0)
+        e = cudaErrorLaunchFailure;
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     cudaFree(d);
+    cudaFree(dc);
     return e == cudaSuccess ? FALCON_OK : FALCON_ECUDA;
 }
 

@@ -1,0 +1,115 @@
+// cellmath.cuh — the BOCD cell loop's log2 / exp2.
+//
+// The cell loop needs, per run-length cell and step, lg beta' and 2^(l - Dc)
+// (bocd_kernel.cuh).  In the log-joint form an error in either enters only the
+// current step's q' (it is not carried forward by a multiplicative recursion), so
+// polynomial degree is traded for table size against the 1e-9 parity budget
+// (BASELINE.json north_star; the measured errors stay orders of magnitude below it):
+//   cell_log2<LB>: b = 2^k z, z in [1, 2) split into 2^LB intervals of width 2^-LB by the
+//              top LB mantissa bits; {invc_i, l_i = -log2(invc_i)} from the table;
+//              r = z invc_i - 1 (one FMA, |r| <= 2^-(LB+1)); log2 b = k + l_i + r P(r),
+//              P the degree-3 Chebyshev interpolant of log2(1+r)/r: max |error| of r P(r)
+//              1.0e-15 (LB = 8), 3.2e-17 (LB = 9), 9.9e-19 (LB = 10).  7 FP64 ops.
+//   cell_exp2: d = (256 k + j)/256 + r exactly (|r| <= 2^-9), 2^d = 2^k T_j (1 + r Q(r)),
+//              T_j = 2^(j/256) from a 256-entry table, Q the degree-3 Chebyshev interpolant
+//              of (2^r - 1)/r (max |error| of r Q(r) 4.8e-18).  8 FP64 ops.
+// The coefficients were fitted with 60-digit mpmath (Chebyshev nodes on the reduced
+// interval) and rounded to double; the leading ones are DFMA immediates.  Tables are
+// computed on the host in long double.  Accuracy: tests/test_gpu_fastmath.py.
+//
+// Shared-memory layout inside the BOCD kernel's dynamic window (absolute shared addresses,
+// LDS immediates): the exp2 table replicated EC times (entry j of copy c at kCellExpBase +
+// 8 (EC j + c); lane L reads copy L mod EC, so EC = 16 makes a warp-wide lookup
+// conflict-free), then the log2 table (2^LB entries of 16 B).
+#pragma once
+
+#include <cstdint>
+#include <cstring>
+#include <cmath>
+#include <cuda_runtime.h>
+
+namespace fbocd {
+
+#ifndef FALCON_BOCD_LOGBITS
+#define FALCON_BOCD_LOGBITS 8
+#endif
+constexpr int kCellLB = FALCON_BOCD_LOGBITS;  // log2 table bits (8, 9 or 10)
+static_assert(kCellLB >= 8 && kCellLB <= 10, "FALCON_BOCD_LOGBITS: 8, 9 or 10");
+constexpr int kCellExpTab = 256;
+
+struct CellTables {
+    double exptab[kCellExpTab];       // 2^(j/256), high word minus (j << 12)
+    double2 logtab[1 << kCellLB];     // {invc_i, -log2(invc_i)}, z in [1 + i/2^LB, 1 + (i+1)/2^LB)
+};
+
+inline void fill_cell_tables(CellTables* t) {
+    for (int j = 0; j < kCellExpTab; ++j) {
+        const double v = (double)exp2l((long double)j / 256.0L);
+        uint64_t b;
+        std::memcpy(&b, &v, sizeof(b));
+        b -= uint64_t(uint32_t(j) << 12) << 32;  // n * 2^12 + hi(T'_j) = (k << 20) + hi(T_j)
+        std::memcpy(&t->exptab[j], &b, sizeof(b));
+    }
+    const int n = 1 << kCellLB;
+    for (int i = 0; i < n; ++i) {
+        const long double c = 1.0L + ((long double)i + 0.5L) / (long double)n;
+        const double invc = (double)(1.0L / c);
+        t->logtab[i].x = invc;
+        t->logtab[i].y = (double)(-log2l((long double)invc));
+    }
+}
+
+// Polynomial coefficients (constant bank; uploaded with the fast-math constants): P0..P2 of
+// the log for LB = 8, 9, 10 at 3 (LB - 8), Q0..Q2 of the exp at 9.
+static __constant__ double c_cell[12];
+static const double kCellConstants[12] = {
+    1.4426950408884385, -0.7213475204440444, 0.4808994476545776,   // LB = 8
+    1.4426950408889305, -0.7213475204444544, 0.4808986221353932,   // LB = 9
+    1.4426950408889614, -0.72134752044448, 0.4808984157560584,     // LB = 10
+    0.6931471805599428, 0.24022650695910044, 0.05550411375117056};  // exp
+// leading coefficients rounded to 20 mantissa bits (DFMA immediates; the rounding is weighted
+// by r^4 <= 2^-36, i.e. below 1e-18)
+constexpr double kCellLogP3 = kCellLB == 8 ? -0.3606746196746826 : -0.3606739044189453;
+constexpr double kCellExpQ3 = 0.009618133306503296;  // 0.009618129695226546
+
+constexpr unsigned kCellExpBase = 0x1A00u;
+template <int EC>
+__host__ __device__ constexpr unsigned cell_log_base() { return kCellExpBase + kCellExpTab * EC * 8u; }
+template <int EC>
+__host__ __device__ constexpr unsigned cell_tables_end() { return cell_log_base<EC>() + (16u << kCellLB); }
+
+// log2 table entry of b, tb = hi(b)
+template <int EC>
+__device__ __forceinline__ double2 cell_log_entry(unsigned tb) {
+    double2 v;
+    asm("ld.shared.v2.f64 {%0, %1}, [%2+%3];"
+        : "=d"(v.x), "=d"(v.y)
+        : "r"((tb >> (16 - kCellLB)) & (((1u << kCellLB) - 1u) << 4)), "n"(cell_log_base<EC>()));
+    return v;
+}
+
+template <int EC>
+__device__ __forceinline__ double cell_log2(double b) {
+    const unsigned tb = unsigned(__double2hiint(b));
+    const double2 t = cell_log_entry<EC>(tb);
+    const double invs = __hiloint2double(__double2hiint(t.x) + 0x3FF00000 - int(tb & 0x7FF00000u), __double2loint(t.x));
+    const double r = fma(b, invs, -1.0);
+    const double kt = (__hiloint2double(0x43300000, int(tb >> 20)) - 4503599627371519.0) + t.y;  // k + l_i
+    constexpr int o = 3 * (kCellLB - 8);
+    double p = fma(r, kCellLogP3, c_cell[o + 2]);
+    p = fma(p, r, c_cell[o + 1]);
+    p = fma(p, r, c_cell[o]);
+    return fma(r, p, kt);
+}
+
+// exp2 table entry for the rounded argument ki (low word of the 1.5 2^52 + 2^31 rounding);
+// lbe = 8 (lane mod EC)
+template <int EC>
+__device__ __forceinline__ double cell_exp_entry(unsigned ki, unsigned lbe) {
+    double v;
+    constexpr int sh = EC == 16 ? 7 : 6;
+    asm("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(((ki << sh) & (255u << sh)) | lbe), "n"(kCellExpBase));
+    return v;
+}
+
+}  // namespace fbocd

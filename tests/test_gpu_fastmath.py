@@ -63,3 +63,36 @@ def test_fast_exp2_clamps_below():
     x = np.array([-np.inf, -1e300, -1022.0, -1074.5, -1e5])
     got = _probe(1, x)
     assert np.all(np.isfinite(got)) and np.all(got >= 0) and np.all(got < 1e-306)
+
+
+def test_cell_log2_accuracy():
+    """The cell loop's log2 (csrc/cellmath.cuh): 2^LB intervals + degree-3 Chebyshev fit (max
+    |error| 1.0e-15 at LB = 8), plus the rounding of k + l_i: an ABSOLUTE error (the recursion
+    uses alpha * lg beta' against a per-cell offset) within 1.1e-15 + 2 ulp(max(|log2 x|, 1))."""
+    rng = np.random.default_rng(2)
+    x = np.concatenate([
+        np.exp(rng.uniform(np.log(1e-300), np.log(1e300), 200000)),
+        rng.uniform(0.5, 4.0, 200000),
+        1.0 + rng.normal(0, 1e-6, 20000),
+        np.array([1.0, 2.0, 0.5, np.nextafter(1.0, 2), np.nextafter(1.0, 0), np.nextafter(2.0, 0),
+                  2.2250738585072014e-308, 1.7e308]),
+    ])
+    got = _probe(2, x)
+    ref = np.log2(x)
+    err = np.abs(got - ref)
+    bad = err > 1.1e-15 + 2.0 * np.spacing(np.maximum(np.abs(ref), 1.0))
+    assert not np.any(bad), list(zip(x[bad][:5], got[bad][:5], ref[bad][:5]))
+
+
+def test_cell_exp2_accuracy_and_cutoff():
+    """The cell loop's exp2 (256-entry table, degree-4 Chebyshev fit): relative error within
+    2.5e-16 on (-1021, 30]; exactly 0 below 2^-1021 and for -inf (impossible cells)."""
+    rng = np.random.default_rng(3)
+    x = np.concatenate([-rng.exponential(5.0, 200000), rng.uniform(-1020.9, 0, 200000),
+                        rng.uniform(0, 30, 20000), np.array([0.0, -0.0, 1e-12, -1e-300, -1020.5])])
+    got = _probe(3, x)
+    ref = np.exp2(x)
+    err = np.abs(got - ref) / ref
+    assert np.all(err <= 2.5e-16), float(err.max())
+    dead = _probe(3, np.array([-np.inf, -1021.5, -1e4, -2e6]))
+    assert np.all(dead == 0.0)
