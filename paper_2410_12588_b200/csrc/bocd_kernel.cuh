@@ -65,6 +65,7 @@
 namespace fbocd {
 
 constexpr int kTile = 256;     // x steps per shared-memory tile (2 KB)
+constexpr int kTileP = 64;     // persistent (streaming) kernels: calls of <= 64 steps
 constexpr int kRebase = 256;   // generic kernels: global steps between frame rebases (ROT: every NT)
 #ifndef FALCON_BOCD_KG
 #define FALCON_BOCD_KG 4
@@ -127,10 +128,10 @@ struct KParams {
     int tma_ok;  // x base 16-B aligned and ld even
 };
 
-template <int NT>
+template <int NT, int TILE = kTile>
 struct __align__(16) GroupSmem {
-    double xbuf[2][kTile];
-    int kbuf[2][kTile];  // K0_t = round(l0_t) of the tile's steps
+    double xbuf[2][TILE];
+    int kbuf[2][TILE];  // K0_t = round(l0_t) of the tile's steps
     // red2 / red1 / spec are double-buffered by step parity: a warp that runs ahead into
     // step t+1 cannot overwrite what a slower warp still reads after barrier t
     double red2[2][NT / 32 > 0 ? NT / 32 : 1];
@@ -220,17 +221,18 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long k)
     return (static_cast<unsigned long long>(hmax) << 32) | lmax;
 }
 
-template <int NT>
-__device__ __forceinline__ void issue_tile_tma(GroupSmem<NT>& gs, const double* xrow, int k, int T) {
-    const int base = k * kTile;
-    const int n = min(kTile, T - base);
+template <int NT, int TILE>
+__device__ __forceinline__ void issue_tile_tma(GroupSmem<NT, TILE>& gs, const double* xrow, int k, int T) {
+    const int base = k * TILE;
+    const int n = min(TILE, T - base);
     fence_proxy_async();
     mbar_arrive_expect_tx(&gs.mbar[k & 1], unsigned(n) * 8u);
     tma_load_1d(gs.xbuf[k & 1], xrow + base, unsigned(n) * 8u, &gs.mbar[k & 1]);
 }
 
+template <int TILE>
 __device__ __forceinline__ bool tile_tma_ok(const KParams& P, int k) {
-    const int n = min(kTile, P.T - k * kTile);
+    const int n = min(TILE, P.T - k * TILE);
     return P.tma_ok && ((n & 1) == 0);
 }
 
@@ -240,7 +242,7 @@ __device__ __forceinline__ bool tile_tma_ok(const KParams& P, int k) {
 // per group: GroupSmem and (PREF) the prefetch buffer [mu R][beta R][a R][scalars]
 template <int NT, bool PREF>
 __host__ __device__ constexpr size_t group_bytes(int R) {
-    return sizeof(GroupSmem<NT>) +
+    return sizeof(GroupSmem<NT, PREF ? kTileP : kTile>) +
            (PREF ? ((3 * size_t(R) * sizeof(double) + sizeof(SeriesScalars) + 15) & ~size_t(15)) : 0);
 }
 // bytes of the per-r tables ({G_{r+1}, alpha_{r+1}} and y_r) for `entries` table rows
@@ -307,9 +309,13 @@ constexpr unsigned kFmBase = 0x800u;
 // The cell loop's tables (cellmath.cuh) follow the fast-math tables at compile-time
 // addresses; the per-r tables start after them.  EC: copies of the exp2 table (16, conflict-
 // free, for the R <= 1024 FULL kernels; 8 otherwise, where the per-r tables are larger).
-__host__ __device__ constexpr int cell_ec(bool full, int r_full) { return (full && r_full <= 1024) ? 16 : 8; }
+// The persistent prefetching kernels (HBM-bound streaming) take 4 copies and 64-step x tiles
+// so that two CTAs with their prefetch buffers still fit one SM.
+__host__ __device__ constexpr int cell_ec(bool full, int r_full, bool pref) {
+    return pref ? 4 : ((full && r_full <= 1024) ? 16 : 8);
+}
 __host__ __device__ constexpr unsigned bocd_fm_bytes(int ec) {
-    return (ec == 16 ? cell_tables_end<16>() : cell_tables_end<8>()) - kDynBase;
+    return (ec == 16 ? cell_tables_end<16>() : ec == 8 ? cell_tables_end<8>() : cell_tables_end<4>()) - kDynBase;
 }
 static_assert(kFmBase + kFmSmemBytes - 2048u <= kCellExpBase, "fast-math tables overlap the cell tables");
 
@@ -351,7 +357,9 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     constexpr bool PREF = PERSIST && kPrefOk<NT, J, FULL>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr bool ROT = FULL;
-    constexpr int EC = cell_ec(FULL, NT * J);
+    constexpr int EC = cell_ec(FULL, NT * J, PREF);
+    constexpr int TILE = PREF ? kTileP : kTile;
+    using GS = GroupSmem<NT, TILE>;
     const int R = FULL ? NT * J : P.R;
     const int RT = table_entries<NT, J, FULL, TAB2>(R);
     // dynamic shared memory: [fast-math tables, cell tables (bocd_fm_bytes)][per-r tables][groups]
@@ -377,9 +385,9 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     const int i = threadIdx.x % NT;
     const int lane = threadIdx.x & 31;
     const int w = i >> 5;
-    GroupSmem<NT>& gs = *reinterpret_cast<GroupSmem<NT>*>(gbase + size_t(g) * group_bytes<NT, PREF>(R));
+    GS& gs = *reinterpret_cast<GS*>(gbase + size_t(g) * group_bytes<NT, PREF>(R));
     // PREF: the prefetched next-unit state [mu R][beta R][a R][SeriesScalars], position order
-    double* const pf = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(&gs) + sizeof(GroupSmem<NT>));
+    double* const pf = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(&gs) + sizeof(GS));
     SeriesScalars* const pf_sc = reinterpret_cast<SeriesScalars*>(pf + 3 * size_t(R));
     const int64_t nunits = (P.S + SPB - 1) / SPB;
     if (i == 0) {
@@ -389,7 +397,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         mbar_fence_init();
     }
     __syncthreads();
-    const int ntiles = (P.T + kTile - 1) / kTile;
+    const int ntiles = (P.T + TILE - 1) / TILE;
     const bool merge = (P.mode == 0);
     const bool any_out = P.out_map || P.out_pnew || P.out_logz;  // per-step outputs requested
     // argmax-eligible run lengths: MERGE r <= R-3 (slot R-1 is the bucket), DROP r <= R-2
@@ -417,7 +425,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         if (s >= P.S) break;  // group-uniform; later units only have larger s
         const double* xrow = P.x + s * P.ld;
         // Prefetch tile 0 (TMA) as early as possible.
-        if (i == 0 && ntiles > 0 && tile_tma_ok(P, 0)) issue_tile_tma<NT>(gs, xrow, 0, P.T);
+        if (i == 0 && ntiles > 0 && tile_tma_ok<TILE>(P, 0)) issue_tile_tma<NT, TILE>(gs, xrow, 0, P.T);
 
         // ---- load or initialise the state --------------------------------
         double mu[J], be[J], a[J];
@@ -507,13 +515,13 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         if (i == 0 && P.out_logz) gs.lzd_prev = fast_log2(gs.zd_prev, kFmBase);
 
         for (int k = 0; k < ntiles; ++k) {
-            const int base = k * kTile;
-            const int n = min(kTile, P.T - base);
+            const int base = k * TILE;
+            const int n = min(TILE, P.T - base);
             const int buf = k & 1;
             // prefetch the next tile into the other buffer (its previous readers all
             // passed at least one group barrier since their last read)
-            if (i == 0 && k + 1 < ntiles && tile_tma_ok(P, k + 1)) issue_tile_tma<NT>(gs, xrow, k + 1, P.T);
-            if (tile_tma_ok(P, k)) {
+            if (i == 0 && k + 1 < ntiles && tile_tma_ok<TILE>(P, k + 1)) issue_tile_tma<NT, TILE>(gs, xrow, k + 1, P.T);
+            if (tile_tma_ok<TILE>(P, k)) {
                 mbar_wait(&gs.mbar[buf], (xphase >> buf) & 1u);
                 xphase ^= 1u << buf;
             } else {

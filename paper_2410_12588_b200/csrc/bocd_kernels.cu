@@ -20,7 +20,8 @@ static void make_variant(Variant* out) {
     v.spb = SPB;
     v.full = FULL;
     v.tab2 = TAB2;
-    v.group_smem = sizeof(GroupSmem<NT>);  // (+ PREF buffer): group_bytes
+    v.group_smem = sizeof(GroupSmem<NT, kTile>);
+    v.group_smem_p = sizeof(GroupSmem<NT, kPrefOk<NT, J, FULL> ? kTileP : kTile>);  // (+ PREF buffer): group_bytes
     *out = v;
 }
 
@@ -36,6 +37,8 @@ int select_variant(int R, Variant* out) {
         if (ev && strcmp(ev, "128x8s3") == 0) { make_variant<128, 8, true, true, 3, 1>(out); return 0; }
         if (ev && strcmp(ev, "64x16s8") == 0) { make_variant<64, 16, true, true, 8, 1>(out); return 0; }
         if (ev && strcmp(ev, "64x16s4") == 0) { make_variant<64, 16, true, true, 4, 1>(out); return 0; }
+        if (ev && strcmp(ev, "64x16s3m2") == 0) { make_variant<64, 16, true, true, 3, 2>(out); return 0; }
+        if (ev && strcmp(ev, "64x16s2m3") == 0) { make_variant<64, 16, true, true, 2, 3>(out); return 0; }
         if (ev && strcmp(ev, "128x8s2m1") == 0) { make_variant<128, 8, true, true, 2, 1>(out); return 0; }
         if (ev && strcmp(ev, "256x4s1m2") == 0) { make_variant<256, 4, true, true, 1, 2>(out); return 0; }
         if (ev && strcmp(ev, "256x4s1m3") == 0) { make_variant<256, 4, true, true, 1, 3>(out); return 0; }
@@ -61,9 +64,9 @@ int select_variant(int R, Variant* out) {
 size_t variant_smem(const Variant& v, int R, bool persistent) {
     const int rows = v.full ? R + v.nt : (v.tab2 ? 2 * R : R);  // table_entries
     const bool pref = persistent && v.pref;  // only the persistent kernels carry the prefetch buffer
-    const size_t grp = v.group_smem +
+    const size_t grp = (pref ? v.group_smem_p : v.group_smem) +
                        (pref ? ((3 * size_t(R) * sizeof(double) + sizeof(SeriesScalars) + 15) & ~size_t(15)) : 0);
-    return bocd_fm_bytes(cell_ec(v.full, v.nt * v.j)) + table_bytes(rows) + size_t(v.spb) * grp;
+    return bocd_fm_bytes(cell_ec(v.full, v.nt * v.j, pref)) + table_bytes(rows) + size_t(v.spb) * grp;
 }
 
 // Test hook: elementwise fast_log2 / fast_exp2 (which 0 / 1) and the cell loop's cell_log2 /

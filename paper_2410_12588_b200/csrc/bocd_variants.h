@@ -17,7 +17,8 @@ struct Variant {
     int spb = 0;               // series groups per CTA
     bool full = false;         // R == nt * j at compile time
     bool tab2 = false;         // doubled per-r tables
-    size_t group_smem = 0;     // bytes of GroupSmem (the q row and the PREF buffer come on top)
+    size_t group_smem = 0;     // bytes of GroupSmem (one-unit kernels)
+    size_t group_smem_p = 0;   // of the persistent kernels' GroupSmem (64-step tiles); + PREF buffer
     bool pref = false;         // the persistent kernels prefetch the next unit's state (TMA)
 };
 

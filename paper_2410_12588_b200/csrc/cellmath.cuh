@@ -103,11 +103,11 @@ __device__ __forceinline__ double cell_log2(double b) {
 }
 
 // exp2 table entry for the rounded argument ki (low word of the 1.5 2^52 + 2^31 rounding);
-// lbe = 8 (lane mod EC)
+// lbe = 8 (lane mod EC), EC = 4, 8 or 16
 template <int EC>
 __device__ __forceinline__ double cell_exp_entry(unsigned ki, unsigned lbe) {
     double v;
-    constexpr int sh = EC == 16 ? 7 : 6;
+    constexpr int sh = EC == 16 ? 7 : EC == 8 ? 6 : 5;  // 3 + log2(EC)
     asm("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(((ki << sh) & (255u << sh)) | lbe), "n"(kCellExpBase));
     return v;
 }
