@@ -78,6 +78,22 @@ constexpr int kStepUnroll = FALCON_BOCD_STEP_UNROLL;  // steps per unrolled loop
 // K0_t = round(l0_t) is clamped to +-kK0Max so that |N_t| < 2^14 and 256 Dc stays below 2^31
 // (at most 512 steps between rebases)
 constexpr double kK0Max = 8192.0;
+// FLOOR (default): a cell's joint below 2^-1021 of the step reference is floored to
+// [2^-1021, 2^-1019) by a two-sided integer clamp (no select per cell), and impossible cells
+// (run lengths longer than the data seen) carry the finite offset kImpossible instead of
+// -inf (read_posterior still reports -inf for them).  FALCON_BOCD_FLOOR=0: exact zeros.
+#ifndef FALCON_BOCD_FLOOR
+#define FALCON_BOCD_FLOOR 1
+#endif
+constexpr bool kFloor = FALCON_BOCD_FLOOR != 0;
+constexpr double kImpossible = -1048576.0;  // -2^20: 256 |l - Dc| stays below 2^31
+// A MERGE bucket mass below this (floored dead / impossible cells only) is an exact 0, so run
+// lengths longer than the data seen stay impossible.
+constexpr double kDeadMass = 0x1p-1015;
+__device__ __forceinline__ double bucket_mass(double qA, double qB) {
+    const double v = qA + qB;
+    return (kFloor && v < kDeadMass) ? 0.0 : v;
+}
 
 struct SeriesScalars {  // per-series state carried between calls (HBM), 48 B
     double mu0, beta0;  // prior (set from x_0 when prior_first_obs)
@@ -263,13 +279,14 @@ __device__ __forceinline__ void set_slot(double (&a)[J], int j, double v) {
 }
 
 // log2 of v >= 0 for the per-step scalars (new change-point mass, MERGE bucket):
-// 0 -> -inf; arguments outside fast_log2's range (2^-1000, 2^1000) are scaled by 2^-+600.
+// 0 -> -inf (kImpossible under FLOOR); arguments outside fast_log2's range (2^-1000, 2^1000)
+// are scaled by 2^-+600.
 __device__ __forceinline__ double safe_log2(double v) {
     const bool tiny = v < 0x1p-900;
     const bool huge = v > 0x1p+900;
     const double s = tiny ? v * 0x1p+600 : (huge ? v * 0x1p-600 : v);
     const double l = fast_log2(s, 0x800u) + (tiny ? -600.0 : (huge ? 600.0 : 0.0));
-    return v > 0.0 ? l : -__longlong_as_double(0x7FF0000000000000ll);
+    return v > 0.0 ? l : (kFloor ? kImpossible : -__longlong_as_double(0x7FF0000000000000ll));
 }
 
 // Prior predictive of x (A1 + A2 of the prior, log2 units): the tile's exponent
@@ -320,8 +337,9 @@ __host__ __device__ constexpr unsigned bocd_fm_bytes(int ec) {
 static_assert(kFmBase + kFmSmemBytes - 2048u <= kCellExpBase, "fast-math tables overlap the cell tables");
 
 // exp2 of a cell: q' = 2^(ell - Dc) with C7 = 1.5 2^52 + 2^31 - 256 Dc (cellmath.cuh's
-// reduction with the frame folded into the rounding constant).  Exactly 0 below 2^-1021
-// (also for ell = -inf), exponent clamped at +1000.  The cell loop evaluates
+// reduction with the frame folded into the rounding constant).  Below 2^-1021: floored to
+// [2^-1021, 2^-1019) (FLOOR) or exactly 0 (also for ell = -inf); exponent clamped at +1000
+// (DESIGN.md §3).  The cell loop evaluates
 // the same operations stage by stage; the on-demand MAP recomputation calls this and must
 // agree bit for bit.
 template <int EC>
@@ -335,9 +353,10 @@ __device__ __forceinline__ double cell_exp2(double ell, double C7, unsigned lbe)
     p = fma(p, re, c_cell[9]);
     const double qq = p * re;
     const bool dead = ki < 0x80000000u - 261376u;
-    const unsigned kc = min(ki, 0x80000000u + 256255u);
+    const unsigned kc = kFloor ? max(min(ki, 0x80000000u + 256255u), 0x80000000u - 261376u)
+                               : min(ki, 0x80000000u + 256255u);
     const double Ts = __hiloint2double(int(kc * 4096u) + __double2hiint(T), __double2loint(T));
-    return dead ? 0.0 : fma(Ts, qq, Ts);
+    return (!kFloor && dead) ? 0.0 : fma(Ts, qq, Ts);
 }
 
 // PREF is used for power-of-two R up to 1024, where the buffer (24 B x R per series) fits
@@ -350,7 +369,7 @@ constexpr bool kPrefOk = FULL && NT * J <= 1024;
 // once per CTA.  PREF: the state rows (mu, beta, a) and scalars of the group's NEXT unit
 // are prefetched into shared memory by 1-D TMA bulk copies while the current unit computes
 // (streaming calls with a few steps per call are then bound by HBM, not by load latency).
-template <int NT, int J, bool FULL, bool TAB2, bool EAGER, int SPB, int MINB, bool PERSIST>
+template <int NT, int J, bool FULL, bool TAB2, bool EAGER, int SPB, int MINB, bool PERSIST, int MODE>
 __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParams P) {
     // PERSIST: grid = co-resident CTAs looping over units (streaming calls); otherwise one
     // unit per CTA (long calls: the hardware scheduler, no loop overhead).  Same arithmetic.
@@ -358,6 +377,10 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr bool ROT = FULL;
     constexpr int EC = cell_ec(FULL, NT * J, PREF);
+    // FULL: absolute shared addresses of the per-r tables (the dynamic window starts at
+    // kDynBase, checked at entry with the fast-math tables)
+    constexpr unsigned kCaBase = kDynBase + bocd_fm_bytes(EC);
+    constexpr unsigned kYBase = kCaBase + unsigned(NT * J + NT) * 16u;
     constexpr int TILE = PREF ? kTileP : kTile;
     using GS = GroupSmem<NT, TILE>;
     const int R = FULL ? NT * J : P.R;
@@ -398,11 +421,11 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     }
     __syncthreads();
     const int ntiles = (P.T + TILE - 1) / TILE;
-    const bool merge = (P.mode == 0);
+    constexpr bool merge = (MODE == 0);  // truncation at R: MERGE (0) or DROP (1)
     const bool any_out = P.out_map || P.out_pnew || P.out_logz;  // per-step outputs requested
     // argmax-eligible run lengths: MERGE r <= R-3 (slot R-1 is the bucket), DROP r <= R-2
     const int r_elig = merge ? R - 3 : R - 2;
-    const double ninf = -__longlong_as_double(0x7FF0000000000000ll);
+    const double ninf = kFloor ? kImpossible : -__longlong_as_double(0x7FF0000000000000ll);
     unsigned xphase = 0u;  // parity of the two x-tile mbarriers (bit b: mbar[b])
     unsigned sphase = 0u;  // parity of the state mbarrier
     auto issue_state = [&](int64_t sn) {  // thread 0 of the group: next unit's state -> pf
@@ -551,7 +574,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 if (!ROT && (unsigned(t) & (kRebase - 1)) == 0u) {  // generic: rebase at t % kRebase == 0
                     const double dcd = double(dc);
 #pragma unroll
-                    for (int j = 0; j < J; ++j) a[j] -= dcd;
+                    for (int j = 0; j < J; ++j) a[j] = kFloor ? fmax(a[j] - dcd, kImpossible) : a[j] - dcd;
                     dc = 0;
                 }
                 dc += K0 + zexp;  // Dc_t = Dc_{t-1} + N_t
@@ -593,8 +616,13 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                             idx[kk] += (idx[kk] < 0) ? R : 0;
                         }
                         if (!FULL && p >= R) idx[kk] = 0;  // masked cell: any valid entry
-                        ca[kk] = s_ca[idx[kk]];
-                        yv[kk] = s_y[idx[kk]];
+                        if constexpr (FULL) {  // compile-time shared addresses (no generic pointers)
+                            ca[kk] = lds_v2f64(unsigned(idx[kk]) * 16u + kCaBase);
+                            yv[kk] = lds_f64(unsigned(idx[kk]) * 8u + kYBase);
+                        } else {
+                            ca[kk] = s_ca[idx[kk]];
+                            yv[kk] = s_y[idx[kk]];
+                        }
                     }
                     // A1: NIG update
 #pragma unroll
@@ -669,10 +697,11 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                         // 2^e, e = floor(n/256) for n = ki - 2^31: exactly 0 below 2^-1021, e clamped
                         // at +1000; hi word = kc * 2^12 + hi(T'_j) (cellmath.cuh)
                         const bool dead = ki[kk] < 0x80000000u - 261376u;
-                        const unsigned kc = min(ki[kk], 0x80000000u + 256255u);
+                        const unsigned kc = kFloor ? max(min(ki[kk], 0x80000000u + 256255u), 0x80000000u - 261376u)
+                                                   : min(ki[kk], 0x80000000u + 256255u);
                         const double Ts = __hiloint2double(int(kc * 4096u) + __double2hiint(Tv[kk]),
                                                            __double2loint(Tv[kk]));
-                        double E = dead ? 0.0 : fma(Ts, qq, Ts);
+                        double E = (!kFloor && dead) ? 0.0 : fma(Ts, qq, Ts);
                         if (ROT && j == 0) E *= wq;  // slot 0's pending weight (new CP / bucket mass)
                         if (FULL || p < R) {
                             sum += E;
@@ -746,7 +775,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     const double offA = fma(-cA.y, gs.l0[par][iB + 1], cA.x);
                     const double m0 = gs.mu0, b0 = gs.beta0;
                     const double aB = gs.aprior + dcd, aA = dcd - offA;
-                    const double wB = P.hr * Z, wA = qA + qB;
+                    const double wB = P.hr * Z, wA = bucket_mass(qA, qB);
                     mu[0] = ownB ? m0 : mu[0];
                     be[0] = ownB ? b0 : be[0];
                     a[0] = ownB ? aB : (ownA ? aA : a[0]);
@@ -755,7 +784,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 const bool ownB = (unsigned(kB) % NT) == unsigned(i);
                 const bool ownA = merge && ((unsigned(kA) % NT) == unsigned(i));
                 if (ownB || ownA) {
-                    const double lv = safe_log2(ownB ? P.hr * Z : qA + qB);
+                    const double lv = safe_log2(ownB ? P.hr * Z : bucket_mass(qA, qB));
                     if (ownB) {  // R_t(0) = H Z / Zd: mass hr Z in this step's frame, prior statistics
                         const double anew = (lv + gs.aprior) + double(dc);
                         const int jb = kB / NT;
@@ -875,12 +904,12 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 a[0] += safe_log2(wq);
                 wq = 1.0;
 #pragma unroll
-                for (int j = 0; j < J; ++j) a[j] -= dcd;
+                for (int j = 0; j < J; ++j) a[j] = kFloor ? fmax(a[j] - dcd, kImpossible) : a[j] - dcd;
                 dc = 0;
                 if (merge && i == 0 && J > 1) {
                     const double2 cA = s_ca[R - 2];
                     a[1] = -fma(-cA.y, gs.l0[par][NT], cA.x);
-                    wq = gs.e0[par][NT] + gs.e0[par][NT - 1];
+                    wq = bucket_mass(gs.e0[par][NT], gs.e0[par][NT - 1]);
                 }
                 // rotate slot j <- slot j+1
                 phi = (phi + 1) & (J - 1);

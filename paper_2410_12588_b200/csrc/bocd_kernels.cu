@@ -7,13 +7,13 @@
 
 namespace fbocd {
 
-template <int NT, int J, bool FULL, bool TAB2, int SPB, int MINB>
-static void make_variant(Variant* out) {
+template <int NT, int J, bool FULL, bool TAB2, int SPB, int MINB, int MODE>
+static void make_variant_mode(Variant* out) {
     Variant v;
-    v.fn = reinterpret_cast<const void*>(&bocd_update_kernel<NT, J, FULL, TAB2, false, SPB, MINB, false>);
-    v.fn_eager = reinterpret_cast<const void*>(&bocd_update_kernel<NT, J, FULL, TAB2, true, SPB, MINB, false>);
-    v.fn_p = reinterpret_cast<const void*>(&bocd_update_kernel<NT, J, FULL, TAB2, false, SPB, MINB, true>);
-    v.fn_eager_p = reinterpret_cast<const void*>(&bocd_update_kernel<NT, J, FULL, TAB2, true, SPB, MINB, true>);
+    v.fn = reinterpret_cast<const void*>(&bocd_update_kernel<NT, J, FULL, TAB2, false, SPB, MINB, false, MODE>);
+    v.fn_eager = reinterpret_cast<const void*>(&bocd_update_kernel<NT, J, FULL, TAB2, true, SPB, MINB, false, MODE>);
+    v.fn_p = reinterpret_cast<const void*>(&bocd_update_kernel<NT, J, FULL, TAB2, false, SPB, MINB, true, MODE>);
+    v.fn_eager_p = reinterpret_cast<const void*>(&bocd_update_kernel<NT, J, FULL, TAB2, true, SPB, MINB, true, MODE>);
     v.pref = kPrefOk<NT, J, FULL>;
     v.nt = NT;
     v.j = J;
@@ -24,40 +24,37 @@ static void make_variant(Variant* out) {
     v.group_smem_p = sizeof(GroupSmem<NT, kPrefOk<NT, J, FULL> ? kTileP : kTile>);  // (+ PREF buffer): group_bytes
     *out = v;
 }
+// the truncation mode is a template parameter of the kernels (MERGE / DROP specialised tails)
+template <int NT, int J, bool FULL, bool TAB2, int SPB, int MINB>
+static void make_variant(int mode, Variant* out) {
+    if (mode == 0)
+        make_variant_mode<NT, J, FULL, TAB2, SPB, MINB, 0>(out);
+    else
+        make_variant_mode<NT, J, FULL, TAB2, SPB, MINB, 1>(out);
+}
 
 // Variant choice: FULL kernels (R = NT*J, compile-time ring arithmetic) for the
 // power-of-two R of the BASELINE configs; generic kernels (runtime R, masked
 // cells) for any other 2 <= R <= 4096.  Each variant has a lazy-MAP and an
-// EAGER-MAP kernel (bocd_kernel.cuh).
-int select_variant(int R, Variant* out) {
-    // Tuning hook (bench / profiling only): alternative shapes for R = 1024.
-    if (R == 1024) {
-        const char* ev = getenv("FALCON_BOCD_VARIANT");
-        if (ev && strcmp(ev, "128x8s4") == 0) { make_variant<128, 8, true, true, 4, 1>(out); return 0; }
-        if (ev && strcmp(ev, "128x8s3") == 0) { make_variant<128, 8, true, true, 3, 1>(out); return 0; }
-        if (ev && strcmp(ev, "64x16s8") == 0) { make_variant<64, 16, true, true, 8, 1>(out); return 0; }
-        if (ev && strcmp(ev, "64x16s4") == 0) { make_variant<64, 16, true, true, 4, 1>(out); return 0; }
-        if (ev && strcmp(ev, "64x16s3m2") == 0) { make_variant<64, 16, true, true, 3, 2>(out); return 0; }
-        if (ev && strcmp(ev, "64x16s2m3") == 0) { make_variant<64, 16, true, true, 2, 3>(out); return 0; }
-        if (ev && strcmp(ev, "128x8s2m1") == 0) { make_variant<128, 8, true, true, 2, 1>(out); return 0; }
-        if (ev && strcmp(ev, "256x4s1m2") == 0) { make_variant<256, 4, true, true, 1, 2>(out); return 0; }
-        if (ev && strcmp(ev, "256x4s1m3") == 0) { make_variant<256, 4, true, true, 1, 3>(out); return 0; }
-    }
+// EAGER-MAP kernel (bocd_kernel.cuh), one-unit and persistent, per truncation mode.
+// (Shapes measured slower for R = 1024 and removed: 128x8 with 3-4 series per CTA, 64x16
+// (J = 16: > 168 registers), 256x4.)
+int select_variant(int R, int mode, Variant* out) {
     switch (R) {
-        case 256: make_variant<32, 8, true, true, 8, 2>(out); return 0;
-        case 512: make_variant<64, 8, true, true, 4, 2>(out); return 0;
-        case 1024: make_variant<128, 8, true, true, 2, 2>(out); return 0;
-        case 2048: make_variant<256, 8, true, false, 1, 2>(out); return 0;
-        case 4096: make_variant<512, 8, true, false, 1, 1>(out); return 0;
+        case 256: make_variant<32, 8, true, true, 8, 2>(mode, out); return 0;
+        case 512: make_variant<64, 8, true, true, 4, 2>(mode, out); return 0;
+        case 1024: make_variant<128, 8, true, true, 2, 2>(mode, out); return 0;
+        case 2048: make_variant<256, 8, true, false, 1, 2>(mode, out); return 0;
+        case 4096: make_variant<512, 8, true, false, 1, 1>(mode, out); return 0;
         default: break;
     }
     if (R < 2 || R > 4096) return -1;
-    if (R <= 32) { make_variant<32, 1, false, true, 8, 2>(out); return 0; }
-    if (R <= 256) { make_variant<32, 8, false, true, 8, 2>(out); return 0; }
-    if (R <= 512) { make_variant<64, 8, false, true, 4, 2>(out); return 0; }
-    if (R <= 1024) { make_variant<128, 8, false, true, 2, 2>(out); return 0; }
-    if (R <= 2048) { make_variant<256, 8, false, false, 1, 2>(out); return 0; }
-    make_variant<512, 8, false, false, 1, 1>(out);
+    if (R <= 32) { make_variant<32, 1, false, true, 8, 2>(mode, out); return 0; }
+    if (R <= 256) { make_variant<32, 8, false, true, 8, 2>(mode, out); return 0; }
+    if (R <= 512) { make_variant<64, 8, false, true, 4, 2>(mode, out); return 0; }
+    if (R <= 1024) { make_variant<128, 8, false, true, 2, 2>(mode, out); return 0; }
+    if (R <= 2048) { make_variant<256, 8, false, false, 1, 2>(mode, out); return 0; }
+    make_variant<512, 8, false, false, 1, 1>(mode, out);
     return 0;
 }
 

@@ -124,7 +124,7 @@ __global__ void init_state_kernel(double* mu, double* beta, double* a, const Ser
         const int p = int(k - s * R);
         mu[k] = scal[s].mu0;
         beta[k] = scal[s].beta0;
-        a[k] = (p == 0) ? alpha0 * log2(scal[s].beta0) : -INFINITY;
+        a[k] = (p == 0) ? alpha0 * log2(scal[s].beta0) : fbocd::kImpossible;
     }
 }
 
@@ -217,7 +217,8 @@ __global__ void posterior_kernel(const double* mu, const double* beta, const dou
             const double al = r ? ca[r - 1].y : alpha0;
             double lq = (a[src] + G) - al * log2(beta[src]) - double(sc.dc);
             if (w && p / nt == phi) lq += log2(w[(s0 + i) * nt + p % nt]);
-            logR_out[k] = 0.6931471805599453 * lq + log(omH / sc.zd_prev);
+            // impossible cells carry a = kImpossible (or -inf): log R = -inf
+            logR_out[k] = lq < -262144.0 ? -INFINITY : 0.6931471805599453 * lq + log(omH / sc.zd_prev);
         }
         if (mu_out) mu_out[k] = mu[src];
         if (beta_out) beta_out[k] = beta[src];
@@ -347,7 +348,7 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
     h->cfg = c;
     h->cfg.mu0 = nullptr;
     h->cfg.beta0 = nullptr;
-    if (fbocd::select_variant(c.R, &h->var) != 0) {
+    if (fbocd::select_variant(c.R, c.trunc_mode, &h->var) != 0) {
         delete h;
         return fail(nullptr, FALCON_EINVAL, "no kernel variant for this R");
     }

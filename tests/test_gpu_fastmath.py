@@ -84,9 +84,11 @@ def test_cell_log2_accuracy():
     assert not np.any(bad), list(zip(x[bad][:5], got[bad][:5], ref[bad][:5]))
 
 
-def test_cell_exp2_accuracy_and_cutoff():
+def test_cell_exp2_accuracy_and_floor():
     """The cell loop's exp2 (256-entry table, degree-4 Chebyshev fit): relative error within
-    2.5e-16 on (-1021, 30]; exactly 0 below 2^-1021 and for -inf (impossible cells)."""
+    2.5e-16 on (-1021, 30]; below 2^-1021 (dead cells, and the finite offset -2^20 that
+    impossible cells carry) the result is floored into [2^-1022, 2^-1018): a dead cell then
+    carries < 2^-1010 of a step's evidence."""
     rng = np.random.default_rng(3)
     x = np.concatenate([-rng.exponential(5.0, 200000), rng.uniform(-1020.9, 0, 200000),
                         rng.uniform(0, 30, 20000), np.array([0.0, -0.0, 1e-12, -1e-300, -1020.5])])
@@ -94,5 +96,5 @@ def test_cell_exp2_accuracy_and_cutoff():
     ref = np.exp2(x)
     err = np.abs(got - ref) / ref
     assert np.all(err <= 2.5e-16), float(err.max())
-    dead = _probe(3, np.array([-np.inf, -1021.5, -1e4, -2e6]))
-    assert np.all(dead == 0.0)
+    dead = _probe(3, np.array([-1021.5, -1e4, -2e6, -1048576.0 - 3000.0]))
+    assert np.all(dead >= 2.0 ** -1022) and np.all(dead < 2.0 ** -1018), dead
