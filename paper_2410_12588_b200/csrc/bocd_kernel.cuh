@@ -68,7 +68,7 @@ constexpr int kTile = 256;     // x steps per shared-memory tile (2 KB)
 constexpr int kTileP = 64;     // persistent (streaming) kernels: calls of <= 64 steps
 constexpr int kRebase = 256;   // generic kernels: global steps between frame rebases (ROT: every NT)
 #ifndef FALCON_BOCD_KG
-#define FALCON_BOCD_KG 4
+#define FALCON_BOCD_KG 2
 #endif
 constexpr int kG = FALCON_BOCD_KG;  // cells per interleaved group (ILP)
 #ifndef FALCON_BOCD_STEP_UNROLL
@@ -86,6 +86,9 @@ constexpr double kK0Max = 8192.0;
 #define FALCON_BOCD_FLOOR 1
 #endif
 constexpr bool kFloor = FALCON_BOCD_FLOOR != 0;
+#ifndef FALCON_BOCD_OWNER_SELECT
+#define FALCON_BOCD_OWNER_SELECT 1  // 0: one divergent owner block (measured 0.3% slower)
+#endif
 constexpr double kImpossible = -1048576.0;  // -2^20: 256 |l - Dc| stays below 2^31
 // A MERGE bucket mass below this (floored dead / impossible cells only) is an exact 0, so run
 // lengths longer than the data seen stay impossible.
@@ -768,6 +771,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 // step's critical path), folded into a at the next rotation step.  Generic: one
                 // divergent block for the one or two owner lanes (one shared log2 pass).
                 if constexpr (ROT) {
+#if FALCON_BOCD_OWNER_SELECT
                     const bool ownB = (i == iB);
                     const bool ownA = merge && (i == iB + 1);  // iB = NT-1: thread 0, slot 1 (rotation)
                     const double dcd = double(dc);
@@ -780,6 +784,23 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     be[0] = ownB ? b0 : be[0];
                     a[0] = ownB ? aB : (ownA ? aA : a[0]);
                     wq = ownB ? wB : (ownA ? wA : wq);
+#else
+                    // one short divergent block for the one or two owner lanes (no log: the new
+                    // masses are pending weights), skipped by the other warps of the group
+                    if (unsigned(i - iB) <= (merge ? 1u : 0u)) {  // i == iB (CP) or i == iB + 1 (bucket)
+                        const double dcd = double(dc);
+                        if (i == iB) {
+                            mu[0] = gs.mu0;
+                            be[0] = gs.beta0;
+                            a[0] = gs.aprior + dcd;
+                            wq = P.hr * Z;
+                        } else {  // iB = NT-1: thread 0, slot 1 (rotation block)
+                            const double2 cA = s_ca[R - 2];  // G_{R-1} - alpha_{R-1} lg beta' of cell kA
+                            a[0] = dcd - fma(-cA.y, gs.l0[par][iB + 1], cA.x);
+                            wq = bucket_mass(qA, qB);
+                        }
+                    }
+#endif
                 } else {
                 const bool ownB = (unsigned(kB) % NT) == unsigned(i);
                 const bool ownA = merge && ((unsigned(kA) % NT) == unsigned(i));
