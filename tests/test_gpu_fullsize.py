@@ -4,7 +4,9 @@ outputs the oracle can compute (whole series, all steps) plus size-independent p
 C2: 1,024 series x 10,000 steps (R=512) — 6 sampled series checked step by step.
 C3: 32,768 series x 20,000 steps (R=1024, bench chunking: 1,000-step calls) — 4 sampled
     series checked against the oracle over all 20,000 steps; the event stream of every
-    series is checked for the invariants t >= 1, cp_index <= t, p_new > 0.9.
+    series is checked for the invariants t >= 1, cp_index <= t, p_new > 0.9; and the full
+    C3 length, 100,000 steps (512 series, 2 sampled), where errors carried by the MERGE
+    bucket would show.
 """
 import numpy as np
 import pytest
@@ -46,6 +48,7 @@ def _run_full(cfg, S, T, chunk, sample, mode=0, cap=256, outputs=True):
     ("C2", 1024, 10000, 2500, [0, 1, 511, 777, 1022, 1023], True),
     ("C3", 32768, 20000, 1000, [0, 12345, 20000, 32767], False),  # bench launch configuration
     ("C3", 32768, 6000, 1000, [3, 4097, 32766], True),
+    ("C3", 512, 100000, 1000, [7, 300], True),  # the full C3 length (100,000 steps)
 ])
 def test_full_size_sampled_parity(oracle_mod, cfgname, S, T, chunk, sample, outputs):
     cfg = tracegen.CONFIGS[cfgname]

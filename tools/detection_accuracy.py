@@ -7,6 +7,9 @@ Detectors, per series (a link or a rank; ground truth = the generator's injected
   raw BOCD : any PROB change point (p_new > 0.9, P:770) at t >= 1;
   BOCD+V   : any verified DEGRADE change point paired into a fail-slow event (the 10%
              before/after rule of P:772-779 + pairing, readings V1-V5).
+Change points are PROB events (p_new > 0.9), or PROB + MAP resets.  delay_steps: from the
+first injected onset to the first flag (raw: the event's step; BOCD+V: the step at which the
+verification's after-window is complete), over series flagged at or after their onset.
 SlideWindow (the paper's comparison baseline) is out of scope.
 """
 import json
@@ -17,7 +20,7 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2410_12588_b200 import bocd, detection, tracegen  # noqa: E402
+from paper_2410_12588_b200 import _native as N, bocd, detection, tracegen  # noqa: E402
 
 
 def main():
@@ -40,12 +43,18 @@ def main():
     for label, mask in (("prob", 1), ("prob_mapreset", 3)):
         raw = ev[(ev["flags"] & mask) != 0]
         first_raw = detection.first_flag(raw["series"], raw["t"], S)
-        pairs = bocd.pair_failslow(bocd.verify_changepoints(x, raw, t_lo=0))
-        first_v = detection.first_flag(pairs["series"], pairs["onset"], S)
+        ver = bocd.verify_changepoints(x, raw, t_lo=0)
+        pairs = bocd.pair_failslow(ver)
+        # a verified change point is known once its 20-sample after-window is complete
+        deg = ver[ver["status"] == N.CP_DEGRADE]
+        t_known = np.maximum(deg["t"], deg["cp_index"] + 19)
+        first_v = detection.first_flag(deg["series"], t_known, S)
+        flagged_v = np.zeros(S, dtype=bool)
+        flagged_v[pairs["series"]] = True  # every fail-slow event starts at a verified DEGRADE
         out["bocd_" + label] = {**detection.confusion(first_raw >= 0, truth), "raw_events": int(len(raw)),
-                                "latency_steps": detection.latency(first_raw, onset, truth)}
-        out["bocd_v_" + label] = {**detection.confusion(first_v >= 0, truth), "failslow_events": int(len(pairs)),
-                                  "latency_steps": detection.latency(first_v, onset, truth)}
+                                "delay_steps": detection.latency(first_raw, onset, truth)}
+        out["bocd_v_" + label] = {**detection.confusion(flagged_v, truth), "failslow_events": int(len(pairs)),
+                                  "delay_steps": detection.latency(np.where(flagged_v, first_v, -1), onset, truth)}
     out["note"] = ("synthetic labelled traces (tracegen); detectors: raw BOCD change points (PROB = "
                    "p_new > 0.9, optionally + MAP resets) and the same verified by the 10% rule and "
                    "paired (BOCD+V); the paper's Tables 5-6 are context only")
