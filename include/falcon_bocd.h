@@ -179,8 +179,9 @@ int falcon_bocd_predictive_constants(int32_t R, double kappa0, double alpha0, do
 
 /* Test hook (no handle): out_dev[k] = f(in_dev[k]) for k < n on the device with the
  * kernels' own branch-free transcendentals: which = 0 -> log2, 1 -> exp2 of
- * csrc/fastmath.cuh (per-step scalars); 2 / 3 -> the cell loop's log2 / exp2
- * (csrc/cellmath.cuh).  log2 inputs must be
+ * csrc/fastmath.cuh (per-step scalars); 2 / 3 -> the cell loop's log2 (256 table
+ * intervals) / exp2, 4 -> the cell loop's log2 with 1024 intervals (csrc/cellmath.cuh).
+ * log2 inputs must be
  * positive normal doubles; exp2 inputs <= ~0, -inf allowed (fastmath: arguments below
  * -1021 are clamped; cell loop: 2^d below 2^-1021 is exactly 0).  Synchronises `stream`. */
 int falcon_bocd_debug_fastmath(int32_t which, const double *in_dev, double *out_dev, int64_t n,

@@ -121,6 +121,7 @@ struct KParams {
     int64_t S;
     double H, omH, hr, theta, alpha0, prior_cov;  // omH = 1-H, hr = H/(1-H)
     double ln_omH;                                // log(1-H)
+    double c_bucket, alpha_bucket;                // c_{R-1}/ln2 and alpha_{R-1} (MERGE bucket, FULL)
     int mode;                                     // 0 MERGE, 1 DROP
     int prior_first_obs;
     uint32_t ev_mask;
@@ -334,8 +335,11 @@ constexpr unsigned kFmBase = 0x800u;
 __host__ __device__ constexpr int cell_ec(bool full, int r_full, bool pref) {
     return pref ? 4 : ((full && r_full <= 1024) ? 16 : 8);
 }
-__host__ __device__ constexpr unsigned bocd_fm_bytes(int ec) {
-    return (ec == 16 ? cell_tables_end<16>() : ec == 8 ? cell_tables_end<8>() : cell_tables_end<4>()) - kDynBase;
+__host__ __device__ constexpr unsigned bocd_fm_bytes(int ec, int lb) {
+    return (lb == 8 ? (ec == 16 ? cell_tables_end<16, 8>() : ec == 8 ? cell_tables_end<8, 8>() : cell_tables_end<4, 8>())
+                    : (ec == 16 ? cell_tables_end<16, 10>() : ec == 8 ? cell_tables_end<8, 10>()
+                                                                       : cell_tables_end<4, 10>())) -
+           kDynBase;
 }
 static_assert(kFmBase + kFmSmemBytes - 2048u <= kCellExpBase, "fast-math tables overlap the cell tables");
 
@@ -380,9 +384,15 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr bool ROT = FULL;
     constexpr int EC = cell_ec(FULL, NT * J, PREF);
+    constexpr int LB = cell_logbits(FULL, NT * J);
+    // the MERGE bucket's multiplicative continuation (below) for R >= 2048, where the log-joint's
+    // larger terms (alpha to 2048, frames of up to 512 steps) would carry ~1e-12 per step of
+    // rounding along the bucket's chain (6.3e-10 measured at R = 2048 after 5,120 steps); at
+    // R <= 1024 the plain form measures 6.2e-11 after the full 100,000 C3 steps
+    constexpr bool BUCKET_PRED = FULL && NT * J >= 2048 && MODE == 0;
     // FULL: absolute shared addresses of the per-r tables (the dynamic window starts at
     // kDynBase, checked at entry with the fast-math tables)
-    constexpr unsigned kCaBase = kDynBase + bocd_fm_bytes(EC);
+    constexpr unsigned kCaBase = kDynBase + bocd_fm_bytes(EC, LB);
     constexpr unsigned kYBase = kCaBase + unsigned(NT * J + NT) * 16u;
     constexpr int TILE = PREF ? kTileP : kTile;
     using GS = GroupSmem<NT, TILE>;
@@ -390,9 +400,9 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     const int RT = table_entries<NT, J, FULL, TAB2>(R);
     // dynamic shared memory: [fast-math tables, cell tables (bocd_fm_bytes)][per-r tables][groups]
     unsigned char* const smem = smem_raw;
-    double2* s_ca = reinterpret_cast<double2*>(smem + bocd_fm_bytes(EC));
+    double2* s_ca = reinterpret_cast<double2*>(smem + bocd_fm_bytes(EC, LB));
     double* s_y = reinterpret_cast<double*>(s_ca + RT);
-    unsigned char* gbase = smem + bocd_fm_bytes(EC) + table_bytes(RT);
+    unsigned char* gbase = smem + bocd_fm_bytes(EC, LB) + table_bytes(RT);
 
     for (int k = threadIdx.x; k < RT; k += blockDim.x) {
         const int r = k < R ? k : k - R;
@@ -404,7 +414,8 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         double* ex = reinterpret_cast<double*>(smem_raw + (kCellExpBase - kDynBase));
         for (int k = threadIdx.x; k < kCellExpTab * EC; k += blockDim.x) ex[k] = P.ct->exptab[k / EC];
         double2* lg = reinterpret_cast<double2*>(smem_raw + (cell_log_base<EC>() - kDynBase));
-        for (int k = threadIdx.x; k < (1 << kCellLB); k += blockDim.x) lg[k] = P.ct->logtab[k];
+        const double2* src = LB == 8 ? P.ct->log8 : P.ct->log10;
+        for (int k = threadIdx.x; k < (1 << LB); k += blockDim.x) lg[k] = src[k];
     }
     const unsigned lb = 8u * (threadIdx.x & unsigned(EC - 1));  // exp2 table copy of this lane
     const int g = threadIdx.x / NT;
@@ -458,6 +469,13 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         // ROT: pending weight of slot 0 (the mass of a new change-point / bucket cell, kept as a
         // factor of its q' until the next rotation step folds it into a)
         double wq = 1.0;
+        // BUCKET_PRED: lg beta of slot 0 at the previous step.  The cell that truncation at R
+        // recycles (r = R-1, slot 0 of thread iB) is the MERGE bucket; its mass is continued
+        // multiplicatively by its Student-t predictive,
+        // q' = w 2^(c_{R-1}/ln2 + alpha_{R-1} (lg beta - lg beta') - lg beta'/2 - N_t), whose
+        // terms are O(10): the log-joint's O(10^3..10^4) terms would carry their rounding
+        // (~1e-12 per step) along the bucket's chain of merged masses.
+        double L0p = 0.0;
         const int64_t sbase = s * int64_t(R);
         if constexpr (PREF) {
             if (P.t0 > 0) {
@@ -530,6 +548,10 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         }
         if constexpr (ROT) {
             if (P.t0 > 0) wq = P.st_w[s * NT + i];
+            // before x_0 the cell that step 0 truncates (thread iB's slot 0) is impossible: its
+            // continuation weight is 0 (later steps: the bucket the previous step formed)
+            else if (BUCKET_PRED && i == iB) wq = 0.0;
+            if (BUCKET_PRED) L0p = cell_log2<EC, LB>(be[0]);  // = the previous step's lg beta' of slot 0
         }
         if constexpr (PREF) {
             // pf is free once every thread of the group has read it: prefetch the next unit
@@ -584,6 +606,8 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 // exp2 rounding constant 1.5*2^52 + 2^31 - 256 Dc_t: zf = fma(l, 256, C7) holds
                 // round(256 l) - 256 Dc_t + 2^31 in its low word (exact integers below 2^52)
                 const double C7 = __hiloint2double(0x43380000, int(0x80000000u - unsigned(dc) * 256u));
+                // the bucket's continuation is relative to the previous step's frame: shift N_t only
+                const double C7b = __hiloint2double(0x43380000, int(0x80000000u - unsigned(K0 + zexp) * 256u));
                 // ---- A1-A4 for the J cells (groups of G, every stage across the group) ----
                 // table index of slot j: ib - NT*j  (= r or r + R).  FULL: r of slot j is
                 // (pB - 1 - p) mod R = (iB - 1 - i - NT j) mod R.
@@ -644,7 +668,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
 #pragma unroll
                     for (int kk = 0; kk < G; ++kk) {
                         tb[kk] = unsigned(__double2hiint(bn[kk]));
-                        lt[kk] = cell_log_entry<EC>(tb[kk]);
+                        lt[kk] = cell_log_entry<EC, LB>(tb[kk]);
                     }
 #pragma unroll
                     for (int kk = 0; kk < G; ++kk) {
@@ -655,9 +679,9 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                         kt[kk] = (__hiloint2double(0x43300000, int(tb[kk] >> 20)) - 4503599627371519.0) + lt[kk].y;
                     }
                     {
-                        constexpr int o = 3 * (kCellLB - 8);
+                        constexpr int o = 3 * (LB - 8);
 #pragma unroll
-                        for (int kk = 0; kk < G; ++kk) pl[kk] = fma(rl[kk], kCellLogP3, c_cell[o + 2]);
+                        for (int kk = 0; kk < G; ++kk) pl[kk] = fma(rl[kk], kCellLogP3<LB>, c_cell[o + 2]);
 #pragma unroll
                         for (int kk = 0; kk < G; ++kk) pl[kk] = fma(pl[kk], rl[kk], c_cell[o + 1]);
 #pragma unroll
@@ -669,6 +693,13 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                         const int j = j0 + kk;
                         const double Ln = fma(rl[kk], pl[kk], kt[kk]);
                         ell[kk] = fma(-ca[kk].y, Ln, a[j] + ca[kk].x);
+                        if constexpr (BUCKET_PRED) {
+                            if (j == 0) {  // the truncated cell (thread iB): the bucket's continuation
+                                const double lb_ = fma(P.alpha_bucket, L0p - Ln, fma(-0.5, Ln, P.c_bucket));
+                                ell[kk] = (i == iB) ? lb_ : ell[kk];
+                                L0p = Ln;
+                            }
+                        }
                         if constexpr (ROT) {  // lg beta' of slot 0 (and slot 1 of thread 0) for the bucket
                             if (j == 0) gs.l0[par][i] = Ln;
                             if (J > 1 && j == 1 && i == 0) gs.l0[par][NT] = Ln;
@@ -681,9 +712,10 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     unsigned ki[G];
 #pragma unroll
                     for (int kk = 0; kk < G; ++kk) {
-                        const double zf = fma(ell[kk], 256.0, C7);
+                        const double Cj = (BUCKET_PRED && j0 + kk == 0 && i == iB) ? C7b : C7;
+                        const double zf = fma(ell[kk], 256.0, Cj);
                         ki[kk] = unsigned(__double2loint(zf));
-                        re[kk] = fma(zf - C7, -0.00390625, ell[kk]);  // exact, |re| <= 2^-9
+                        re[kk] = fma(zf - Cj, -0.00390625, ell[kk]);  // exact, |re| <= 2^-9
                         Tv[kk] = cell_exp_entry<EC>(ki[kk], lb);
                     }
 #pragma unroll
@@ -854,7 +886,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                                         aj = (jj == j) ? a[jj] : aj;
                                     }
                                     const double2 c2 = s_ca[id];
-                                    const double Ln = cell_log2<EC>(bj);
+                                    const double Ln = cell_log2<EC, LB>(bj);
                                     double E = cell_exp2<EC>(fma(-c2.y, Ln, aj + c2.x), C7, lb);
                                     if (ROT && j == 0) E *= wq;
                                     const unsigned long long kq = argmax_key(E, r);
@@ -944,6 +976,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 mu[J - 1] = m0;
                 be[J - 1] = b0;
                 a[J - 1] = a0;
+                if (BUCKET_PRED) L0p = cell_log2<EC, LB>(be[0]);  // slot 0 is a new cell
                 iB = 0;
             }
             }

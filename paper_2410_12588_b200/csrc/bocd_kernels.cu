@@ -63,7 +63,8 @@ size_t variant_smem(const Variant& v, int R, bool persistent) {
     const bool pref = persistent && v.pref;  // only the persistent kernels carry the prefetch buffer
     const size_t grp = (pref ? v.group_smem_p : v.group_smem) +
                        (pref ? ((3 * size_t(R) * sizeof(double) + sizeof(SeriesScalars) + 15) & ~size_t(15)) : 0);
-    return bocd_fm_bytes(cell_ec(v.full, v.nt * v.j, pref)) + table_bytes(rows) + size_t(v.spb) * grp;
+    return bocd_fm_bytes(cell_ec(v.full, v.nt * v.j, pref), cell_logbits(v.full, v.nt * v.j)) + table_bytes(rows) +
+           size_t(v.spb) * grp;
 }
 
 // Test hook: elementwise fast_log2 / fast_exp2 (which 0 / 1) and the cell loop's cell_log2 /
@@ -76,7 +77,8 @@ __global__ void fastmath_probe_kernel(int which, const double* in, double* out, 
     double* ex = reinterpret_cast<double*>(dyn + (kCellExpBase - kDynBase));
     for (int k = threadIdx.x; k < kCellExpTab * 16; k += blockDim.x) ex[k] = ct->exptab[k >> 4];
     double2* lg = reinterpret_cast<double2*>(dyn + (cell_log_base<16>() - kDynBase));
-    for (int k = threadIdx.x; k < (1 << kCellLB); k += blockDim.x) lg[k] = ct->logtab[k];
+    const double2* src = which == 4 ? ct->log10 : ct->log8;
+    for (int k = threadIdx.x; k < (which == 4 ? 1024 : 256); k += blockDim.x) lg[k] = src[k];
     __syncthreads();
     const double C7 = __hiloint2double(0x43380000, int(0x80000000u));  // Dc = 0
     const unsigned lbe = 8u * (threadIdx.x & 15u);
@@ -85,7 +87,8 @@ __global__ void fastmath_probe_kernel(int which, const double* in, double* out, 
         switch (which) {
             case 0: v = fast_log2(in[k], fmb); break;
             case 1: v = fast_exp2(in[k], fmb); break;
-            case 2: v = cell_log2<16>(in[k]); break;
+            case 2: v = cell_log2<16, 8>(in[k]); break;
+            case 4: v = cell_log2<16, 10>(in[k]); break;
             default: v = cell_exp2<16>(in[k], C7, lbe); break;
         }
         out[k] = at_base ? v : __longlong_as_double(0x7FF8000000000000ll);  // NaN: layout check failed
@@ -97,7 +100,7 @@ int launch_fastmath_probe(int which, const double* in, double* out, int64_t n, c
     int64_t blocks = (n + 255) / 256;
     if (blocks > 4096) blocks = 4096;
     if (blocks < 1) blocks = 1;
-    const size_t smem = bocd_fm_bytes(16);
+    const size_t smem = bocd_fm_bytes(16, 10);
     if (cudaFuncSetAttribute(fastmath_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
         cudaSuccess)
         return -1;

@@ -31,6 +31,7 @@ struct falcon_bocd_s {
     size_t smem_p = 0;  // of the persistent kernels (+ the state prefetch buffers)
     int64_t grid_cap = 0;  // co-resident CTAs (persistent grid)
     int64_t t = 0;  // observations absorbed
+    double c_bucket = 0.0;  // c_{R-1} / ln2 (the MERGE bucket's predictive constant)
     double2* d_ca = nullptr;
     double* d_y = nullptr;
     fbocd::FastMathTables* d_fm = nullptr;
@@ -407,6 +408,7 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
             const long double kap = (long double)c.kappa0 + r;
             const long double cr = D - 0.5L * logl(two_pi * (kap + 1.0L) / kap);
             G += cr * inv_ln2;
+            if (r == R - 1) h->c_bucket = (double)(cr * inv_ln2);
             ca[r] = make_double2((double)G, (double)((long double)c.alpha0 + 0.5L * (r + 1)));
             D = logl((long double)c.alpha0 + 0.5L * r) - D;
         }
@@ -481,6 +483,8 @@ static int launch_update(falcon_bocd_t h, const double* x_dev, int64_t ld, int64
         P.H = c.hazard;
         P.omH = 1.0 - c.hazard;
         P.ln_omH = log1p(-c.hazard);
+        P.c_bucket = h->c_bucket;
+        P.alpha_bucket = c.alpha0 + 0.5 * (c.R - 1);
         P.hr = (double)((long double)c.hazard / (1.0L - (long double)c.hazard));
         P.theta = c.threshold;
         P.alpha0 = c.alpha0;
@@ -761,7 +765,7 @@ int falcon_bocd_destroy(falcon_bocd_t h) {
 const char* falcon_bocd_last_error(falcon_bocd_t h) { return h ? h->err.c_str() : g_create_err.c_str(); }
 
 int falcon_bocd_debug_fastmath(int32_t which, const double* in_dev, double* out_dev, int64_t n, void* stream) {
-    if (which < 0 || which > 3 || n < 0 || (n > 0 && (!in_dev || !out_dev))) return FALCON_EINVAL;
+    if (which < 0 || which > 4 || n < 0 || (n > 0 && (!in_dev || !out_dev))) return FALCON_EINVAL;
     if (n == 0) return FALCON_OK;
     fbocd::FastMathTables fmt;
     fbocd::fill_fastmath_tables(&fmt);

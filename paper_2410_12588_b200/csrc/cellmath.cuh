@@ -9,7 +9,7 @@
 //              top LB mantissa bits; {invc_i, l_i = -log2(invc_i)} from the table;
 //              r = z invc_i - 1 (one FMA, |r| <= 2^-(LB+1)); log2 b = k + l_i + r P(r),
 //              P the degree-3 Chebyshev interpolant of log2(1+r)/r: max |error| of r P(r)
-//              1.0e-15 (LB = 8), 3.2e-17 (LB = 9), 9.9e-19 (LB = 10).  7 FP64 ops.
+//              1.0e-15 (LB = 8), 9.9e-19 (LB = 10).  7 FP64 ops.
 //   cell_exp2: d = (256 k + j)/256 + r exactly (|r| <= 2^-9), 2^d = 2^k T_j (1 + r Q(r)),
 //              T_j = 2^(j/256) from a 256-entry table, Q the degree-3 Chebyshev interpolant
 //              of (2^r - 1)/r (max |error| of r Q(r) 4.8e-18).  8 FP64 ops.
@@ -30,16 +30,16 @@
 
 namespace fbocd {
 
-#ifndef FALCON_BOCD_LOGBITS
-#define FALCON_BOCD_LOGBITS 8
-#endif
-constexpr int kCellLB = FALCON_BOCD_LOGBITS;  // log2 table bits (8, 9 or 10)
-static_assert(kCellLB >= 8 && kCellLB <= 10, "FALCON_BOCD_LOGBITS: 8, 9 or 10");
+// log2 table bits: 8 for the R <= 1024 FULL kernels (speed), 10 for the others: there alpha
+// reaches 1024-2048 and the log's error, carried along the MERGE bucket's chain of merged
+// masses, would approach the parity budget (measured 6.2e-10 at R = 2048 with LB = 8).
+__host__ __device__ constexpr int cell_logbits(bool full, int r_full) { return (full && r_full <= 1024) ? 8 : 10; }
 constexpr int kCellExpTab = 256;
 
 struct CellTables {
-    double exptab[kCellExpTab];       // 2^(j/256), high word minus (j << 12)
-    double2 logtab[1 << kCellLB];     // {invc_i, -log2(invc_i)}, z in [1 + i/2^LB, 1 + (i+1)/2^LB)
+    double exptab[kCellExpTab];  // 2^(j/256), high word minus (j << 12)
+    double2 log8[256];           // {invc_i, -log2(invc_i)}, z in [1 + i/2^LB, 1 + (i+1)/2^LB)
+    double2 log10[1024];
 };
 
 inline void fill_cell_tables(CellTables* t) {
@@ -50,13 +50,16 @@ inline void fill_cell_tables(CellTables* t) {
         b -= uint64_t(uint32_t(j) << 12) << 32;  // n * 2^12 + hi(T'_j) = (k << 20) + hi(T_j)
         std::memcpy(&t->exptab[j], &b, sizeof(b));
     }
-    const int n = 1 << kCellLB;
-    for (int i = 0; i < n; ++i) {
-        const long double c = 1.0L + ((long double)i + 0.5L) / (long double)n;
-        const double invc = (double)(1.0L / c);
-        t->logtab[i].x = invc;
-        t->logtab[i].y = (double)(-log2l((long double)invc));
-    }
+    auto fill_log = [](double2* tab, int n) {
+        for (int i = 0; i < n; ++i) {
+            const long double c = 1.0L + ((long double)i + 0.5L) / (long double)n;
+            const double invc = (double)(1.0L / c);
+            tab[i].x = invc;
+            tab[i].y = (double)(-log2l((long double)invc));
+        }
+    };
+    fill_log(t->log8, 256);
+    fill_log(t->log10, 1024);
 }
 
 // Polynomial coefficients (constant bank; uploaded with the fast-math constants): P0..P2 of
@@ -69,34 +72,35 @@ static const double kCellConstants[12] = {
     0.6931471805599428, 0.24022650695910044, 0.05550411375117056};  // exp
 // leading coefficients rounded to 20 mantissa bits (DFMA immediates; the rounding is weighted
 // by r^4 <= 2^-36, i.e. below 1e-18)
-constexpr double kCellLogP3 = kCellLB == 8 ? -0.3606746196746826 : -0.3606739044189453;
+template <int LB>
+constexpr double kCellLogP3 = LB == 8 ? -0.3606746196746826 : -0.3606739044189453;
 constexpr double kCellExpQ3 = 0.009618133306503296;  // 0.009618129695226546
 
 constexpr unsigned kCellExpBase = 0x1A00u;
 template <int EC>
 __host__ __device__ constexpr unsigned cell_log_base() { return kCellExpBase + kCellExpTab * EC * 8u; }
-template <int EC>
-__host__ __device__ constexpr unsigned cell_tables_end() { return cell_log_base<EC>() + (16u << kCellLB); }
+template <int EC, int LB>
+__host__ __device__ constexpr unsigned cell_tables_end() { return cell_log_base<EC>() + (16u << LB); }
 
 // log2 table entry of b, tb = hi(b)
-template <int EC>
+template <int EC, int LB>
 __device__ __forceinline__ double2 cell_log_entry(unsigned tb) {
     double2 v;
     asm("ld.shared.v2.f64 {%0, %1}, [%2+%3];"
         : "=d"(v.x), "=d"(v.y)
-        : "r"((tb >> (16 - kCellLB)) & (((1u << kCellLB) - 1u) << 4)), "n"(cell_log_base<EC>()));
+        : "r"((tb >> (16 - LB)) & (((1u << LB) - 1u) << 4)), "n"(cell_log_base<EC>()));
     return v;
 }
 
-template <int EC>
+template <int EC, int LB>
 __device__ __forceinline__ double cell_log2(double b) {
     const unsigned tb = unsigned(__double2hiint(b));
-    const double2 t = cell_log_entry<EC>(tb);
+    const double2 t = cell_log_entry<EC, LB>(tb);
     const double invs = __hiloint2double(__double2hiint(t.x) + 0x3FF00000 - int(tb & 0x7FF00000u), __double2loint(t.x));
     const double r = fma(b, invs, -1.0);
     const double kt = (__hiloint2double(0x43300000, int(tb >> 20)) - 4503599627371519.0) + t.y;  // k + l_i
-    constexpr int o = 3 * (kCellLB - 8);
-    double p = fma(r, kCellLogP3, c_cell[o + 2]);
+    constexpr int o = 3 * (LB - 8);
+    double p = fma(r, kCellLogP3<LB>, c_cell[o + 2]);
     p = fma(p, r, c_cell[o + 1]);
     p = fma(p, r, c_cell[o]);
     return fma(r, p, kt);

@@ -126,17 +126,18 @@ def test_generic_R_parity(oracle_mod, R):
         _full_check(g, res, mask=3, name=f"C3[3:9,:1500] R={R} mode={mode}")
 
 
-@pytest.mark.parametrize("R", [2048, 4096])
-def test_large_R_parity(oracle_mod, R):
+@pytest.mark.parametrize("R,span", [(2048, 2.5), (4096, 2.5), (2048, 10)])
+def test_large_R_parity(oracle_mod, R, span):
     """The FULL kernels for R = 2048 (256 threads per series) and R = 4096 (C4: 512 threads,
-    one series per CTA), past R steps so that truncation, rotation and the rebase all run."""
+    one series per CTA), past R steps so that truncation, rotation and the rebase all run;
+    10 R steps: a long chain of MERGE bucket merges (its multiplicative continuation)."""
     cfg = tracegen.CONFIGS["C4"]
-    x = tracegen.generate(tracegen.make_spec(cfg, n_series=64), 5, 3, 0, int(2.5 * R))
-    for mode in (0, 1):
+    x = tracegen.generate(tracegen.make_spec(cfg, n_series=64), 5, 3, 0, int(span * R))
+    for mode in ((0, 1) if span < 5 else (0,)):
         g = _run_gpu(x, R, cfg.hazard, mode, prior_cov=cfg.prior_cov, ev_mask=3, cap=4096)
         res = _oracle(oracle_mod, x, R, cfg.hazard, mode, prior_cov=cfg.prior_cov)
         assert not g["dropped"]
-        _full_check(g, res, mask=3, name=f"C4-recipe[5:8,:{int(2.5 * R)}] R={R} mode={mode}")
+        _full_check(g, res, mask=3, name=f"C4-recipe[5:8,:{int(span * R)}] R={R} mode={mode}")
 
 
 def test_chunk_split_bit_exact():
