@@ -140,11 +140,15 @@ def test_large_R_parity(oracle_mod, R, span):
         _full_check(g, res, mask=3, name=f"C4-recipe[5:8,:{int(span * R)}] R={R} mode={mode}")
 
 
-def test_chunk_split_bit_exact():
+@pytest.mark.parametrize("R,T,chunks", [(1024, 1300, [1, 255, 257, 3, 512, 1, 271]),
+                                         (2048, 2600, [1, 700, 1, 2, 1300, 64, 532])])
+def test_chunk_split_bit_exact(R, T, chunks):
+    """Any split into calls (1-step calls run the persistent kernels) gives bit-identical
+    results; R = 2048 also covers the MERGE bucket's multiplicative continuation."""
     cfg = tracegen.CONFIGS["C3"]
-    x = tracegen.generate(tracegen.make_spec(cfg), 0, 8, 0, 1300)
-    a = _run_gpu(x, 1024, cfg.hazard, 0, prior_cov=0.3, ev_mask=3)
-    b = _run_gpu(x, 1024, cfg.hazard, 0, prior_cov=0.3, ev_mask=3, chunks=[1, 255, 257, 3, 512, 1, 271])
+    x = tracegen.generate(tracegen.make_spec(cfg), 0, 8, 0, T)
+    a = _run_gpu(x, R, cfg.hazard, 0, prior_cov=0.3, ev_mask=3)
+    b = _run_gpu(x, R, cfg.hazard, 0, prior_cov=0.3, ev_mask=3, chunks=chunks)
     for k in ("map", "pnew", "logz", "logR", "mu", "beta"):
         assert np.array_equal(a[k], b[k], equal_nan=True), k
     assert np.array_equal(a["events"], b["events"])
