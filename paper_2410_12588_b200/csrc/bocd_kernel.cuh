@@ -86,6 +86,9 @@ constexpr double kK0Max = 8192.0;
 #define FALCON_BOCD_FLOOR 1
 #endif
 constexpr bool kFloor = FALCON_BOCD_FLOOR != 0;
+#ifndef FALCON_BOCD_KT_I2F
+#define FALCON_BOCD_KT_I2F 1  // k via I2F.F64 (0: the 2^52 magic; 0.8% slower, same bits)
+#endif
 #ifndef FALCON_BOCD_OWNER_SELECT
 #define FALCON_BOCD_OWNER_SELECT 1  // 0: one divergent owner block (measured 0.3% slower)
 #endif
@@ -676,7 +679,11 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                                                                  int(tb[kk] & 0x7FF00000u),
                                                              __double2loint(lt[kk].x));
                         rl[kk] = fma(bn[kk], invs, -1.0);
+#if FALCON_BOCD_KT_I2F
+                        kt[kk] = __int2double_rn(int(tb[kk] >> 20) - 1023) + lt[kk].y;
+#else
                         kt[kk] = (__hiloint2double(0x43300000, int(tb[kk] >> 20)) - 4503599627371519.0) + lt[kk].y;
+#endif
                     }
                     {
                         constexpr int o = 3 * (LB - 8);

@@ -98,7 +98,7 @@ __device__ __forceinline__ double cell_log2(double b) {
     const double2 t = cell_log_entry<EC, LB>(tb);
     const double invs = __hiloint2double(__double2hiint(t.x) + 0x3FF00000 - int(tb & 0x7FF00000u), __double2loint(t.x));
     const double r = fma(b, invs, -1.0);
-    const double kt = (__hiloint2double(0x43300000, int(tb >> 20)) - 4503599627371519.0) + t.y;  // k + l_i
+    const double kt = __int2double_rn(int(tb >> 20) - 1023) + t.y;  // k + l_i (k exact)
     constexpr int o = 3 * (LB - 8);
     double p = fma(r, kCellLogP3<LB>, c_cell[o + 2]);
     p = fma(p, r, c_cell[o + 1]);
