@@ -40,8 +40,9 @@ UNIT = "series*steps/s"
 #   folded into its rounding constant), joint + evidence sum 2  =  26.  It is fixed across
 #   kernel formulations (comparable between rounds).  The current kernel evaluates the same
 #   recursion in the log-joint form (bocd_kernel.cuh: the predictive ratio telescopes into
-#   the NIG marginal likelihood; cellmath.cuh transcendentals) with 21 FP64 instructions per
-#   cell: "frac_executed" reports the fraction on that basis.  Per-step work (group reduction, scalar tail, the tile's prior
+#   the NIG marginal likelihood; cellmath.cuh transcendentals) with 21 FP64-pipe
+#   instructions (20 DFMA/DADD/DMUL + one I2F.F64) per cell: "frac_executed" reports the
+#   fraction on that basis.  Per-step work (group reduction, scalar tail, the tile's prior
 #   references) is counted in neither.  For context the textbook cell with libdevice log/exp
 #   (30 + 18 FP64 instructions, cuobjdump, P0) is 60.
 FP64_INSTR_PER_CELL = 26
