@@ -96,3 +96,21 @@ def test_predictive_constants_within_1ulp(L, R, kappa0, alpha0):
         for got, ref in ((c[r], cr), (a[r], alp), (g[r], kap / (2 * (kap + 1))), (k1[r], 1 / (kap + 1))):
             ref = float(ref)
             assert abs(got - ref) <= math.ulp(ref), (r, got, ref)
+
+
+@pytest.mark.parametrize("R,kappa0,alpha0", [(4096, 1.0, 1.0), (1024, 0.37, 2.25)])
+def test_predictive_constants_telescope_to_the_marginal(L, R, kappa0, alpha0):
+    """The log-joint kernel (bocd_kernel.cuh) uses G_n = sum_{r<n} c_r: the product of the
+    Student-t predictives' constants telescopes into the NIG marginal likelihood's constant
+    lnGamma(alpha_n) - lnGamma(alpha0) + 1/2 ln(kappa0/kappa_n) - n/2 ln(2 pi) (closed form,
+    50-digit mpmath)."""
+    out = [np.empty(R) for _ in range(4)]
+    assert L.falcon_bocd_predictive_constants(R, kappa0, alpha0, *[o.ctypes.data for o in out]) == 0
+    c = out[0]
+    G = np.cumsum(c)  # G[n-1] = sum_{r<n} c_r
+    mpmath.mp.dps = 50
+    for n in (1, 2, 3, 17, R // 2, R - 1, R):
+        al = mpmath.mpf(alpha0) + mpmath.mpf(n) / 2
+        ref = (mpmath.loggamma(al) - mpmath.loggamma(mpmath.mpf(alpha0))
+               + mpmath.log(mpmath.mpf(kappa0) / (kappa0 + n)) / 2 - n * mpmath.log(2 * mpmath.pi) / 2)
+        assert abs(G[n - 1] - float(ref)) <= 1e-12 * max(1.0, abs(float(ref))), (n, G[n - 1], float(ref))
