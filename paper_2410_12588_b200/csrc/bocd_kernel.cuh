@@ -77,7 +77,7 @@ constexpr int kG = FALCON_BOCD_KG;  // cells per interleaved group (ILP)
 constexpr int kStepUnroll = FALCON_BOCD_STEP_UNROLL;  // steps per unrolled loop body
 // K0_t = round(l0_t) is clamped to +-kK0Max so that |N_t| < 2^14 and 256 Dc stays below 2^31
 // (at most 512 steps between rebases)
-constexpr double kK0Max = 8192.0;
+constexpr double kK0Max = FALCON_BOCD_EXPBITS == 9 ? 4096.0 : 8192.0;
 // FLOOR (default): a cell's joint below 2^-1021 of the step reference is floored to
 // [2^-1021, 2^-1019) by a two-sided integer clamp (no select per cell), and impossible cells
 // (run lengths longer than the data seen) carry the finite offset kImpossible instead of
@@ -336,12 +336,13 @@ constexpr unsigned kFmBase = 0x800u;
 // The persistent prefetching kernels (HBM-bound streaming) take 4 copies and 64-step x tiles
 // so that two CTAs with their prefetch buffers still fit one SM.
 __host__ __device__ constexpr int cell_ec(bool full, int r_full, bool pref) {
-    return pref ? 4 : ((full && r_full <= 1024) ? 16 : 8);
+    return (pref ? 4 : ((full && r_full <= 1024) ? 16 : 8)) >> (kCellEB - 8);
 }
 __host__ __device__ constexpr unsigned bocd_fm_bytes(int ec, int lb) {
-    return (lb == 8 ? (ec == 16 ? cell_tables_end<16, 8>() : ec == 8 ? cell_tables_end<8, 8>() : cell_tables_end<4, 8>())
+    return (lb == 8 ? (ec == 16 ? cell_tables_end<16, 8>() : ec == 8 ? cell_tables_end<8, 8>()
+                                   : ec == 4 ? cell_tables_end<4, 8>() : cell_tables_end<2, 8>())
                     : (ec == 16 ? cell_tables_end<16, 10>() : ec == 8 ? cell_tables_end<8, 10>()
-                                                                       : cell_tables_end<4, 10>())) -
+                                   : ec == 4 ? cell_tables_end<4, 10>() : cell_tables_end<2, 10>())) -
            kDynBase;
 }
 static_assert(kFmBase + kFmSmemBytes - 2048u <= kCellExpBase, "fast-math tables overlap the cell tables");
@@ -354,18 +355,23 @@ static_assert(kFmBase + kFmSmemBytes - 2048u <= kCellExpBase, "fast-math tables 
 // agree bit for bit.
 template <int EC>
 __device__ __forceinline__ double cell_exp2(double ell, double C7, unsigned lbe) {
-    const double zf = fma(ell, 256.0, C7);
+    const double zf = fma(ell, kCellExpScale, C7);
     const unsigned ki = unsigned(__double2loint(zf));
-    const double re = fma(zf - C7, -0.00390625, ell);
+    const double re = fma(zf - C7, -1.0 / kCellExpScale, ell);
     const double T = cell_exp_entry<EC>(ki, lbe);
-    double p = fma(re, kCellExpQ3, c_cell[11]);
-    p = fma(p, re, c_cell[10]);
-    p = fma(p, re, c_cell[9]);
+    double p;
+    if constexpr (kCellEB == 8) {
+        p = fma(re, kCellExpQ3, c_cell[11]);
+        p = fma(p, re, c_cell[10]);
+        p = fma(p, re, c_cell[9]);
+    } else {
+        p = fma(re, kCellExpQ2i, c_cell[10]);
+        p = fma(p, re, c_cell[9]);
+    }
     const double qq = p * re;
-    const bool dead = ki < 0x80000000u - 261376u;
-    const unsigned kc = kFloor ? max(min(ki, 0x80000000u + 256255u), 0x80000000u - 261376u)
-                               : min(ki, 0x80000000u + 256255u);
-    const double Ts = __hiloint2double(int(kc * 4096u) + __double2hiint(T), __double2loint(T));
+    const bool dead = ki < kCellExpLo;
+    const unsigned kc = kFloor ? max(min(ki, kCellExpHi), kCellExpLo) : min(ki, kCellExpHi);
+    const double Ts = __hiloint2double(int(kc * (1048576u >> kCellEB)) + __double2hiint(T), __double2loint(T));
     return (!kFloor && dead) ? 0.0 : fma(Ts, qq, Ts);
 }
 
@@ -608,9 +614,9 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 dc += K0 + zexp;  // Dc_t = Dc_{t-1} + N_t
                 // exp2 rounding constant 1.5*2^52 + 2^31 - 256 Dc_t: zf = fma(l, 256, C7) holds
                 // round(256 l) - 256 Dc_t + 2^31 in its low word (exact integers below 2^52)
-                const double C7 = __hiloint2double(0x43380000, int(0x80000000u - unsigned(dc) * 256u));
+                const double C7 = __hiloint2double(0x43380000, int(0x80000000u - unsigned(dc) * unsigned(kCellExpTab)));
                 // the bucket's continuation is relative to the previous step's frame: shift N_t only
-                const double C7b = __hiloint2double(0x43380000, int(0x80000000u - unsigned(K0 + zexp) * 256u));
+                const double C7b = __hiloint2double(0x43380000, int(0x80000000u - unsigned(K0 + zexp) * unsigned(kCellExpTab)));
                 // ---- A1-A4 for the J cells (groups of G, every stage across the group) ----
                 // table index of slot j: ib - NT*j  (= r or r + R).  FULL: r of slot j is
                 // (pB - 1 - p) mod R = (iB - 1 - i - NT j) mod R.
@@ -720,15 +726,18 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
 #pragma unroll
                     for (int kk = 0; kk < G; ++kk) {
                         const double Cj = (BUCKET_PRED && j0 + kk == 0 && i == iB) ? C7b : C7;
-                        const double zf = fma(ell[kk], 256.0, Cj);
+                        const double zf = fma(ell[kk], kCellExpScale, Cj);
                         ki[kk] = unsigned(__double2loint(zf));
-                        re[kk] = fma(zf - Cj, -0.00390625, ell[kk]);  // exact, |re| <= 2^-9
+                        re[kk] = fma(zf - Cj, -1.0 / kCellExpScale, ell[kk]);  // exact, |re| <= 2^-(EB+1)
                         Tv[kk] = cell_exp_entry<EC>(ki[kk], lb);
                     }
 #pragma unroll
-                    for (int kk = 0; kk < G; ++kk) pe[kk] = fma(re[kk], kCellExpQ3, c_cell[11]);
+                    for (int kk = 0; kk < G; ++kk)
+                        pe[kk] = kCellEB == 8 ? fma(re[kk], kCellExpQ3, c_cell[11]) : fma(re[kk], kCellExpQ2i, c_cell[10]);
+                    if constexpr (kCellEB == 8) {
 #pragma unroll
-                    for (int kk = 0; kk < G; ++kk) pe[kk] = fma(pe[kk], re[kk], c_cell[10]);
+                        for (int kk = 0; kk < G; ++kk) pe[kk] = fma(pe[kk], re[kk], c_cell[10]);
+                    }
 #pragma unroll
                     for (int kk = 0; kk < G; ++kk) pe[kk] = fma(pe[kk], re[kk], c_cell[9]);
 #pragma unroll
@@ -738,10 +747,9 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                         const double qq = pe[kk] * re[kk];
                         // 2^e, e = floor(n/256) for n = ki - 2^31: exactly 0 below 2^-1021, e clamped
                         // at +1000; hi word = kc * 2^12 + hi(T'_j) (cellmath.cuh)
-                        const bool dead = ki[kk] < 0x80000000u - 261376u;
-                        const unsigned kc = kFloor ? max(min(ki[kk], 0x80000000u + 256255u), 0x80000000u - 261376u)
-                                                   : min(ki[kk], 0x80000000u + 256255u);
-                        const double Ts = __hiloint2double(int(kc * 4096u) + __double2hiint(Tv[kk]),
+                        const bool dead = ki[kk] < kCellExpLo;
+                        const unsigned kc = kFloor ? max(min(ki[kk], kCellExpHi), kCellExpLo) : min(ki[kk], kCellExpHi);
+                        const double Ts = __hiloint2double(int(kc * (1048576u >> kCellEB)) + __double2hiint(Tv[kk]),
                                                            __double2loint(Tv[kk]));
                         double E = (!kFloor && dead) ? 0.0 : fma(Ts, qq, Ts);
                         if (ROT && j == 0) E *= wq;  // slot 0's pending weight (new CP / bucket mass)

@@ -75,21 +75,22 @@ __global__ void fastmath_probe_kernel(int which, const double* in, double* out, 
     const unsigned fmb = fm_setup(dyn, tab);
     const bool at_base = smem_addr(dyn) == kDynBase && fmb == kFmBase;
     double* ex = reinterpret_cast<double*>(dyn + (kCellExpBase - kDynBase));
-    for (int k = threadIdx.x; k < kCellExpTab * 16; k += blockDim.x) ex[k] = ct->exptab[k >> 4];
-    double2* lg = reinterpret_cast<double2*>(dyn + (cell_log_base<16>() - kDynBase));
+    constexpr int EC = cell_ec(true, 1024, false);
+    for (int k = threadIdx.x; k < kCellExpTab * EC; k += blockDim.x) ex[k] = ct->exptab[k / EC];
+    double2* lg = reinterpret_cast<double2*>(dyn + (cell_log_base<EC>() - kDynBase));
     const double2* src = which == 4 ? ct->log10 : ct->log8;
     for (int k = threadIdx.x; k < (which == 4 ? 1024 : 256); k += blockDim.x) lg[k] = src[k];
     __syncthreads();
     const double C7 = __hiloint2double(0x43380000, int(0x80000000u));  // Dc = 0
-    const unsigned lbe = 8u * (threadIdx.x & 15u);
+    const unsigned lbe = 8u * (threadIdx.x & unsigned(EC - 1));
     for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
         double v;
         switch (which) {
             case 0: v = fast_log2(in[k], fmb); break;
             case 1: v = fast_exp2(in[k], fmb); break;
-            case 2: v = cell_log2<16, 8>(in[k]); break;
-            case 4: v = cell_log2<16, 10>(in[k]); break;
-            default: v = cell_exp2<16>(in[k], C7, lbe); break;
+            case 2: v = cell_log2<EC, 8>(in[k]); break;
+            case 4: v = cell_log2<EC, 10>(in[k]); break;
+            default: v = cell_exp2<EC>(in[k], C7, lbe); break;
         }
         out[k] = at_base ? v : __longlong_as_double(0x7FF8000000000000ll);  // NaN: layout check failed
     }
@@ -100,7 +101,7 @@ int launch_fastmath_probe(int which, const double* in, double* out, int64_t n, c
     int64_t blocks = (n + 255) / 256;
     if (blocks > 4096) blocks = 4096;
     if (blocks < 1) blocks = 1;
-    const size_t smem = bocd_fm_bytes(16, 10);
+    const size_t smem = bocd_fm_bytes(cell_ec(true, 1024, false), 10);
     if (cudaFuncSetAttribute(fastmath_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
         cudaSuccess)
         return -1;
