@@ -262,3 +262,23 @@ def test_repeat_runs_bit_identical():
         for k in ("map", "pnew", "logz", "logR", "mu", "beta"):
             assert np.array_equal(runs[0][k], runs[1][k], equal_nan=True), (chunks[:2], k)
         assert np.array_equal(runs[0]["events"], runs[1]["events"])
+
+
+@pytest.mark.parametrize("R,mode", [(1024, 0), (1024, 1), (2048, 0), (300, 0)])
+def test_lazy_map_equals_eager_map(R, mode):
+    """The on-demand MAP (recomputed q' at event steps, no per-step outputs: the bench's kernel)
+    reports exactly the PROB events of the EAGER kernel (r* reduced every step)."""
+    cfg = tracegen.CONFIGS["C3"]
+    x = tracegen.generate(tracegen.make_spec(cfg), 0, 64, 0, max(2 * R, 1500))
+    xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    evs = []
+    for outputs in (True, False):
+        b = bocd.BocdBatch(64, R=R, hazard=cfg.hazard, prior_first_obs=True, prior_cov=0.3,
+                           trunc_mode=mode, event_mask=1, event_capacity=2048)
+        b.update_chunk(xd, outputs=outputs)
+        ev, dropped = b.changepoints()
+        b.close()
+        assert not dropped
+        evs.append(ev)
+    assert len(evs[0]) > 0
+    assert np.array_equal(evs[0], evs[1])
