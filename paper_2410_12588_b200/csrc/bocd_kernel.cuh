@@ -86,6 +86,9 @@ constexpr double kK0Max = FALCON_BOCD_EXPBITS == 9 ? 4096.0 : 8192.0;
 #define FALCON_BOCD_FLOOR 1
 #endif
 constexpr bool kFloor = FALCON_BOCD_FLOOR != 0;
+#ifndef FALCON_BOCD_PRED_PUBLISH
+#define FALCON_BOCD_PRED_PUBLISH 1  // only the lanes whose published cells the tail reads store them (0.7%)
+#endif
 #ifndef FALCON_BOCD_KT_I2F
 #define FALCON_BOCD_KT_I2F 1  // k via I2F.F64 (0: the 2^52 magic; 0.8% slower, same bits)
 #endif
@@ -714,7 +717,11 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                             }
                         }
                         if constexpr (ROT) {  // lg beta' of slot 0 (and slot 1 of thread 0) for the bucket
+#if FALCON_BOCD_PRED_PUBLISH
+                            if (j == 0 && i == iB + 1) gs.l0[par][i] = Ln;  // only the bucket's is read
+#else
                             if (j == 0) gs.l0[par][i] = Ln;
+#endif
                             if (J > 1 && j == 1 && i == 0) gs.l0[par][NT] = Ln;
                         } else {
                             if (merge && i + NT * j == kA) gs.spec[par][3] = fma(-ca[kk].y, Ln, ca[kk].x);
@@ -763,7 +770,11 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                             }
                             // the tail's cells, published by their owners
                             if constexpr (ROT) {
+#if FALCON_BOCD_PRED_PUBLISH
+                                if (j == 0 && unsigned(i - iB + 1) <= 2u) gs.e0[par][i] = E;  // iB-1 .. iB+1
+#else
                                 if (j == 0) gs.e0[par][i] = E;
+#endif
                                 if (J > 1 && j == 1 && i == 0) gs.e0[par][NT] = E;
                                 if (j == J - 1 && i == NT - 1) gs.e0[par][NT + 1] = E;
                             } else {
