@@ -282,3 +282,18 @@ def test_lazy_map_equals_eager_map(R, mode):
         evs.append(ev)
     assert len(evs[0]) > 0
     assert np.array_equal(evs[0], evs[1])
+
+
+@pytest.mark.parametrize("R,S", [(1024, 5), (256, 13), (512, 7)])
+def test_partial_cta_series_counts(oracle_mod, R, S):
+    """Series counts that leave a CTA's last series groups empty (2, 8 and 4 series per CTA for
+    R = 1024, 256, 512), through a long call and through 1-step (persistent-kernel) calls."""
+    cfg = tracegen.CONFIGS["C3"]
+    x = tracegen.generate(tracegen.make_spec(cfg), 11, S, 0, max(R + 300, 600))
+    T = x.shape[1]
+    a = _run_gpu(x, R, cfg.hazard, 0, prior_cov=0.3, ev_mask=1, cap=256)
+    b = _run_gpu(x, R, cfg.hazard, 0, prior_cov=0.3, ev_mask=1, cap=256, chunks=[1] * 20 + [T - 20])
+    for k in ("map", "pnew", "logz", "logR", "mu", "beta"):
+        assert np.array_equal(a[k], b[k], equal_nan=True), k
+    res = _oracle(oracle_mod, x, R, cfg.hazard, 0, prior_cov=0.3)
+    _full_check(a, res, mask=1, name=f"C3[11:{11 + S},:{T}] R={R} S={S}")
