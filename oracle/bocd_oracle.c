@@ -31,6 +31,10 @@
  * Cauchy special case, chain rule vs closed-form marginal likelihood,
  * brute-force segmentation enumeration (DROP / MERGE / untruncated), the
  * invariants sum R = 1 and R_t(0) = H, and the hand-built step examples.
+ * The O8 decision outputs (p_new, r*, margin, cp_index, PROB) are pinned to their
+ * definitions on the enumerated segmentations (test_decisions_equal_enumeration:
+ * p_new = Pr(x_t opens a segment | x_{0..t}), including an H = 0.3 case where the
+ * 1/(1 - R_t(0)) normalisation is a factor 1.43).
  */
 #include <math.h>
 #include <stdint.h>

@@ -41,8 +41,20 @@ def log_ml(xs, mu0, k0, a0, b0):
             + mpmath.log(k0 / kn) / 2 - n * mpmath.log(2 * mpmath.pi) / 2)
 
 
-def posterior(x, R, H, mu0, k0, a0, b0, mode, dps=40):
-    """Return (logR[t][r] as floats, cumulative log evidence per t) for t = 0..len(x)-1."""
+def posterior(x, R, H, mu0, k0, a0, b0, mode, dps=40, decisions=False):
+    """Return (logR[t][r] as floats, cumulative log evidence per t) for t = 0..len(x)-1.
+
+    decisions=True also returns, per t, the decision quantities of reading Q4/Q5
+    ("likelihood of r_t = 0 ... exceeds 0.9"; P:762-770 MAP run length),
+    each defined directly on the segmentations rather than from the slot values:
+      * p_new_t = Pr(x_t opens a new segment | x_{0..t}, the open segment fits the
+        truncation) = W(last segment has length 1) / W(every admissible pattern whose
+        open segment is a growth slot: length <= R-1 under DROP, any under MERGE), W the
+        summed pattern weights without the change-point factor that follows x_t.  (Slot 1
+        of MERGE with R = 2 is the ">= 1" bucket: then "length 1" means "in slot 1".)
+      * map_t = the growth slot r >= 1 of largest posterior mass (ties -> smaller r) and
+        margin_t = its log mass minus the next largest log mass over r >= 1, r != map_t.
+    """
     mpmath.mp.dps = dps
     xs = [mpmath.mpf(float(v)) for v in x]
     mu0, k0, a0, b0 = (mpmath.mpf(float(v)) for v in (mu0, k0, a0, b0))
@@ -65,9 +77,10 @@ def posterior(x, R, H, mu0, k0, a0, b0, mode, dps=40):
                 cache[key] = log_ml(xs[a:b + 1], mu0, k0, a0, b0)
         return cache[key]
 
-    out, evid = [], []
+    out, evid, dec = [], [], []
     for t in range(n):
         acc = [[] for _ in range(R)]
+        w_new, w_open = [], []
         for bits in itertools.product((0, 1), repeat=t):
             starts = [0] + [k + 1 for k in range(t) if bits[k]]
             ends = starts[1:] + [t + 1]
@@ -82,12 +95,26 @@ def posterior(x, R, H, mu0, k0, a0, b0, mode, dps=40):
                     acc[0].append(lH + lw)
                 if last <= R - 1:
                     acc[last].append(l1H + lw)
+                    w_open.append(lw)
+                    if last == 1:
+                        w_new.append(lw)
             else:
                 acc[0].append(lH + lw)
                 acc[min(last, R - 1)].append(l1H + lw)
+                w_open.append(lw)
+                if min(last, R - 1) == 1:
+                    w_new.append(lw)
         slot = [mpmath.log(mpmath.fsum(mpmath.exp(v) for v in a)) if a else None for a in acc]
         live = [v for v in slot if v is not None]
         tot = mpmath.log(mpmath.fsum(mpmath.exp(v) for v in live))
         out.append([float(v - tot) if v is not None else float("-inf") for v in slot])
         evid.append(float(tot))
-    return out, evid
+        if decisions:
+            lse = lambda a: mpmath.log(mpmath.fsum(mpmath.exp(v) for v in a))
+            p_new = mpmath.exp(lse(w_new) - lse(w_open)) if w_new else mpmath.mpf(0)
+            grow = [(slot[r], r) for r in range(1, R) if slot[r] is not None]
+            best = max(grow, key=lambda vr: (vr[0], -vr[1]))
+            rest = [v for v, r in grow if r != best[1]]
+            margin = best[0] - max(rest) if rest else mpmath.inf
+            dec.append({"p_new": float(p_new), "map": best[1], "margin": float(margin)})
+    return (out, evid, dec) if decisions else (out, evid)
