@@ -1,26 +1,39 @@
 #!/usr/bin/env python
-"""Benchmark: batched BOCD series*timesteps/s (R=1024, fp64) on B200 — BASELINE.json metric.
+"""Benchmark: batched BOCD series*timesteps/s (fp64) on B200 — BASELINE.json metric.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-    torchrun --nproc-per-node N bench.py --gpus N ...       (one rank per GPU, NCCL)
+                    [--config C3|C2|C4|C5] [--scaling strong|weak] [--eager]
 
-Workload (BASELINE.json configs[2], "C3"): 32,768 per-link communication-time
-series per GPU (weak scaling: rank g owns global series [g*32768, (g+1)*32768)),
-R = 1024, constant hazard 1/250, MERGE truncation, prior from the first
-observation (Q2/Q3/Q6), synthetic traces from the counter-based
-generator (tracegen.py recipe), generated in HBM before timing.  One bench
-"step" = one falcon_bocd_update_chunk call absorbing --chunk (default 1,000)
-new observations for every series of the rank: all of §8(a)'s rows.  The timed
-region ends with the change-point drain (falcon_bocd_changepoints) and, for
-N > 1, the NCCL all-gather of the events, then the max over ranks.
+--gpus N > 1 without torchrun's WORLD_SIZE re-launches this script under
+`torch.distributed.run` (one rank per GPU, NCCL, 127.0.0.1); under torchrun the
+world size must equal --gpus.
 
-Emits ONE JSON line on rank 0 (see DESIGN.md §7 for every field).
+Workloads (BASELINE.json configs, tracegen.py recipe, DESIGN.md §4/§7):
+  C3 (default, the metric's config): 32,768 per-link comm-time series, R = 1024.
+  C2: 1,024 per-rank iteration-time series, R = 512.
+  C4: 100,000 series, R = 4096 (the config that is sharded across 8 B200).
+  C5: online streaming, 10,240 series, one observation per series per call, R = 1024.
+Scaling: strong (default) keeps the config's GLOBAL series count at every N and gives
+rank g the contiguous block distributed.shard_range(S, g, N); weak gives every rank the
+config's full series count.  Constant hazard 1/250, MERGE truncation, prior from the first
+observation (readings Q2/Q3/Q6); synthetic traces generated in HBM before timing.
+
+One bench "step" = one pass of the whole hot path (every §8(a) row) over one batch:
+  C2/C3/C4: one falcon_bocd_update_chunk call absorbing --chunk (default 1,000) new
+            observations for every local series;
+  C5:       --calls (default 1,000) back-to-back T = 1 calls.
+The timed region ends with the change-point drain (falcon_bocd_changepoints; C5: one per
+step) and, for N > 1, the NCCL all-gather of the events; the time is the max over ranks.
+
+Emits ONE JSON line on rank 0 (DESIGN.md §7 lists every field).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
+import statistics
 import subprocess
 import sys
 import threading
@@ -35,26 +48,34 @@ UNIT = "series*steps/s"
 # FP64-pipe work per cell (one run length, one step): DESIGN.md §6.
 #   ALGORITHMIC work = the textbook recursion of PAPER App. A per cell, counted
 #   as FP64-pipe instructions with this library's table-driven transcendentals: NIG update 4
-#   (d, mu', x - mu' folded with 1/2, beta'), lg beta' 8 (fast_log2: 256-entry table,
-#   degree-4 polynomial), Student-t predictive 3, 2^(l - N) 9 (fast_exp2, the reference
-#   folded into its rounding constant), joint + evidence sum 2  =  26.  It is fixed across
-#   kernel formulations (comparable between rounds).  The current kernel evaluates the same
-#   recursion in the log-joint form (bocd_kernel.cuh: the predictive ratio telescopes into
-#   the NIG marginal likelihood; cellmath.cuh transcendentals) with 21 FP64-pipe
-#   instructions (20 DFMA/DADD/DMUL + one I2F.F64) per cell: "frac_executed" reports the
-#   fraction on that basis.  Per-step work (group reduction, scalar tail, the tile's prior
-#   references) is counted in neither.  For context the textbook cell with libdevice log/exp
-#   (30 + 18 FP64 instructions, cuobjdump, P0) is 60.
+#   (d, mu', x - mu' folded with 1/2, beta'), lg beta' 8 (table + degree-3 polynomial + the
+#   exponent), Student-t predictive 3, 2^(l - N) 9 (table + degree-4 polynomial, the frame
+#   folded into its rounding constant), joint + evidence sum 2  =  26.  Fixed across kernel
+#   formulations (comparable between rounds).  The kernel evaluates the same recursion in
+#   the log-joint form (bocd_kernel.cuh: the predictive ratio telescopes into the NIG marginal
+#   likelihood) with 21 FP64-pipe instructions per cell: "frac_executed" reports the fraction
+#   on that basis.  Per-step work (group reduction, scalar tail, the tile's prior references)
+#   is counted in neither.
 FP64_INSTR_PER_CELL = 26
 FP64_INSTR_PER_CELL_EXECUTED = 21
-FP64_INSTR_PER_CELL_LIBDEVICE = 60
-# FP64 pipe peak: 148 SMs x 64 FP64 lanes/clk x 1965 MHz (sm_max_mhz, MEASURED_PEAKS.json);
-# P0 measured 58.9 DFMA/clk/SM sustained at 1965 MHz (profiles/r01_p0_fp64_peaks.json).
+# FP64 pipe: 148 SMs x 64 FP64 lanes/clk (guide unit counts) x 1965 MHz (MEASURED_PEAKS.json
+# sm_max_mhz) = 1.861e13/s nominal; measured DFMA throughput 1.712e13/s (58.9 DFMA/clk/SM at
+# 1965 MHz, tools/peaks/fp64_peak.cu, profiles/r02_p0_fp64_peaks.json).
 SMS, FP64_PER_CLK_SM = 148, 64
+FP64_MEASURED_PER_S = 1.712e13
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
            0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
            0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
            0x100: "display_clock_setting"}
+BAD_REASONS = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+CONFIG_TEXT = {
+    "C2": "1,024 per-rank iteration-time series x 10,000 steps (1024-GPU job), R=512 (BASELINE.json configs[1])",
+    "C3": "32,768 per-link comm-time series x 100,000 steps (~4,000-node RoCE cluster), R=1024 "
+          "(BASELINE.json configs[2])",
+    "C4": "100,000 series x 100,000 steps, R=4096, sharded across GPUs (BASELINE.json configs[3])",
+    "C5": "online streaming: 10,240 series, one new observation per series per call, R=1024 "
+          "(BASELINE.json configs[4])",
+}
 
 
 def _peaks():
@@ -122,13 +143,30 @@ class ClockSampler:
                 "samples": len(sm), "power_w_max": max(pw) if pw else None}
 
 
+def clocks_bad(cs) -> bool:
+    """A run to re-measure: thermal / hardware slowdown, or SM clocks well below max with no
+    reason reported (a leftover clock lock).  sw_power_cap is kept and noted."""
+    if BAD_REASONS & set(cs.get("reasons", [])):
+        return True
+    return bool(cs.get("sm_mhz") and cs.get("sm_max_mhz") and cs["sm_mhz"] < 0.9 * cs["sm_max_mhz"]
+                and not cs["reasons"])
+
+
 def host_cores() -> int:
-    """Cores this process may run on (torchrun sets OMP_NUM_THREADS=1 per rank; the oracle
-    legs ask for every core explicitly)."""
+    """Cores this process may run on (the oracle legs ask for every one explicitly)."""
     try:
         return len(os.sched_getaffinity(0))
     except AttributeError:  # pragma: no cover
         return os.cpu_count() or 1
+
+
+def oracle_sample(cfg):
+    """Bounded oracle sample for a config: (series, steps).  Steps cover 3R so that most of
+    the sample runs with all R run lengths live; series fill the cores."""
+    cores = host_cores()
+    T_s = min(cfg.T, 3 * cfg.R)
+    n_s = max(cores, int(32 * cores * (1024 / cfg.R) ** 2))  # ~10-30 s of oracle work
+    return min(n_s, cfg.n_series), T_s
 
 
 def cpu_baseline_run(cfg, spec, n_series, T_s, s_offset=0):
@@ -143,8 +181,15 @@ def cpu_baseline_run(cfg, spec, n_series, T_s, s_offset=0):
     return n_series * T_s / dt, dt
 
 
+def _sample_text(cfg, n_s, T_s, dt=None):
+    tail = f" ({dt:.1f} s)" if dt is not None else ""
+    return (f"{n_s} {cfg.name} series x first {T_s} steps, R={cfg.R}{tail}; steps 0..{cfg.R - 1} have "
+            f"< R live run lengths")
+
+
 def run_reference(args):
-    """--impl reference: the oracle (the deliberately slow CPU program) on the host cores."""
+    """--impl reference: the oracle (the deliberately slow CPU program) on the host cores,
+    rank 0 only (other ranks exit 0 without work)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
@@ -152,8 +197,9 @@ def run_reference(args):
     cfg = tracegen.CONFIGS[args.config]
     spec = tracegen.make_spec(cfg, n_series=cfg.n_series)
     cores = host_cores()
-    n_s = max(1, min(cfg.n_series // max(1, args.steps + args.warmup), 4 * cores))
-    T_s = min(cfg.T, args.ref_steps)
+    n_s, T_s = oracle_sample(cfg)
+    n_s = max(1, min(n_s, max(cores, n_s // 8)))  # per step: the whole run stays within minutes
+    T_s = min(T_s, args.ref_steps) if args.ref_steps else T_s
     times = []
     for k in range(args.warmup + args.steps):
         _, dt = cpu_baseline_run(cfg, spec, n_s, T_s, s_offset=(k * n_s) % max(1, cfg.n_series - n_s))
@@ -164,12 +210,11 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": _config_block(cfg, args, n_series_rank=cfg.n_series, world=1),
+        "config": _config_block(cfg, args, cfg.n_series, 1, cfg.n_series),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": f"each step: {n_s} C3 series x first {T_s} steps (R={cfg.R}, "
-                                   f"steps 0..{cfg.R - 1} have < R live run lengths)"},
+                         "sample": "each step: " + _sample_text(cfg, n_s, T_s)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -177,13 +222,59 @@ def run_reference(args):
     return 0
 
 
-def _config_block(cfg, args, n_series_rank, world):
-    return {"workload": f"{cfg.name}: {cfg.n_series:,} per-link comm-time series x {cfg.T:,} steps, "
-                        f"R={cfg.R} (BASELINE.json configs[2]); timed: {args.steps} x {args.chunk} steps",
-            "series_per_gpu": n_series_rank, "series_global": n_series_rank * world, "R": cfg.R,
-            "hazard": cfg.hazard, "truncation": "merge", "chunk_steps": args.chunk,
-            "parallelism": f"series-sharded x{world}",
-            "l2": "no flush: every step streams a fresh x chunk and the whole state, both > 126 MB L2"}
+def _config_block(cfg, args, n_local, world, n_global):
+    step = (f"{args.calls} calls of 1 step" if cfg.name == "C5" else f"{args.chunk} steps")
+    return {"workload": f"{cfg.name}: {CONFIG_TEXT[cfg.name]}; timed: {args.steps} x {step}",
+            "series_global": n_global, "series_per_gpu": n_local, "R": cfg.R,
+            "hazard": cfg.hazard, "truncation": "merge",
+            "events": "PROB+MAPRESET (EAGER kernel: r* every step)" if args.eager else "PROB (MAP on demand)",
+            "chunk_steps": 1 if cfg.name == "C5" else args.chunk,
+            "parallelism": f"series-sharded x{world} ({args.scaling} scaling)",
+            "l2": ("no flush: every call streams the whole state (> 126 MB L2) through HBM" if cfg.name == "C5"
+                   else "no flush: every step streams a fresh x chunk and the whole state, both > 126 MB L2")}
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch(args) -> int:
+    """--gpus N > 1 outside torchrun: one rank per GPU under torch.distributed.run."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def _roofline_alu(cells_per_launch, k_avg_ms, kernel, peaks):
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    peak = SMS * FP64_PER_CLK_SM * sm_max * 1e6
+    achieved = FP64_INSTR_PER_CELL * cells_per_launch / (k_avg_ms * 1e-3)
+    return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "FP64-pipe instr/s",
+            "frac": achieved / peak, "kernel": kernel, "kernel_ms_avg": k_avg_ms,
+            "work_per_cell": FP64_INSTR_PER_CELL,
+            "frac_executed": FP64_INSTR_PER_CELL_EXECUTED * cells_per_launch / (k_avg_ms * 1e-3) / peak,
+            "frac_vs_measured_dfma_peak": achieved / FP64_MEASURED_PER_S,
+            "peak_basis": f"{SMS} SMs x {FP64_PER_CLK_SM} FP64/clk x {sm_max:.0f} MHz (guide unit counts; "
+                          f"measured DFMA peak {FP64_MEASURED_PER_S:.3e}/s)"}
+
+
+def _traffic(tag, scale_units):
+    """DRAM bytes per launch from the committed ncu capture (profiles/ncu_traffic*.json),
+    scaled to this launch's units."""
+    path = os.path.join(ROOT, "profiles", f"ncu_traffic_{tag}.json")
+    if not os.path.exists(path):
+        path = os.path.join(ROOT, "profiles", "ncu_traffic.json") if tag == "C3" else None
+    if not path or not os.path.exists(path):
+        return None
+    try:
+        tj = json.load(open(path))
+        return tj["bytes_per_launch"] * scale_units / tj["units"] if tj.get("units") else (
+            tj["bytes_per_launch"] * scale_units / (tj["series"] * tj["chunk"]))
+    except Exception:
+        return None
 
 
 def main():
@@ -192,180 +283,295 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C3")
-    ap.add_argument("--chunk", type=int, default=1000, help="timesteps absorbed per bench step")
-    ap.add_argument("--series", type=int, default=0, help="series per GPU (default: the config's)")
+    ap.add_argument("--config", default="C3", choices=["C2", "C3", "C4", "C5"])
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
+    ap.add_argument("--eager", action="store_true", help="MAPRESET events too (per-step MAP: EAGER kernel)")
+    ap.add_argument("--chunk", type=int, default=1000, help="timesteps absorbed per bench step (C2-C4)")
+    ap.add_argument("--calls", type=int, default=1000, help="T=1 calls per bench step (C5)")
+    ap.add_argument("--series", type=int, default=0, help="global series (default: the config's)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-steps", type=int, default=2048, help="oracle sample length (reference arm)")
-    ap.add_argument("--cpu-sample-steps", type=int, default=3072)
+    ap.add_argument("--ref-steps", type=int, default=0, help="oracle sample length (reference arm)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
 
     import torch
     import torch.distributed as dist
     from paper_2410_12588_b200 import bocd, tracegen
-    from paper_2410_12588_b200.distributed import allgather_events, max_over_ranks
+    from paper_2410_12588_b200.distributed import ShardedBocd, allgather_events, max_over_ranks, shard_range
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     cfg = tracegen.CONFIGS[args.config]
-    S = args.series or cfg.n_series
-    s0 = rank * S
-    total = (args.warmup + args.steps) * args.chunk
-    assert total <= cfg.T, "warmup+steps exceed the workload length"
-    spec = tracegen.make_spec(cfg, n_series=S * world)
+    n_cfg = args.series or cfg.n_series
+    if args.scaling == "strong":
+        n_global = n_cfg
+        lo, hi = shard_range(n_global, rank, world)
+    else:
+        n_global = n_cfg * world
+        lo, hi = rank * n_cfg, (rank + 1) * n_cfg
+    S = hi - lo
+    assert S > 0, "every rank needs at least one series"
+    streaming = cfg.name == "C5"
+    per_step = args.calls if streaming else args.chunk
+    total = (args.warmup + args.steps) * per_step
+    assert total <= cfg.T, "warmup + steps exceed the workload length"
+    spec = tracegen.make_spec(cfg, n_series=n_global)
     dtrace = bocd.DeviceTrace(spec, dev)
-    x = torch.empty((S, total), dtype=torch.float64, device=dev)
-    dtrace.generate(x, s0, 0)
+    if streaming:
+        # online layout: one contiguous column of S observations per call (x_t for every series)
+        xs = torch.empty((S, total), dtype=torch.float64, device=dev)
+        dtrace.generate(xs, lo, 0)
+        x = xs.t().contiguous()  # [total][S]
+        del xs
+        col = lambda k: x[k].view(S, 1)  # noqa: E731  ([S][1], ld = 1)
+    else:
+        x = torch.empty((S, total), dtype=torch.float64, device=dev)
+        dtrace.generate(x, lo, 0)
     torch.cuda.synchronize()
 
-    b = bocd.BocdBatch(S, R=cfg.R, hazard=cfg.hazard, kappa0=cfg.kappa0, alpha0=cfg.alpha0,
-                       prior_first_obs=True, prior_cov=cfg.prior_cov, threshold=cfg.threshold,
-                       trunc_mode="merge", event_mask=bocd.N.EV_PROB, event_capacity=256,
-                       device=local, series_base=s0)
+    mask = bocd.N.EV_PROB | (bocd.N.EV_MAPRESET if args.eager else 0)
+    kw = dict(R=cfg.R, hazard=cfg.hazard, kappa0=cfg.kappa0, alpha0=cfg.alpha0, prior_first_obs=True,
+              prior_cov=cfg.prior_cov, threshold=cfg.threshold, trunc_mode="merge", event_mask=mask,
+              event_capacity=256)
+    # (weak scaling: n_global = world x n_cfg, so shard_range gives rank g the block [g n_cfg, (g+1) n_cfg))
+    sb = ShardedBocd(n_global, rank=rank, world=world, device=local, **kw)
+    assert (sb.lo, sb.hi) == (lo, hi)
+    b = sb.batch
     stream = torch.cuda.current_stream()
-    C = args.chunk
+
+    def run_step(k):  # one bench step: every §8(a) row over one batch
+        if streaming:
+            for c in range(per_step):
+                b.update_chunk(col(k * per_step + c))
+        else:
+            c0 = k * per_step
+            b.update_chunk(x[:, c0:c0 + per_step])
+
     for k in range(args.warmup):
-        b.update_chunk(x[:, k * C:(k + 1) * C])
+        run_step(k)
     b.changepoints()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+
     def timed_region():
         ev_start, ev_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        k_start = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-        k_end = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        n_marks = args.steps * (per_step if streaming else 1)
+        ks = [torch.cuda.Event(enable_timing=True) for _ in range(n_marks)]
+        ke = [torch.cuda.Event(enable_timing=True) for _ in range(n_marks)]
+        events = []
         with ClockSampler(local) as clk:
             time.sleep(0.3)
             torch.cuda.synchronize()
             ev_start.record(stream)
+            m = 0
             for k in range(args.steps):
-                c0 = (args.warmup + k) * C
-                k_start[k].record(stream)
-                b.update_chunk(x[:, c0:c0 + C])
-                k_end[k].record(stream)
-            recs, dropped = b.changepoints(device_out=True)
+                kk = args.warmup + k
+                if streaming:
+                    for c in range(per_step):
+                        ks[m].record(stream)
+                        b.update_chunk(col(kk * per_step + c))
+                        ke[m].record(stream)
+                        m += 1
+                    recs, dropped = b.changepoints(device_out=True)  # each step's result
+                    events.append(recs)
+                else:
+                    ks[m].record(stream)
+                    b.update_chunk(x[:, kk * per_step:(kk + 1) * per_step])
+                    ke[m].record(stream)
+                    m += 1
+            if not streaming:
+                recs, dropped = b.changepoints(device_out=True)
+                events.append(recs)
+            recs = torch.cat(events) if len(events) > 1 else events[0]
             if world > 1:
                 allgather_events(recs)
             ev_end.record(stream)
             torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        return ev_start, ev_end, k_start, k_end, clk, recs, dropped
+        return ev_start, ev_end, ks, ke, clk, recs, dropped
 
-    ev_start, ev_end, k_start, k_end, clk, recs, dropped = timed_region()
-    # a run that saw thermal / hardware slowdown (on any rank) is measured once more, over
-    # the same chunks again (the per-step cost does not depend on the data)
+    ev_start, ev_end, ks, ke, clk, recs, dropped = timed_region()
     cs = clk.summary()
-    bad = bool({"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"} & set(cs["reasons"]))
-    # SM clock well below max with no reason reported: a leftover clock lock
-    bad = bad or bool(cs.get("sm_mhz") and cs.get("sm_max_mhz") and cs["sm_mhz"] < 0.9 * cs["sm_max_mhz"]
-                      and not cs["reasons"])
-    bad_any = max_over_ranks(float(bool(bad)), dev) > 0 if world > 1 else bool(bad)
+    bad_any = max_over_ranks(float(clocks_bad(cs)), dev) > 0 if world > 1 else clocks_bad(cs)
     remeasured = False
-    if bad_any:
-        ev_start, ev_end, k_start, k_end, clk, recs, dropped = timed_region()
+    if bad_any:  # measured once more over the same steps (the per-step cost is data-independent)
+        ev_start, ev_end, ks, ke, clk, recs, dropped = timed_region()
         remeasured = True
-    n_events_rank = int(recs.shape[0])
     t_ms = ev_start.elapsed_time(ev_end)
     t_max = max_over_ranks(t_ms, dev)
-    k_ms = [a.elapsed_time(e) for a, e in zip(k_start, k_end)]
+    k_ms = [a.elapsed_time(e) for a, e in zip(ks, ke)]
     k_avg = sum(k_ms) / len(k_ms)
     k_share = sum(k_ms) / t_ms
-    value = S * world * C * args.steps / (t_max * 1e-3)
+    value = n_global * per_step * args.steps / (t_max * 1e-3) if args.scaling == "strong" else (
+        S * world * per_step * args.steps / (t_max * 1e-3))
     nt, j, spb = b.kernel_shape()
-    cells_per_launch = S * C * cfg.R
-    achieved = FP64_INSTR_PER_CELL * cells_per_launch / (k_avg * 1e-3)
     peaks = _peaks()
-    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    peak = SMS * FP64_PER_CLK_SM * sm_max * 1e6
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            tj = json.load(open(tpath))
-            if tj.get("series") and tj.get("chunk"):
-                # DRAM bytes scale with series x chunk for this kernel (x stream + one state pass)
-                traffic = tj["bytes_per_launch"] * (S * C) / (tj["series"] * tj["chunk"])
-        except Exception:
-            traffic = None
+    kname = f"bocd_update_kernel<{nt},{j},FULL,{'EAGER' if args.eager else 'lazy MAP'}{',persistent' if streaming else ''}>"
+    if streaming:
+        bytes_per_call = S * (48 * cfg.R + 8)  # state (mu, beta, a) in + out and one x per series
+        achieved = bytes_per_call / (k_avg * 1e-3)
+        peak = float(peaks.get("hbm_gbs", 6537.6)) * 1e9
+        roof = {"bound": "hbm", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "GB/s",
+                "frac": achieved / peak, "kernel": kname, "kernel_ms_avg": k_avg,
+                "bytes_per_launch": bytes_per_call,
+                "peak_basis": "MEASURED_PEAKS.json hbm_gbs (copy, read+write)"}
+        roof["traffic"] = _traffic(cfg.name, S)
+    else:
+        roof = _roofline_alu(S * per_step * cfg.R, k_avg, kname, peaks)
+        roof["traffic"] = _traffic(cfg.name, S * per_step)
+    roof["kernel_share_of_step"] = k_share
     clocks = clk.summary()
     if remeasured:
         clocks["remeasured"] = True
 
-    # ---- e2e: host buffers through falcon_bocd_update_chunk_host + host drain ----------
+    latency = None
+    if streaming:
+        latency = streaming_latency(b, col, args, cfg, stream)
+
     e2e = None
     if not args.no_e2e:
-        hb = [torch.empty((S, C), dtype=torch.float64).pin_memory() for _ in range(2)]
-        for i in range(2):
-            hb[i].copy_(x[:, (args.warmup + i) * C:(args.warmup + i + 1) * C])
-        b2 = bocd.BocdBatch(S, R=cfg.R, hazard=cfg.hazard, kappa0=cfg.kappa0, alpha0=cfg.alpha0,
-                            prior_first_obs=True, prior_cov=cfg.prior_cov, trunc_mode="merge",
-                            event_mask=bocd.N.EV_PROB, event_capacity=256, device=local,
-                            series_base=s0)
-        b2.update_chunk_host(hb[0])
-        b2.changepoints()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        d2h = 0
-        e0.record(stream)
-        for k in range(args.steps):
-            b2.update_chunk_host(hb[k % 2])
-            evs, _ = b2.changepoints()
-            d2h += evs.nbytes + 16 + 4 + 8  # records + scan meta + sticky flag + pending count
-        e1.record(stream)
-        torch.cuda.synchronize()
-        et = max_over_ranks(e0.elapsed_time(e1), dev)
-        b2.close()
-        e2e = {"value": S * world * C * args.steps / (et * 1e-3), "unit": UNIT,
-               "h2d_bytes_per_step": S * C * 8, "d2h_bytes_per_step": int(d2h / args.steps),
-               "api": "falcon_bocd_update_chunk_host + falcon_bocd_changepoints (pinned host x)"}
+        e2e = e2e_run(sb, bocd, x, col if streaming else None, args, cfg, kw, local, lo, S, n_global, world, dev,
+                      stream)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cores = host_cores()
-        n_s = 32 * cores
-        v, dt = cpu_baseline_run(cfg, spec, n_s, args.cpu_sample_steps)
-        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"{n_s} C3 series x first {args.cpu_sample_steps} steps, R={cfg.R} "
-                         f"({dt:.1f} s; steps 0..{cfg.R - 1} have < R live run lengths)"}
-    b.close()
+        n_s, T_s = oracle_sample(cfg)
+        v, dt = cpu_baseline_run(cfg, spec, n_s, T_s)
+        cpu = {"value": v, "unit": UNIT, "cores": host_cores(), "kind": "oracle",
+               "sample": _sample_text(cfg, n_s, T_s, dt)}
+    launches = args.steps * (per_step + 2) if streaming else args.steps + 2
+    n_events = int(recs.shape[0])
+    sb.close()
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (counter-based generator, C3 recipe, generated in HBM)",
-            "config": _config_block(cfg, args, S, world),
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak,
-                         "unit": "FP64-pipe instr/s", "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "bocd_update_kernel<128,8,FULL,ROT>",
-                         "kernel_ms_avg": k_avg, "kernel_share_of_step": k_share,
-                         "work_per_cell": FP64_INSTR_PER_CELL,
-                         "frac_executed": FP64_INSTR_PER_CELL_EXECUTED * cells_per_launch
-                         / (k_avg * 1e-3) / peak,
-                         "frac_vs_libdevice_work": FP64_INSTR_PER_CELL_LIBDEVICE * cells_per_launch
-                         / (k_avg * 1e-3) / peak,
-                         "peak_basis": f"{SMS} SMs x {FP64_PER_CLK_SM} FP64/clk x {sm_max:.0f} MHz (derived)"},
-            "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": args.steps + 3,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+            "data": f"synthetic (counter-based generator, {cfg.name} recipe, generated in HBM)",
+            "config": _config_block(cfg, args, S, world, n_global),
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches,
             "clocks": clocks,
-            "events": {"rank0": n_events_rank, "dropped": bool(dropped)},
+            "events": {"rank0": n_events, "dropped": bool(dropped)},
             "kernel_shape": {"threads_per_series": nt, "cells_per_thread": j, "series_per_cta": spb},
         }
+        if latency:
+            line["latency"] = latency
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def streaming_latency(b, col, args, cfg, stream, n=300):
+    """C5 per-call latency three ways (after the timed region, same handle, data continued):
+    device time of the update kernel (CUDA events), host wall time of one call including the
+    launch and a stream synchronise, and host wall time of one call followed by a full event
+    drain (falcon_bocd_changepoints) every call."""
+    import torch
+    base = (args.warmup + args.steps) * args.calls
+    avail = cfg.T - base
+    n = max(10, min(n, avail // 3))
+    dev_ms, wall_ms, drain_ms = [], [], []
+    for i in range(n):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        b.update_chunk(col(base + i))
+        e1.record(stream)
+        e1.synchronize()
+        dev_ms.append(e0.elapsed_time(e1))
+    base += n
+    for i in range(n):
+        t0 = time.perf_counter()
+        b.update_chunk(col(base + i))
+        stream.synchronize()
+        wall_ms.append(1e3 * (time.perf_counter() - t0))
+    base += n
+    for i in range(n):
+        t0 = time.perf_counter()
+        b.update_chunk(col(base + i))
+        b.changepoints()
+        drain_ms.append(1e3 * (time.perf_counter() - t0))
+    q = lambda v, p: sorted(v)[min(len(v) - 1, int(p * len(v)))]  # noqa: E731
+    return {"calls_each": n, "device_ms_median": statistics.median(dev_ms), "device_ms_p99": q(dev_ms, 0.99),
+            "host_wall_ms_median": statistics.median(wall_ms), "host_wall_ms_p99": q(wall_ms, 0.99),
+            "with_drain_ms_median": statistics.median(drain_ms), "with_drain_ms_p99": q(drain_ms, 0.99),
+            "drain_over_no_drain": statistics.median(drain_ms) / statistics.median(wall_ms)}
+
+
+def e2e_run(sb0, bocd, x, col, args, cfg, kw, local, lo, S, n_global, world, dev, stream):
+    """The same metric end to end through the public API with HOST buffers: every step copies
+    that step's observations from pinned host memory (falcon_bocd_update_chunk_host) and reads
+    that step's change points back (falcon_bocd_changepoints_async into page-locked memory,
+    collected while the next step's copy and kernel run); N > 1: the final all-gather."""
+    import torch
+    from paper_2410_12588_b200.distributed import allgather_events, max_over_ranks
+    streaming = col is not None
+    per_step = args.calls if streaming else args.chunk
+    nbuf = 2
+    if streaming:
+        hb = [torch.empty((per_step, S), dtype=torch.float64).pin_memory() for _ in range(nbuf)]
+        for i in range(nbuf):
+            hb[i].copy_(x[(args.warmup + i) * per_step:(args.warmup + i + 1) * per_step])
+    else:
+        hb = [torch.empty((S, per_step), dtype=torch.float64).pin_memory() for _ in range(nbuf)]
+        for i in range(nbuf):
+            hb[i].copy_(x[:, (args.warmup + i) * per_step:(args.warmup + i + 1) * per_step])
+    b2 = bocd.BocdBatch(S, device=local, series_base=lo, **kw)
+
+    def host_step(k):
+        h = hb[k % nbuf]
+        if streaming:
+            for c in range(per_step):
+                b2.update_chunk_host(h[c].view(S, 1))
+        else:
+            b2.update_chunk_host(h)
+        return b2.changepoints_async()
+
+    host_step(0).result()
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    pending, got, d2h = None, [], 0
+    for k in range(args.steps):
+        ticket = host_step(k)
+        if pending is not None:
+            evs, _ = pending.result()  # the previous step's events, read while this step runs
+            got.append(evs)
+            d2h += evs.nbytes + 32
+        pending = ticket
+    evs, _ = pending.result()
+    got.append(evs)
+    d2h += evs.nbytes + 32
+    if world > 1:
+        import numpy as np
+        allrec = np.concatenate(got) if got else np.empty(0, bocd.EVENT_DTYPE)
+        allgather_events(torch.from_numpy(allrec.view(np.uint8).reshape(-1, 40).copy()).to(dev))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    et = max_over_ranks(e0.elapsed_time(e1), dev)
+    b2.close()
+    n_units = (n_global if args.scaling == "strong" else S * world) * per_step * args.steps
+    return {"value": n_units / (et * 1e-3), "unit": UNIT, "h2d_bytes_per_step": S * per_step * 8,
+            "d2h_bytes_per_step": int(d2h / args.steps),
+            "api": ("falcon_bocd_update_chunk_host per call" if streaming else "falcon_bocd_update_chunk_host")
+                   + " + falcon_bocd_changepoints_async per step (pinned host x and events)"}
 
 
 if __name__ == "__main__":

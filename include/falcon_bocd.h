@@ -131,15 +131,31 @@ int falcon_bocd_update_chunk_host(falcon_bocd_t h, const double *x_host, int64_t
 
 /* Drains the per-series event buffers into out[capacity] (HOST or DEVICE
  * memory, detected), in (series, t) order, and resets them.  *n_out receives
- * the number written.  Synchronises `stream`.  Returns FALCON_WARN_EVENTS_DROPPED
+ * the number written.  Synchronises `stream` (once for device or page-locked host
+ * `out`, which the gather kernel writes directly; twice for pageable host memory,
+ * staged through a device buffer).  Returns FALCON_WARN_EVENTS_DROPPED
  * if any series overflowed event_capacity since the last drain (the first
  * event_capacity events of each series are kept), FALCON_EINVAL if capacity is
  * smaller than the number of buffered events (nothing is drained; *n_out = the
- * number needed), FALCON_ENONFINITE if a non-finite observation was seen. */
+ * number needed), FALCON_ENONFINITE if a non-finite observation was seen (nothing
+ * is drained).  Each event is a report of P:770 ("reports t as a change-point"). */
 int falcon_bocd_changepoints(falcon_bocd_t h, falcon_bocd_event *out, int64_t capacity,
                              int64_t *n_out, void *stream);
 
-/* Number of buffered events (synchronises `stream`). */
+/* Stream-ordered, asynchronous drain (no host synchronisation): enqueues the
+ * same count + gather kernels on `stream`.  out[capacity] and meta[4] must be
+ * memory the device can write: device memory or page-locked host memory.  When
+ * the work completes, meta = {total buffered events, overflow flag (as
+ * FALCON_WARN_EVENTS_DROPPED), sticky error bits (1: non-finite observation,
+ * 2: bad prior, 4: internal), drained (1 if the events were written to out and
+ * the buffers reset; 0 if total > capacity or an error bit is set, in which
+ * case nothing changed)}.  Lets a caller read the events of chunk k while
+ * chunk k+1 is copied and computed.  Returns FALCON_EINVAL for bad pointers,
+ * FALCON_ESTATE on a poisoned handle. */
+int falcon_bocd_changepoints_async(falcon_bocd_t h, falcon_bocd_event *out, int64_t capacity,
+                                   int64_t *meta, void *stream);
+
+/* Number of buffered events (synchronises `stream`; nothing is drained). */
 int falcon_bocd_pending_events(falcon_bocd_t h, int64_t *n_out, void *stream);
 
 /* Copies the normalised log run-length posterior log Pr(r_t = r | x_{1:t}) and

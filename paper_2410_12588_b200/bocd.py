@@ -25,10 +25,26 @@ def _ld(x):
     return x.stride(0) if x.shape[0] > 1 else max(x.stride(0), x.shape[1])
 
 
-def _stream_ptr(stream):
+def _stream_ptr(stream, device=None):
     if stream is None:
-        stream = torch.cuda.current_stream()
+        stream = torch.cuda.current_stream(device)
     return ctypes.c_void_p(stream.cuda_stream)
+
+
+class DrainTicket:
+    """An enqueued asynchronous drain (BocdBatch.changepoints_async)."""
+
+    def __init__(self, batch, buf, meta, event, stream):
+        self._batch, self._buf, self._meta, self._event, self._stream = batch, buf, meta, event, stream
+
+    def result(self):
+        """Waits for the drain; returns (events, dropped) as BocdBatch.changepoints()."""
+        self._event.synchronize()
+        total, ovf, err, drained = (int(v) for v in self._meta.tolist())
+        self._batch._ev_hint = max(self._batch._ev_hint, total)
+        if not drained:  # capacity too small or a sticky error: nothing changed, drain (or raise) now
+            return self._batch.changepoints(self._stream)
+        return self._buf[:total].numpy().reshape(-1).view(EVENT_DTYPE).copy(), bool(ovf)
 
 
 class BocdBatch:
@@ -75,6 +91,10 @@ class BocdBatch:
         self._h = h
         self.n_series, self.R, self.device = int(n_series), int(R), torch.device("cuda", int(device))
         self.event_capacity = int(event_capacity)
+        self._evbufs = {}
+        self._ev_hint = min(self.n_series * self.event_capacity, 4096)
+        self._metas = [torch.zeros(4, dtype=torch.int64, pin_memory=True) for _ in range(2)]
+        self._ticket_slot = 0
 
     # -- hot path ---------------------------------------------------------------
     def update_chunk(self, x: torch.Tensor, outputs: bool = False, stream=None):
@@ -91,7 +111,7 @@ class BocdBatch:
             outs = N.StepOut(res[0].data_ptr(), res[1].data_ptr(), res[2].data_ptr(), T)
         N.check(N.lib().falcon_bocd_update_chunk(self._h, _ptr(x), _ld(x), T,
                                                  ctypes.byref(outs) if outs else None,
-                                                 _stream_ptr(stream)), self._h)
+                                                 _stream_ptr(stream, self.device)), self._h)
         return res
 
     def update_chunk_host(self, x: np.ndarray | torch.Tensor, outputs: bool = False, stream=None):
@@ -109,32 +129,68 @@ class BocdBatch:
             outs = N.StepOut(res[0].ctypes.data, res[1].ctypes.data, res[2].ctypes.data, T)
         N.check(N.lib().falcon_bocd_update_chunk_host(self._h, ctypes.c_void_p(ptr), ld, T,
                                                       ctypes.byref(outs) if outs else None,
-                                                      _stream_ptr(stream)), self._h)
+                                                      _stream_ptr(stream, self.device)), self._h)
         return res
 
+    def _event_buffer(self, where: str, need: int, slot: int = 0):
+        """Cached drain buffer (uint8 [cap, 40]): 'host' = page-locked (the gather kernel writes it
+        directly), 'device' = this handle's device.  Grows geometrically."""
+        key = (where, slot)
+        buf = self._evbufs.get(key)
+        if buf is None or buf.shape[0] < need:
+            cap = max(need, 2 * (buf.shape[0] if buf is not None else 0), 1024)
+            if where == "host":
+                buf = torch.empty((cap, EVENT_DTYPE.itemsize), dtype=torch.uint8, pin_memory=True)
+            else:
+                buf = torch.empty((cap, EVENT_DTYPE.itemsize), dtype=torch.uint8, device=self.device)
+            self._evbufs[key] = buf
+        return buf
+
     def changepoints(self, stream=None, device_out: bool = False):
-        """Drain buffered events in (series, t) order.  Returns (events, dropped) where events
-        is a numpy structured array (host) or a uint8 device tensor of 40-B records."""
+        """Drain buffered events in (series, t) order (falcon_bocd_changepoints).  Returns
+        (events, dropped) where events is a numpy structured array (host) or a uint8 device
+        tensor of 40-B records."""
         L = N.lib()
         n = ctypes.c_int64()
-        N.check(L.falcon_bocd_pending_events(self._h, ctypes.byref(n), _stream_ptr(stream)), self._h)
-        cap = int(n.value)
+        need = self._ev_hint
+        while True:
+            buf = self._event_buffer("device" if device_out else "host", need)
+            rc = L.falcon_bocd_changepoints(self._h, ctypes.c_void_p(buf.data_ptr()), buf.shape[0],
+                                            ctypes.byref(n), _stream_ptr(stream, self.device))
+            if rc == N.FALCON_EINVAL and n.value > buf.shape[0]:
+                need = int(n.value)  # nothing was drained: retry with room for every event
+                continue
+            N.check(rc, self._h)
+            break
+        k = int(n.value)
+        self._ev_hint = max(self._ev_hint, k)
         if device_out:
-            buf = torch.empty((max(cap, 1), EVENT_DTYPE.itemsize), dtype=torch.uint8, device=self.device)
-            ptr = ctypes.c_void_p(buf.data_ptr())
-        else:
-            buf = np.empty(max(cap, 1), dtype=EVENT_DTYPE)
-            ptr = ctypes.c_void_p(buf.ctypes.data)
-        rc = N.check(L.falcon_bocd_changepoints(self._h, ptr, cap, ctypes.byref(n),
-                                                _stream_ptr(stream)), self._h)
-        return buf[: int(n.value)], rc == N.FALCON_WARN_EVENTS_DROPPED
+            return buf[:k].clone(), rc == N.FALCON_WARN_EVENTS_DROPPED
+        return buf[:k].numpy().reshape(-1).view(EVENT_DTYPE).copy(), rc == N.FALCON_WARN_EVENTS_DROPPED
+
+    def changepoints_async(self, stream=None):
+        """Enqueue a drain on `stream` without synchronising (falcon_bocd_changepoints_async);
+        the events land in page-locked host memory.  Returns a DrainTicket whose result()
+        waits for it and returns (events, dropped) like changepoints().  Two tickets may be
+        outstanding at a time (double-buffered)."""
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        slot = self._ticket_slot
+        self._ticket_slot ^= 1
+        buf = self._event_buffer("host", self._ev_hint, slot)
+        meta = self._metas[slot]
+        N.check(N.lib().falcon_bocd_changepoints_async(self._h, ctypes.c_void_p(buf.data_ptr()), buf.shape[0],
+                                                       ctypes.c_void_p(meta.data_ptr()),
+                                                       ctypes.c_void_p(st.cuda_stream)), self._h)
+        ev = torch.cuda.Event()
+        ev.record(st)
+        return DrainTicket(self, buf, meta, ev, stream)
 
     def read_posterior(self, s0: int = 0, count: int | None = None, stream=None):
         """(logR, mu, beta) as device tensors [count][R] in run-length order."""
         count = self.n_series - s0 if count is None else count
         out = [torch.empty((count, self.R), dtype=torch.float64, device=self.device) for _ in range(3)]
         N.check(N.lib().falcon_bocd_read_posterior(self._h, s0, count, _ptr(out[0]), _ptr(out[1]),
-                                                   _ptr(out[2]), _stream_ptr(stream)), self._h)
+                                                   _ptr(out[2]), _stream_ptr(stream, self.device)), self._h)
         return tuple(out)
 
     @property
@@ -189,12 +245,14 @@ def verify_changepoints(x, events, t_lo: int = 0, series_base: int = 0, window: 
     n = len(ev)
     if n == 0:
         return np.empty(0, dtype=VERIFIED_DTYPE)
-    ev_d = torch.from_numpy(ev.view(np.uint8).reshape(n, EVENT_DTYPE.itemsize)).to(x.device)
-    out_d = torch.empty((n, VERIFIED_DTYPE.itemsize), dtype=torch.uint8, device=x.device)
-    N.check(N.lib().falcon_verify_changepoints(_ptr(x), _ld(x), x.shape[0], series_base, t_lo,
-                                               x.shape[1], _ptr(ev_d), n, window, rel_threshold,
-                                               _ptr(out_d), _stream_ptr(stream)))
-    return out_d.cpu().numpy().reshape(-1).view(VERIFIED_DTYPE).copy()
+    st = stream if stream is not None else torch.cuda.current_stream(x.device)
+    with torch.cuda.stream(st):  # upload, kernel and read-back all ordered on `st`
+        ev_d = torch.from_numpy(ev.view(np.uint8).reshape(n, EVENT_DTYPE.itemsize)).to(x.device)
+        out_d = torch.empty((n, VERIFIED_DTYPE.itemsize), dtype=torch.uint8, device=x.device)
+        N.check(N.lib().falcon_verify_changepoints(_ptr(x), _ld(x), x.shape[0], series_base, t_lo,
+                                                   x.shape[1], _ptr(ev_d), n, window, rel_threshold,
+                                                   _ptr(out_d), ctypes.c_void_p(st.cuda_stream)))
+        return out_d.cpu().numpy().reshape(-1).view(VERIFIED_DTYPE).copy()
 
 
 def pair_failslow(verified, device=None, stream=None):
@@ -205,13 +263,15 @@ def pair_failslow(verified, device=None, stream=None):
     if n == 0:
         return np.empty(0, dtype=FAILSLOW_DTYPE)
     dev = device or torch.device("cuda", torch.cuda.current_device())
-    v_d = torch.from_numpy(v.view(np.uint8).reshape(n, VERIFIED_DTYPE.itemsize)).to(dev)
-    cap = int((v["status"] == N.CP_DEGRADE).sum())
-    out_d = torch.empty((max(cap, 1), FAILSLOW_DTYPE.itemsize), dtype=torch.uint8, device=dev)
-    n_out = ctypes.c_int64()
-    N.check(N.lib().falcon_pair_failslow(_ptr(v_d), n, _ptr(out_d), cap, ctypes.byref(n_out),
-                                         _stream_ptr(stream)))
-    return out_d[: n_out.value].cpu().numpy().reshape(-1).view(FAILSLOW_DTYPE).copy()
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    with torch.cuda.stream(st):
+        v_d = torch.from_numpy(v.view(np.uint8).reshape(n, VERIFIED_DTYPE.itemsize)).to(dev)
+        cap = int((v["status"] == N.CP_DEGRADE).sum())
+        out_d = torch.empty((max(cap, 1), FAILSLOW_DTYPE.itemsize), dtype=torch.uint8, device=dev)
+        n_out = ctypes.c_int64()
+        N.check(N.lib().falcon_pair_failslow(_ptr(v_d), n, _ptr(out_d), cap, ctypes.byref(n_out),
+                                             ctypes.c_void_p(st.cuda_stream)))
+        return out_d[: n_out.value].cpu().numpy().reshape(-1).view(FAILSLOW_DTYPE).copy()
 
 
 def classify_groups(times, factor: float = 1.1, stream=None):
@@ -245,10 +305,13 @@ def iteration_times(ts, period, stream=None):
     counts[s]."""
     assert ts.is_cuda and ts.dtype == torch.float64 and ts.dim() == 2 and ts.stride(1) == 1
     S, n = ts.shape
-    out = torch.zeros((S, max(n - 1, 1)), dtype=torch.float64, device=ts.device)
-    cnt = torch.empty(S, dtype=torch.int32, device=ts.device)
-    N.check(N.lib().falcon_iteration_times(_ptr(ts), S, n, _ld(ts), _ptr(period.to(torch.int32).contiguous()),
-                                           _ptr(out), out.stride(0), _ptr(cnt), _stream_ptr(stream)))
+    st = stream if stream is not None else torch.cuda.current_stream(ts.device)
+    with torch.cuda.stream(st):  # temporaries allocated on `st`: reused only after the kernel in stream order
+        per = period.to(device=ts.device, dtype=torch.int32).contiguous()
+        out = torch.zeros((S, max(n - 1, 1)), dtype=torch.float64, device=ts.device)
+        cnt = torch.empty(S, dtype=torch.int32, device=ts.device)
+        N.check(N.lib().falcon_iteration_times(_ptr(ts), S, n, _ld(ts), _ptr(per), _ptr(out), out.stride(0),
+                                               _ptr(cnt), ctypes.c_void_p(st.cuda_stream)))
     return out, cnt
 
 

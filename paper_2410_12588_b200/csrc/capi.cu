@@ -44,8 +44,10 @@ struct falcon_bocd_s {
     EventRec* d_ev = nullptr;
     unsigned* d_err = nullptr;
     // drain scratch
-    int64_t* d_off = nullptr;  // [S+1]
-    int64_t* d_meta = nullptr; // [2]: total kept, overflow flag
+    int32_t* d_off = nullptr;    // [S] offset of each series within its drain block
+    int64_t* d_blk = nullptr;    // [nblk] drain block totals
+    int32_t* d_blkovf = nullptr; // [nblk] drain block overflow bits
+    int64_t* h_meta = nullptr;   // pinned, device-mapped [4]: total, overflow, error bits, drained
     falcon_bocd_event* d_evout = nullptr;
     int64_t evout_cap = 0;
     // host staging (update_chunk_host)
@@ -134,65 +136,104 @@ __global__ void fill_kernel(double* v, int64_t n, double value) {
         v[k] = value;
 }
 
-// Exclusive scan of min(count, cap) over series (single CTA), total + overflow flag in meta.
-__global__ void drain_scan_kernel(const SeriesScalars* scal, int64_t S, int cap, int64_t* off, int64_t* meta) {
-    __shared__ int64_t part[1024];
-    __shared__ int ovf;
-    if (threadIdx.x == 0) ovf = 0;
-    const int64_t per = (S + blockDim.x - 1) / blockDim.x;
-    const int64_t a = threadIdx.x * per, b = min(S, a + per);
-    int64_t loc = 0;
-    int o = 0;
-    for (int64_t s = a; s < b; ++s) {
-        const int c = scal[s].ev_count;
-        loc += c < cap ? c : cap;
-        o |= c > cap;
+// Event drain (falcon_bocd_changepoints[_async]): two launches, no host round trip between
+// them.  drain_count_kernel: block b owns series [b*kDrainSpan, (b+1)*kDrainSpan); it writes
+// each series' exclusive offset WITHIN the block (kept = min(count, cap)) and the block's
+// total and overflow bit.  drain_gather_kernel: one warp per series adds the totals of the
+// blocks before its own (a warp-parallel sum over at most ~100 block totals), copies the
+// kept events in time order and resets the count; block 0 / warp 0 writes the meta record
+// {total, overflow, sticky error bits, drained}.  When the total exceeds `capacity`, or a
+// sticky error is set, nothing is copied or reset (meta.drained = 0).  out == nullptr:
+// count only.
+constexpr int kDrainThreads = 256;
+constexpr int kDrainPer = 4;  // series per thread
+constexpr int kDrainSpan = kDrainThreads * kDrainPer;
+
+__global__ void __launch_bounds__(kDrainThreads) drain_count_kernel(const SeriesScalars* scal, int64_t S, int cap,
+                                                                    int32_t* off_local, int64_t* blk_total,
+                                                                    int32_t* blk_ovf) {
+    __shared__ int32_t wsum[kDrainThreads / 32];
+    const int64_t s0 = int64_t(blockIdx.x) * kDrainSpan + threadIdx.x * kDrainPer;
+    int32_t kept[kDrainPer];
+    int32_t loc = 0, ovf = 0;
+#pragma unroll
+    for (int k = 0; k < kDrainPer; ++k) {
+        const int64_t s = s0 + k;
+        const int c = s < S ? scal[s].ev_count : 0;
+        kept[k] = c < cap ? c : cap;
+        ovf |= c > cap;
+        loc += kept[k];
     }
-    part[threadIdx.x] = loc;
-    __syncthreads();
-    if (o) atomicOr(&ovf, 1);
-    for (int d = 1; d < blockDim.x; d <<= 1) {
-        int64_t v = threadIdx.x >= d ? part[threadIdx.x - d] : 0;
-        __syncthreads();
-        part[threadIdx.x] += v;
-        __syncthreads();
+    // block-wide exclusive scan of loc: warp inclusive scan, then warp totals
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int32_t inc = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
     }
-    int64_t run = part[threadIdx.x] - loc;
-    for (int64_t s = a; s < b; ++s) {
-        off[s] = run;
-        const int c = scal[s].ev_count;
-        run += c < cap ? c : cap;
+    if (lane == 31) wsum[w] = inc;
+    const int any_ovf = __syncthreads_or(ovf);
+    int32_t base = 0;
+    for (int k = 0; k < w; ++k) base += wsum[k];
+    int32_t run = base + inc - loc;
+#pragma unroll
+    for (int k = 0; k < kDrainPer; ++k) {
+        if (s0 + k < S) off_local[s0 + k] = run;
+        run += kept[k];
     }
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) {
-        off[S] = part[threadIdx.x];
-        meta[0] = part[threadIdx.x];
-        meta[1] = ovf;
+    if (threadIdx.x == kDrainThreads - 1) {
+        blk_total[blockIdx.x] = base + inc;
+        blk_ovf[blockIdx.x] = any_ovf;
     }
 }
 
-// One warp per series: copy its kept events (time order) to out[off[s] ..] and reset the count.
-__global__ void drain_gather_kernel(SeriesScalars* scal, const EventRec* ev, int64_t S, int cap, const int64_t* off,
-                                    falcon_bocd_event* out, int reset, int64_t series_base) {
+__global__ void drain_gather_kernel(SeriesScalars* scal, const EventRec* ev, int64_t S, int cap,
+                                    const int32_t* off_local, const int64_t* blk_total, const int32_t* blk_ovf,
+                                    int nblk, const unsigned* err, int64_t capacity, falcon_bocd_event* out,
+                                    int64_t* meta, int64_t series_base) {
     const int64_t s = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (s >= S) return;
+    const int my_blk = s < S ? int(s / kDrainSpan) : nblk;
+    int64_t before = 0, total = 0;
+    int ovf = 0;
+    for (int b = lane; b < nblk; b += 32) {
+        const int64_t v = blk_total[b];
+        total += v;
+        before += b < my_blk ? v : 0;
+        ovf |= blk_ovf[b];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        total += __shfl_xor_sync(0xffffffffu, total, o);
+        before += __shfl_xor_sync(0xffffffffu, before, o);
+        ovf |= __shfl_xor_sync(0xffffffffu, ovf, o);
+    }
+    const unsigned e = *err;
+    const bool drain = out != nullptr && total <= capacity && (e & 7u) == 0u;
+    if (s == 0 && lane == 0) {
+        meta[0] = total;
+        meta[1] = ovf;
+        meta[2] = e;
+        meta[3] = drain ? 1 : 0;
+    }
+    if (!drain || s >= S) return;
     const int c = scal[s].ev_count;
     const int n = c < cap ? c : cap;
-    const int64_t o = off[s];
+    const int64_t o = before + off_local[s];
     for (int k = lane; k < n; k += 32) {
         const EventRec r = ev[s * int64_t(cap) + k];
-        falcon_bocd_event e;
-        e.series = series_base + s;
-        e.t = r.t;
-        e.cp_index = r.cp_index;
-        e.flags = r.flags;
-        e.reserved = 0;
-        e.p_new = r.p_new;
-        out[o + k] = e;
+        falcon_bocd_event q;
+        q.series = series_base + s;
+        q.t = r.t;
+        q.cp_index = r.cp_index;
+        q.flags = r.flags;
+        q.reserved = 0;
+        q.p_new = r.p_new;
+        out[o + k] = q;
     }
     __syncwarp();
-    if (reset && lane == 0) scal[s].ev_count = 0;
+    if (lane == 0) scal[s].ev_count = 0;
 }
 
 // Ring position order -> run-length order; R_t(r) = q_r (1-H) / Zd_t with the cell's
@@ -252,10 +293,24 @@ int check_sticky(falcon_bocd_t h, cudaStream_t st) {
     return FALCON_OK;
 }
 
-int set_device(falcon_bocd_t h) {
-    CUDA_TRY(h, cudaSetDevice(h->cfg.device));
-    return FALCON_OK;
-}
+// Binds the handle's device for the duration of one entry point and restores the caller's
+// current device on every return path.
+struct DeviceGuard {
+    int prev = -1;
+    int set(falcon_bocd_t h) {
+        if (cudaGetDevice(&prev) != cudaSuccess) {
+            cudaGetLastError();
+            prev = -1;
+        }
+        if (prev == h->cfg.device) return FALCON_OK;
+        CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+        return FALCON_OK;
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
 
 }  // namespace
 
@@ -361,7 +416,8 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
         return code;
     };
     int rc;
-    if ((rc = set_device(h)) != 0) return bail(rc);
+    DeviceGuard guard;
+    if ((rc = guard.set(h)) != 0) return bail(rc);
     cudaDeviceProp prop;
     if (cudaGetDeviceProperties(&prop, c.device) != cudaSuccess || prop.major < 10) {
         cudaGetLastError();
@@ -439,12 +495,14 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
     ALLOC(h->d_scal, S * sizeof(SeriesScalars));
     ALLOC(h->d_ev, size_t(S) * c.event_capacity * sizeof(EventRec));
     ALLOC(h->d_err, sizeof(unsigned));
-    ALLOC(h->d_off, (S + 1) * sizeof(int64_t));
-    ALLOC(h->d_meta, 2 * sizeof(int64_t));
+    ALLOC(h->d_off, S * sizeof(int32_t));
+    ALLOC(h->d_blk, ((S + kDrainSpan - 1) / kDrainSpan) * sizeof(int64_t));
+    ALLOC(h->d_blkovf, ((S + kDrainSpan - 1) / kDrainSpan) * sizeof(int32_t));
     ALLOC(dmu0, S * sizeof(double));
     ALLOC(dbeta0, S * sizeof(double));
 #undef ALLOC
-    cudaError_t e3 = cudaSuccess;
+    cudaError_t e3 = cudaHostAlloc((void**)&h->h_meta, 4 * sizeof(int64_t), cudaHostAllocMapped);
+    if (e3 != cudaSuccess) h->h_meta = nullptr;
     if (e3 == cudaSuccess) e3 = cudaMemcpy(h->d_ca, ca.data(), R * sizeof(double2), cudaMemcpyHostToDevice);
     if (e3 == cudaSuccess) e3 = cudaMemcpy(h->d_y, tk.data(), R * sizeof(double), cudaMemcpyHostToDevice);
     if (e3 == cudaSuccess) e3 = cudaMemcpy(h->d_fm, &fmt, sizeof(fmt), cudaMemcpyHostToDevice);
@@ -542,7 +600,8 @@ int falcon_bocd_update_chunk(falcon_bocd_t h, const double* x_dev, int64_t ld, i
         return fail(h, FALCON_EINVAL, "outs->ld < T");
     if (T == 0) return FALCON_OK;
     int rc;
-    if ((rc = set_device(h)) != 0) return rc;
+    DeviceGuard guard;
+    if ((rc = guard.set(h)) != 0) return rc;
     return launch_update(h, x_dev, ld, T, outs ? outs->map_rl : nullptr, outs ? outs->p_new : nullptr,
                          outs ? outs->log_z : nullptr, outs ? outs->ld : 0, (cudaStream_t)stream);
 }
@@ -556,7 +615,8 @@ int falcon_bocd_update_chunk_host(falcon_bocd_t h, const double* x_host, int64_t
     if (want_out && outs->ld < T) return fail(h, FALCON_EINVAL, "outs->ld < T");
     if (T == 0) return FALCON_OK;
     int rc;
-    if ((rc = set_device(h)) != 0) return rc;
+    DeviceGuard guard;
+    if ((rc = guard.set(h)) != 0) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t S = h->cfg.n_series;
     const size_t need = size_t(S) * size_t(T);
@@ -625,66 +685,119 @@ int falcon_bocd_update_chunk_host(falcon_bocd_t h, const double* x_host, int64_t
     return FALCON_OK;
 }
 
+// Enqueues the two drain kernels (count, then gather into `out` unless out == nullptr);
+// meta (device-accessible int64 [4]) receives {total, overflow, error bits, drained}.
+static int enqueue_drain(falcon_bocd_t h, falcon_bocd_event* out, int64_t capacity, int64_t* meta,
+                         cudaStream_t st) {
+    const int64_t S = h->cfg.n_series;
+    const int cap = h->cfg.event_capacity;
+    const int nblk = int((S + kDrainSpan - 1) / kDrainSpan);
+    drain_count_kernel<<<nblk, kDrainThreads, 0, st>>>(h->d_scal, S, cap, h->d_off, h->d_blk, h->d_blkovf);
+    CUDA_TRY(h, cudaGetLastError());
+    const int64_t threads = S * 32;
+    drain_gather_kernel<<<unsigned((threads + 255) / 256), 256, 0, st>>>(
+        h->d_scal, h->d_ev, S, cap, h->d_off, h->d_blk, h->d_blkovf, nblk, h->d_err, capacity, out, meta,
+        h->cfg.series_base);
+    CUDA_TRY(h, cudaGetLastError());
+    return FALCON_OK;
+}
+
+// Memory the drain kernels may write: device / managed memory, or page-locked host memory
+// (mapped into the device address space under UVA).
+static bool device_writable(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged ||
+           (a.type == cudaMemoryTypeHost && a.devicePointer == p);
+}
+
+static int sticky_status(falcon_bocd_t h, int64_t e) {
+    if (e & 1) {
+        h->poisoned = true;
+        return fail(h, FALCON_ENONFINITE, "non-finite observation seen (NaN/Inf in x)");
+    }
+    if (e & 2) {
+        h->poisoned = true;
+        return fail(h, FALCON_ENONFINITE, "non-finite or non-positive prior (beta0 <= 0, or first observation 0)");
+    }
+    if (e & 4) {
+        h->poisoned = true;
+        return fail(h, FALCON_ECUDA, "internal: dynamic shared memory not at the expected address");
+    }
+    return FALCON_OK;
+}
+
 int falcon_bocd_pending_events(falcon_bocd_t h, int64_t* n_out, void* stream) {
     if (!h || !n_out) return FALCON_EINVAL;
+    if (!h->h_meta) return fail(h, FALCON_ENOMEM, "no drain mailbox");
+    DeviceGuard g;
     int rc;
-    if ((rc = set_device(h)) != 0) return rc;
+    if ((rc = g.set(h)) != 0) return rc;
     cudaStream_t st = (cudaStream_t)stream;
-    const int64_t S = h->cfg.n_series;
-    drain_scan_kernel<<<1, 1024, 0, st>>>(h->d_scal, S, h->cfg.event_capacity, h->d_off, h->d_meta);
-    CUDA_TRY(h, cudaGetLastError());
-    int64_t meta[2];
-    CUDA_TRY(h, cudaMemcpyAsync(meta, h->d_meta, sizeof(meta), cudaMemcpyDeviceToHost, st));
+    if ((rc = enqueue_drain(h, nullptr, 0, h->h_meta, st)) != 0) return rc;
     CUDA_TRY(h, cudaStreamSynchronize(st));
-    *n_out = meta[0];
+    *n_out = h->h_meta[0];
     return FALCON_OK;
 }
 
 int falcon_bocd_changepoints(falcon_bocd_t h, falcon_bocd_event* out, int64_t capacity, int64_t* n_out,
                              void* stream) {
     if (!h || !n_out || capacity < 0 || (capacity > 0 && !out)) return FALCON_EINVAL;
+    if (!h->h_meta) return fail(h, FALCON_ENOMEM, "no drain mailbox");
     *n_out = 0;
+    DeviceGuard g;
     int rc;
-    if ((rc = set_device(h)) != 0) return rc;
+    if ((rc = g.set(h)) != 0) return rc;
     cudaStream_t st = (cudaStream_t)stream;
-    if ((rc = check_sticky(h, st)) != 0) return rc;
-    const int64_t S = h->cfg.n_series;
-    const int cap = h->cfg.event_capacity;
-    drain_scan_kernel<<<1, 1024, 0, st>>>(h->d_scal, S, cap, h->d_off, h->d_meta);
-    CUDA_TRY(h, cudaGetLastError());
-    int64_t meta[2];
-    CUDA_TRY(h, cudaMemcpyAsync(meta, h->d_meta, sizeof(meta), cudaMemcpyDeviceToHost, st));
+    // device memory or pinned host memory: the gather kernel writes there directly (one
+    // synchronisation); pageable host memory: staged through a device buffer
+    const bool direct = capacity > 0 && device_writable(out);
+    falcon_bocd_event* dst = out;
+    if (capacity > 0 && !direct) {
+        const int64_t need = std::min<int64_t>(capacity, h->cfg.n_series * int64_t(h->cfg.event_capacity));
+        if (need > h->evout_cap) {
+            CUDA_TRY(h, cudaStreamSynchronize(st));
+            cudaFree(h->d_evout);
+            h->d_evout = nullptr;
+            h->evout_cap = 0;
+            CUDA_TRY(h, cudaMalloc((void**)&h->d_evout, size_t(need) * sizeof(falcon_bocd_event)));
+            h->evout_cap = need;
+        }
+        dst = h->d_evout;
+    }
+    if ((rc = enqueue_drain(h, capacity > 0 ? dst : nullptr, capacity, h->h_meta, st)) != 0) return rc;
     CUDA_TRY(h, cudaStreamSynchronize(st));
-    const int64_t total = meta[0];
+    const int64_t total = h->h_meta[0], ovf = h->h_meta[1], err = h->h_meta[2];
+    if ((rc = sticky_status(h, err)) != 0) return rc;
     if (total > capacity) {
         *n_out = total;
         return fail(h, FALCON_EINVAL, "output capacity smaller than the number of buffered events");
     }
-    const bool dev_out = total > 0 && is_device_ptr(out);
-    falcon_bocd_event* dst = out;
-    if (total > 0 && !dev_out) {
-        if (total > h->evout_cap) {
-            cudaFree(h->d_evout);
-            h->d_evout = nullptr;
-            h->evout_cap = 0;
-            CUDA_TRY(h, cudaMalloc((void**)&h->d_evout, size_t(total) * sizeof(falcon_bocd_event)));
-            h->evout_cap = total;
-        }
-        dst = h->d_evout;
-    }
-    const int64_t threads = S * 32;
-    drain_gather_kernel<<<unsigned((threads + 255) / 256), 256, 0, st>>>(h->d_scal, h->d_ev, S, cap, h->d_off,
-                                                                         dst, 1, h->cfg.series_base);
-    CUDA_TRY(h, cudaGetLastError());
-    if (total > 0 && !dev_out)
+    if (total > 0 && !direct) {
         CUDA_TRY(h, cudaMemcpyAsync(out, dst, size_t(total) * sizeof(falcon_bocd_event), cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(h, cudaStreamSynchronize(st));
+        CUDA_TRY(h, cudaStreamSynchronize(st));
+    }
     *n_out = total;
-    if (meta[1]) {
+    if (ovf) {
         h->err = "event buffer overflow: some events were dropped";
         return FALCON_WARN_EVENTS_DROPPED;
     }
     return FALCON_OK;
+}
+
+int falcon_bocd_changepoints_async(falcon_bocd_t h, falcon_bocd_event* out, int64_t capacity, int64_t* meta,
+                                   void* stream) {
+    if (!h || !meta || capacity < 0 || (capacity > 0 && !out)) return FALCON_EINVAL;
+    if (h->poisoned) return fail(h, FALCON_ESTATE, "handle poisoned by an earlier error");
+    DeviceGuard g;
+    int rc;
+    if ((rc = g.set(h)) != 0) return rc;
+    if (!device_writable(meta) || (capacity > 0 && !device_writable(out)))
+        return fail(h, FALCON_EINVAL, "out / meta must be device memory or page-locked host memory");
+    return enqueue_drain(h, capacity > 0 ? out : nullptr, capacity, meta, (cudaStream_t)stream);
 }
 
 int falcon_bocd_read_posterior(falcon_bocd_t h, int64_t s0, int64_t count, double* logR_out, double* mu_out,
@@ -692,7 +805,8 @@ int falcon_bocd_read_posterior(falcon_bocd_t h, int64_t s0, int64_t count, doubl
     if (!h || s0 < 0 || count < 0 || s0 + count > h->cfg.n_series) return FALCON_EINVAL;
     if (count == 0 || (!logR_out && !mu_out && !beta_out)) return FALCON_OK;
     int rc;
-    if ((rc = set_device(h)) != 0) return rc;
+    DeviceGuard guard;
+    if ((rc = guard.set(h)) != 0) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     if ((rc = check_sticky(h, st)) != 0) return rc;
     const int R = h->cfg.R;
@@ -740,7 +854,8 @@ int falcon_bocd_kernel_shape(falcon_bocd_t h, int32_t* nt, int32_t* j, int32_t* 
 int falcon_bocd_destroy(falcon_bocd_t h) {
     if (!h) return FALCON_OK;
     int rc = FALCON_OK;
-    if (cudaSetDevice(h->cfg.device) == cudaSuccess) {
+    DeviceGuard guard;
+    if (guard.set(h) == FALCON_OK) {
         if (cudaDeviceSynchronize() != cudaSuccess) rc = FALCON_ECUDA;
         if (rc == FALCON_OK && h->d_err) {
             unsigned e = 0;
@@ -750,7 +865,7 @@ int falcon_bocd_destroy(falcon_bocd_t h) {
     }
     cudaGetLastError();
     void* ptrs[] = {h->d_ca, h->d_y, h->d_fm, h->d_ct, h->d_mu, h->d_beta, h->d_a, h->d_w, h->d_scal, h->d_ev, h->d_err, h->d_off,
-                    h->d_meta, h->d_evout, h->d_stage[0], h->d_stage[1], h->d_omap, h->d_opnew, h->d_ologz};
+                    h->d_blk, h->d_blkovf, h->d_evout, h->d_stage[0], h->d_stage[1], h->d_omap, h->d_opnew, h->d_ologz};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (int b = 0; b < 2; ++b) {
@@ -758,6 +873,7 @@ int falcon_bocd_destroy(falcon_bocd_t h) {
         if (h->ev_free[b]) cudaEventDestroy(h->ev_free[b]);
     }
     if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+    if (h->h_meta) cudaFreeHost(h->h_meta);
     delete h;
     return rc;
 }

@@ -54,6 +54,89 @@ def allgather_events(records: torch.Tensor, group=None, dst: int = 0):
     return torch.cat(parts, 0)
 
 
+class ShardedBocd:
+    """Rank `rank`'s shard of a batched BOCD over `n_global` independent series (S:176-177:
+    per-series states are single-owner; one analyzer per node).  The rank owns the
+    contiguous global series [lo, hi) = shard_range(n_global, rank, world) and runs the
+    device kernels on them with no communication; `gather_changepoints` is the run's one
+    exchange.  A rank whose shard is empty (world > n_global) holds no batch.
+
+    batch_factory(n_series, series_base=..., device=..., **bocd_kwargs) builds the local
+    batch (default: bocd.BocdBatch; the CPU tests inject a stand-in)."""
+
+    def __init__(self, n_global: int, rank: int | None = None, world: int | None = None,
+                 device=None, batch_factory=None, group=None, **bocd_kwargs):
+        if rank is None:
+            rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if world is None:
+            world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.n_global, self.rank, self.world, self.group = int(n_global), int(rank), int(world), group
+        self.lo, self.hi = shard_range(self.n_global, self.rank, self.world)
+        if batch_factory is None:
+            from .bocd import BocdBatch as batch_factory
+        self.device = device
+        self.batch = (batch_factory(self.hi - self.lo, series_base=self.lo, device=device, **bocd_kwargs)
+                      if self.hi > self.lo else None)
+
+    @property
+    def n_local(self) -> int:
+        return self.hi - self.lo
+
+    def update_chunk(self, x_local, **kw):
+        """Absorb x_local [n_local][T] (rows = global series lo .. hi-1)."""
+        if self.batch is not None:
+            return self.batch.update_chunk(x_local, **kw)
+        return None
+
+    def local_changepoints(self, device_out: bool):
+        """This shard's drained events as uint8 [n, 40] records and its overflow flag."""
+        if self.batch is None:
+            dev = torch.device("cuda", self.device) if device_out and isinstance(self.device, int) else (
+                self.device if device_out else torch.device("cpu"))
+            return torch.zeros((0, RECORD_BYTES), dtype=torch.uint8, device=dev), False
+        recs, dropped = self.batch.changepoints(device_out=device_out)
+        if not isinstance(recs, torch.Tensor):
+            recs = torch.from_numpy(np.ascontiguousarray(recs).view(np.uint8).reshape(-1, RECORD_BYTES).copy())
+        return recs, bool(dropped)
+
+    def gather_changepoints(self, dst: int = 0):
+        """Drain every shard and all-gather the events (NCCL: device records over NVLink; gloo:
+        host records).  Returns (records uint8 [N, 40] in global (series, t) order, dropped on any
+        rank) on rank `dst`, (None, dropped) elsewhere; single process: the local drain."""
+        multi = dist.is_initialized() and dist.get_world_size(self.group) > 1
+        nccl = multi and dist.get_backend(self.group) == "nccl"
+        recs, dropped = self.local_changepoints(device_out=nccl)
+        if not multi:
+            return recs, dropped
+        out = allgather_events(recs, group=self.group, dst=dst)
+        dev = recs.device
+        dropped_any = max_over_ranks(float(dropped), dev, group=self.group) > 0
+        return out, dropped_any
+
+    def close(self):
+        if self.batch is not None:
+            self.batch.close()
+            self.batch = None
+
+
+def run_sharded(x_source, n_global: int, T: int, chunk: int, device=None, batch_factory=None,
+                group=None, **bocd_kwargs):
+    """Whole sharded run: every rank absorbs T steps of its shard in chunks of `chunk`
+    (x_source(lo, hi, t0, n) -> [hi-lo][n] observations of global series lo..hi-1, steps
+    t0..t0+n-1, generated or loaded where they are used: nothing is scattered), then the
+    events are all-gathered once.  Returns (events as a numpy falcon_bocd_event array in
+    global (series, t) order, dropped) on rank 0, (None, dropped) on other ranks."""
+    sb = ShardedBocd(n_global, device=device, batch_factory=batch_factory, group=group, **bocd_kwargs)
+    try:
+        if sb.n_local:
+            for t0 in range(0, T, chunk):
+                sb.update_chunk(x_source(sb.lo, sb.hi, t0, min(chunk, T - t0)))
+        recs, dropped = sb.gather_changepoints()
+    finally:
+        sb.close()
+    return (records_to_numpy(recs) if recs is not None else None), dropped
+
+
 def records_to_numpy(records: torch.Tensor):
     """uint8 [n, 40] records -> numpy structured array (falcon_bocd_event layout)."""
     from .bocd import EVENT_DTYPE
