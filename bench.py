@@ -22,8 +22,9 @@ One bench "step" = one pass of the whole hot path (every §8(a) row) over one ba
   C2/C3/C4: one falcon_bocd_update_chunk call absorbing --chunk (default 1,000) new
             observations for every local series;
   C5:       --calls (default 1,000) back-to-back T = 1 calls.
-The timed region ends with the change-point drain (falcon_bocd_changepoints; C5: one per
-step) and, for N > 1, the NCCL all-gather of the events; the time is the max over ranks.
+Every step ends with the change-point drain of that step's events (falcon_bocd_changepoints
+into device memory); the timed region ends with the NCCL all-gather of the events (N > 1);
+the time is the max over ranks.
 
 Emits ONE JSON line on rank 0 (DESIGN.md §7 lists every field).
 """
@@ -325,14 +326,15 @@ def main():
     streaming = cfg.name == "C5"
     per_step = args.calls if streaming else args.chunk
     total = (args.warmup + args.steps) * per_step
-    assert total <= cfg.T, "warmup + steps exceed the workload length"
+    n_lat = 300 if streaming else 0  # C5: calls of the per-call latency measurement (after timing)
+    assert total + 3 * n_lat <= cfg.T, "warmup + steps exceed the workload length"
     spec = tracegen.make_spec(cfg, n_series=n_global)
     dtrace = bocd.DeviceTrace(spec, dev)
     if streaming:
         # online layout: one contiguous column of S observations per call (x_t for every series)
-        xs = torch.empty((S, total), dtype=torch.float64, device=dev)
+        xs = torch.empty((S, total + 3 * n_lat), dtype=torch.float64, device=dev)
         dtrace.generate(xs, lo, 0)
-        x = xs.t().contiguous()  # [total][S]
+        x = xs.t().contiguous()  # [total + 3 n_lat][S]
         del xs
         col = lambda k: x[k].view(S, 1)  # noqa: E731  ([S][1], ld = 1)
     else:
@@ -370,7 +372,7 @@ def main():
         n_marks = args.steps * (per_step if streaming else 1)
         ks = [torch.cuda.Event(enable_timing=True) for _ in range(n_marks)]
         ke = [torch.cuda.Event(enable_timing=True) for _ in range(n_marks)]
-        events = []
+        events, drop_any = [], False
         with ClockSampler(local) as clk:
             time.sleep(0.3)
             torch.cuda.synchronize()
@@ -386,14 +388,15 @@ def main():
                         m += 1
                     recs, dropped = b.changepoints(device_out=True)  # each step's result
                     events.append(recs)
+                    drop_any |= dropped
                 else:
                     ks[m].record(stream)
                     b.update_chunk(x[:, kk * per_step:(kk + 1) * per_step])
                     ke[m].record(stream)
                     m += 1
-            if not streaming:
-                recs, dropped = b.changepoints(device_out=True)
-                events.append(recs)
+                    recs, dropped = b.changepoints(device_out=True)  # each step's result
+                    events.append(recs)
+                    drop_any |= dropped
             recs = torch.cat(events) if len(events) > 1 else events[0]
             if world > 1:
                 allgather_events(recs)
@@ -401,7 +404,7 @@ def main():
             torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        return ev_start, ev_end, ks, ke, clk, recs, dropped
+        return ev_start, ev_end, ks, ke, clk, recs, drop_any
 
     ev_start, ev_end, ks, ke, clk, recs, dropped = timed_region()
     cs = clk.summary()
@@ -439,7 +442,7 @@ def main():
 
     latency = None
     if streaming:
-        latency = streaming_latency(b, col, args, cfg, stream)
+        latency = streaming_latency(b, col, args, stream, n_lat)
 
     e2e = None
     if not args.no_e2e:
@@ -452,7 +455,7 @@ def main():
         v, dt = cpu_baseline_run(cfg, spec, n_s, T_s)
         cpu = {"value": v, "unit": UNIT, "cores": host_cores(), "kind": "oracle",
                "sample": _sample_text(cfg, n_s, T_s, dt)}
-    launches = args.steps * (per_step + 2) if streaming else args.steps + 2
+    launches = args.steps * (per_step + 2)  # update kernels + the two drain kernels per step
     n_events = int(recs.shape[0])
     sb.close()
     if rank == 0:
@@ -476,15 +479,13 @@ def main():
     return 0
 
 
-def streaming_latency(b, col, args, cfg, stream, n=300):
+def streaming_latency(b, col, args, stream, n):
     """C5 per-call latency three ways (after the timed region, same handle, data continued):
     device time of the update kernel (CUDA events), host wall time of one call including the
     launch and a stream synchronise, and host wall time of one call followed by a full event
     drain (falcon_bocd_changepoints) every call."""
     import torch
     base = (args.warmup + args.steps) * args.calls
-    avail = cfg.T - base
-    n = max(10, min(n, avail // 3))
     dev_ms, wall_ms, drain_ms = [], [], []
     for i in range(n):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -51,6 +51,8 @@ def main():
     ap.add_argument("--chunk", type=int, default=1000)
     ap.add_argument("--R", type=int, default=1024)
     ap.add_argument("--cmd", default="bench.py --steps 2 --warmup 1 (C3 shape), steady-state launch")
+    ap.add_argument("--config", default="C3", help="writes profiles/ncu_traffic_<config>.json for bench.py")
+    ap.add_argument("--name", default="", help="file stem: profiles/<tag>_ncu_<name>.txt (default top_kernel)")
     a = ap.parse_args()
 
     raw = ncu_csv(a.rep, "--page", "raw")
@@ -102,11 +104,12 @@ def main():
     lines.append(f"DRAM traffic per launch = {(rd + wr) / 1e9:.3f} GB (algorithmic: x {a.series * a.chunk * 8 / 1e9:.3f} GB"
                  f" + state in/out 2 x {3 * a.series * a.R * 8 / 1e9:.3f} GB = {algo / 1e9:.3f} GB)")
     txt = "\n".join(lines) + "\n"
-    path = os.path.join(ROOT, "profiles", f"{a.tag}_ncu_top_kernel.txt")
+    path = os.path.join(ROOT, "profiles", f"{a.tag}_ncu_{a.name or 'top_kernel'}.txt")
     open(path, "w").write(txt)
     json.dump({"kernel": kname, "series": a.series, "chunk": a.chunk, "R": a.R, "bytes_per_launch": rd + wr,
-               "source": f"profiles/{a.tag}_ncu_top_kernel.txt ({os.path.basename(a.rep)})"},
-              open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
+               "units": a.series * a.chunk,
+               "source": f"{os.path.relpath(path, ROOT)} ({os.path.basename(a.rep)})"},
+              open(os.path.join(ROOT, "profiles", f"ncu_traffic_{a.config}.json"), "w"), indent=1)
     print(txt)
 
 
