@@ -34,8 +34,9 @@ def _stream_ptr(stream, device=None):
 class DrainTicket:
     """An enqueued asynchronous drain (BocdBatch.changepoints_async)."""
 
-    def __init__(self, batch, buf, meta, event, stream):
+    def __init__(self, batch, buf, meta, event, stream, device_out=False):
         self._batch, self._buf, self._meta, self._event, self._stream = batch, buf, meta, event, stream
+        self._device_out = device_out
 
     def result(self):
         """Waits for the drain; returns (events, dropped) as BocdBatch.changepoints()."""
@@ -43,12 +44,16 @@ class DrainTicket:
         total, ovf, err, drained = (int(v) for v in self._meta.tolist())
         self._batch._ev_hint = max(self._batch._ev_hint, total)
         if not drained:  # capacity too small or a sticky error: nothing changed, drain (or raise) now
-            return self._batch.changepoints(self._stream)
+            return self._batch.changepoints(self._stream, device_out=self._device_out)
+        if self._device_out:
+            return self._buf[:total].clone(), bool(ovf)
         return self._buf[:total].numpy().reshape(-1).view(EVENT_DTYPE).copy(), bool(ovf)
 
 
 class BocdBatch:
     """falcon_bocd_create / _update_chunk / _changepoints / _read_posterior / _destroy."""
+
+    N_TICKETS = 4  # asynchronous drains that may be outstanding at once
 
     def __init__(self, n_series: int, R: int = 1024, hazard: float = 1.0 / 250.0,
                  kappa0: float = 1.0, alpha0: float = 1.0, mu0=0.0, beta0=1.0,
@@ -93,7 +98,7 @@ class BocdBatch:
         self.event_capacity = int(event_capacity)
         self._evbufs = {}
         self._ev_hint = min(self.n_series * self.event_capacity, 4096)
-        self._metas = [torch.zeros(4, dtype=torch.int64, pin_memory=True) for _ in range(2)]
+        self._metas = [torch.zeros(4, dtype=torch.int64, pin_memory=True) for _ in range(self.N_TICKETS)]
         self._ticket_slot = 0
 
     # -- hot path ---------------------------------------------------------------
@@ -146,6 +151,13 @@ class BocdBatch:
             self._evbufs[key] = buf
         return buf
 
+    def reserve_events(self, n: int, device_out: bool = False):
+        """Pre-allocate every drain buffer for n events (keeps allocations out of a timed loop)."""
+        where = "device" if device_out else "host"
+        for slot in [-1, *range(self.N_TICKETS)]:
+            self._event_buffer(where, n, slot)
+        self._ev_hint = max(self._ev_hint, n // 2)
+
     def changepoints(self, stream=None, device_out: bool = False):
         """Drain buffered events in (series, t) order (falcon_bocd_changepoints).  Returns
         (events, dropped) where events is a numpy structured array (host) or a uint8 device
@@ -154,7 +166,7 @@ class BocdBatch:
         n = ctypes.c_int64()
         need = self._ev_hint
         while True:
-            buf = self._event_buffer("device" if device_out else "host", need)
+            buf = self._event_buffer("device" if device_out else "host", need, slot=-1)
             rc = L.falcon_bocd_changepoints(self._h, ctypes.c_void_p(buf.data_ptr()), buf.shape[0],
                                             ctypes.byref(n), _stream_ptr(stream, self.device))
             if rc == N.FALCON_EINVAL and n.value > buf.shape[0]:
@@ -168,22 +180,22 @@ class BocdBatch:
             return buf[:k].clone(), rc == N.FALCON_WARN_EVENTS_DROPPED
         return buf[:k].numpy().reshape(-1).view(EVENT_DTYPE).copy(), rc == N.FALCON_WARN_EVENTS_DROPPED
 
-    def changepoints_async(self, stream=None):
+    def changepoints_async(self, stream=None, device_out: bool = False):
         """Enqueue a drain on `stream` without synchronising (falcon_bocd_changepoints_async);
-        the events land in page-locked host memory.  Returns a DrainTicket whose result()
-        waits for it and returns (events, dropped) like changepoints().  Two tickets may be
-        outstanding at a time (double-buffered)."""
+        the events land in page-locked host memory (or, device_out, in device memory).  Returns
+        a DrainTicket whose result() waits for it and returns (events, dropped) like
+        changepoints().  Up to N_TICKETS tickets may be outstanding at a time."""
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
         slot = self._ticket_slot
-        self._ticket_slot ^= 1
-        buf = self._event_buffer("host", self._ev_hint, slot)
+        self._ticket_slot = (slot + 1) % self.N_TICKETS
+        buf = self._event_buffer("device" if device_out else "host", 2 * self._ev_hint, slot)
         meta = self._metas[slot]
         N.check(N.lib().falcon_bocd_changepoints_async(self._h, ctypes.c_void_p(buf.data_ptr()), buf.shape[0],
                                                        ctypes.c_void_p(meta.data_ptr()),
                                                        ctypes.c_void_p(st.cuda_stream)), self._h)
         ev = torch.cuda.Event()
         ev.record(st)
-        return DrainTicket(self, buf, meta, ev, stream)
+        return DrainTicket(self, buf, meta, ev, stream, device_out)
 
     def read_posterior(self, s0: int = 0, count: int | None = None, stream=None):
         """(logR, mu, beta) as device tensors [count][R] in run-length order."""

@@ -67,41 +67,21 @@ namespace fbocd {
 constexpr int kTile = 256;     // x steps per shared-memory tile (2 KB)
 constexpr int kTileP = 64;     // persistent (streaming) kernels: calls of <= 64 steps
 constexpr int kRebase = 256;   // generic kernels: global steps between frame rebases (ROT: every NT)
-#ifndef FALCON_BOCD_KG
-#define FALCON_BOCD_KG 2
-#endif
-constexpr int kG = FALCON_BOCD_KG;  // cells per interleaved group (ILP)
-#ifndef FALCON_BOCD_STEP_UNROLL
-#define FALCON_BOCD_STEP_UNROLL 1
-#endif
-constexpr int kStepUnroll = FALCON_BOCD_STEP_UNROLL;  // steps per unrolled loop body
+constexpr int kG = 2;          // cells per interleaved group (ILP; 4 and 8 measured slower)
 // K0_t = round(l0_t) is clamped to +-kK0Max so that |N_t| < 2^14 and 256 Dc stays below 2^31
 // (at most 512 steps between rebases)
-constexpr double kK0Max = FALCON_BOCD_EXPBITS == 9 ? 4096.0 : 8192.0;
-// FLOOR (default): a cell's joint below 2^-1021 of the step reference is floored to
-// [2^-1021, 2^-1019) by a two-sided integer clamp (no select per cell), and impossible cells
-// (run lengths longer than the data seen) carry the finite offset kImpossible instead of
-// -inf (read_posterior still reports -inf for them).  FALCON_BOCD_FLOOR=0: exact zeros.
-#ifndef FALCON_BOCD_FLOOR
-#define FALCON_BOCD_FLOOR 1
-#endif
-constexpr bool kFloor = FALCON_BOCD_FLOOR != 0;
-#ifndef FALCON_BOCD_PRED_PUBLISH
-#define FALCON_BOCD_PRED_PUBLISH 1  // only the lanes whose published cells the tail reads store them (0.7%)
-#endif
-#ifndef FALCON_BOCD_KT_I2F
-#define FALCON_BOCD_KT_I2F 1  // k via I2F.F64 (0: the 2^52 magic; 0.8% slower, same bits)
-#endif
-#ifndef FALCON_BOCD_OWNER_SELECT
-#define FALCON_BOCD_OWNER_SELECT 1  // 0: one divergent owner block (measured 0.3% slower)
-#endif
+constexpr double kK0Max = 8192.0;
+// A cell's joint below 2^-1021 of the step reference is floored to [2^-1021, 2^-1019) by a
+// two-sided integer clamp (no select per cell), and impossible cells (run lengths longer than
+// the data seen) carry the finite offset kImpossible instead of -inf (read_posterior still
+// reports -inf for them).
 constexpr double kImpossible = -1048576.0;  // -2^20: 256 |l - Dc| stays below 2^31
 // A MERGE bucket mass below this (floored dead / impossible cells only) is an exact 0, so run
 // lengths longer than the data seen stay impossible.
 constexpr double kDeadMass = 0x1p-1015;
 __device__ __forceinline__ double bucket_mass(double qA, double qB) {
     const double v = qA + qB;
-    return (kFloor && v < kDeadMass) ? 0.0 : v;
+    return v < kDeadMass ? 0.0 : v;
 }
 
 struct SeriesScalars {  // per-series state carried between calls (HBM), 48 B
@@ -154,15 +134,27 @@ struct KParams {
     int tma_ok;  // x base 16-B aligned and ld even
 };
 
-template <int NT, int TILE = kTile>
+// Series interleaving.  The FULL kernels with at least two series per CTA interleave IL = 2
+// series lane by lane (series = lane & 1): at every step all series of a CTA read the same
+// per-r table rows (the ring position -> run length map depends only on the thread index and
+// t), so the two lanes of a pair share each table entry and a warp's table reads touch half
+// as many distinct rows (profiles/r02_smem_probe.jsonl: a pair-shared 16-B row costs half the
+// shared-memory wavefronts of 32 distinct rows).  A "team" is the IL series that share warps;
+// it synchronises as one (named barrier per team).  IL = 1 otherwise.
+__host__ __device__ constexpr int series_il(int nt, bool full, int spb) { return (full && spb >= 2 && nt >= 32) ? 2 : 1; }
+
+// per-series partial sums of a step: one per (warp, series) pair
+__host__ __device__ constexpr int n_partials(int nt, int il) { return nt * il / 32 > 0 ? nt * il / 32 : 1; }
+
+template <int NT, int TILE = kTile, int IL = 1>
 struct __align__(16) GroupSmem {
     double xbuf[2][TILE];
     int kbuf[2][TILE];  // K0_t = round(l0_t) of the tile's steps
     // red2 / red1 / spec are double-buffered by step parity: a warp that runs ahead into
     // step t+1 cannot overwrite what a slower warp still reads after barrier t
-    double red2[2][NT / 32 > 0 ? NT / 32 : 1];
-    unsigned long long red1[2][NT / 32 > 0 ? NT / 32 : 1];  // EAGER argmax keys
-    unsigned long long red3[NT / 32 > 0 ? NT / 32 : 1];     // on-demand argmax (event steps)
+    double red2[2][n_partials(NT, IL)];
+    unsigned long long red1[2][n_partials(NT, IL)];  // EAGER argmax keys
+    unsigned long long red3[n_partials(NT, IL)];     // on-demand argmax (event steps)
     // generic kernels: q' of the cells r = R-2, R-1, 0 and G - alpha lg beta' of r = R-2;
     // ROT kernels: e0 / l0 hold q' / lg beta' of every thread's slot 0, entry NT = slot 1 of
     // thread 0, entry NT+1 (e0) = slot J-1 of thread NT-1 (the cells the tail needs)
@@ -219,12 +211,23 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
         : "memory");
 }
 
-template <int NT>
-__device__ __forceinline__ void group_sync(int g) {
-    if constexpr (NT == 32) {
+// barrier of one team (NTEAM threads = IL series x NT)
+template <int NTEAM>
+__device__ __forceinline__ void team_sync(int team) {
+    if constexpr (NTEAM == 32) {
         __syncwarp();
     } else {
-        asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(NT) : "memory");
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(NTEAM) : "memory");
+    }
+}
+
+// Fixed-order pairwise sum of the W per-warp partials (deterministic)
+template <int W>
+__device__ __forceinline__ double tree_sum(const double* p) {
+    if constexpr (W == 1) {
+        return p[0];
+    } else {
+        return tree_sum<W / 2>(p) + tree_sum<W / 2>(p + W / 2);
     }
 }
 
@@ -239,16 +242,27 @@ __device__ __forceinline__ double key_val(unsigned long long k) {
     return __longlong_as_double(static_cast<long long>(k & ~0xFFFull));
 }
 
-// 64-bit max over the warp with two 32-bit REDUX passes
+// 64-bit max over the lanes of one series in a warp: IL = 1, two 32-bit REDUX passes over the
+// warp; IL = 2 (series = lane & 1), an xor butterfly over the lanes of the same parity
+template <int IL>
 __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long k) {
-    const unsigned hi = unsigned(k >> 32);
-    const unsigned hmax = __reduce_max_sync(0xffffffffu, hi);
-    const unsigned lmax = __reduce_max_sync(0xffffffffu, hi == hmax ? unsigned(k) : 0u);
-    return (static_cast<unsigned long long>(hmax) << 32) | lmax;
+    if constexpr (IL == 1) {
+        const unsigned hi = unsigned(k >> 32);
+        const unsigned hmax = __reduce_max_sync(0xffffffffu, hi);
+        const unsigned lmax = __reduce_max_sync(0xffffffffu, hi == hmax ? unsigned(k) : 0u);
+        return (static_cast<unsigned long long>(hmax) << 32) | lmax;
+    } else {
+#pragma unroll
+        for (int o = 16; o >= IL; o >>= 1) {
+            const unsigned long long v = __shfl_xor_sync(0xffffffffu, k, o);
+            k = v > k ? v : k;
+        }
+        return k;
+    }
 }
 
-template <int NT, int TILE>
-__device__ __forceinline__ void issue_tile_tma(GroupSmem<NT, TILE>& gs, const double* xrow, int k, int T) {
+template <int NT, int TILE, int IL>
+__device__ __forceinline__ void issue_tile_tma(GroupSmem<NT, TILE, IL>& gs, const double* xrow, int k, int T) {
     const int base = k * TILE;
     const int n = min(TILE, T - base);
     fence_proxy_async();
@@ -266,9 +280,9 @@ __device__ __forceinline__ bool tile_tma_ok(const KParams& P, int k) {
 // TAB2: the per-r tables are stored twice (entries r and r+R) so the ring index
 // (t - p) mod R becomes (t - p + R) with no masking and compile-time offsets per cell.
 // per group: GroupSmem and (PREF) the prefetch buffer [mu R][beta R][a R][scalars]
-template <int NT, bool PREF>
+template <int NT, bool PREF, int IL>
 __host__ __device__ constexpr size_t group_bytes(int R) {
-    return sizeof(GroupSmem<NT, PREF ? kTileP : kTile>) +
+    return sizeof(GroupSmem<NT, PREF ? kTileP : kTile, IL>) +
            (PREF ? ((3 * size_t(R) * sizeof(double) + sizeof(SeriesScalars) + 15) & ~size_t(15)) : 0);
 }
 // bytes of the per-r tables ({G_{r+1}, alpha_{r+1}} and y_r) for `entries` table rows
@@ -296,7 +310,7 @@ __device__ __forceinline__ double safe_log2(double v) {
     const bool huge = v > 0x1p+900;
     const double s = tiny ? v * 0x1p+600 : (huge ? v * 0x1p-600 : v);
     const double l = fast_log2(s, 0x800u) + (tiny ? -600.0 : (huge ? 600.0 : 0.0));
-    return v > 0.0 ? l : (kFloor ? kImpossible : -__longlong_as_double(0x7FF0000000000000ll));
+    return v > 0.0 ? l : kImpossible;
 }
 
 // Prior predictive of x (A1 + A2 of the prior, log2 units): the tile's exponent
@@ -339,7 +353,7 @@ constexpr unsigned kFmBase = 0x800u;
 // The persistent prefetching kernels (HBM-bound streaming) take 4 copies and 64-step x tiles
 // so that two CTAs with their prefetch buffers still fit one SM.
 __host__ __device__ constexpr int cell_ec(bool full, int r_full, bool pref) {
-    return (pref ? 4 : ((full && r_full <= 1024) ? 16 : 8)) >> (kCellEB - 8);
+    return pref ? 4 : ((full && r_full <= 1024) ? 16 : 8);
 }
 __host__ __device__ constexpr unsigned bocd_fm_bytes(int ec, int lb) {
     return (lb == 8 ? (ec == 16 ? cell_tables_end<16, 8>() : ec == 8 ? cell_tables_end<8, 8>()
@@ -352,8 +366,7 @@ static_assert(kFmBase + kFmSmemBytes - 2048u <= kCellExpBase, "fast-math tables 
 
 // exp2 of a cell: q' = 2^(ell - Dc) with C7 = 1.5 2^52 + 2^31 - 256 Dc (cellmath.cuh's
 // reduction with the frame folded into the rounding constant).  Below 2^-1021: floored to
-// [2^-1021, 2^-1019) (FLOOR) or exactly 0 (also for ell = -inf); exponent clamped at +1000
-// (DESIGN.md §3).  The cell loop evaluates
+// [2^-1021, 2^-1019); exponent clamped at +1000.  The cell loop evaluates
 // the same operations stage by stage; the on-demand MAP recomputation calls this and must
 // agree bit for bit.
 template <int EC>
@@ -362,20 +375,13 @@ __device__ __forceinline__ double cell_exp2(double ell, double C7, unsigned lbe)
     const unsigned ki = unsigned(__double2loint(zf));
     const double re = fma(zf - C7, -1.0 / kCellExpScale, ell);
     const double T = cell_exp_entry<EC>(ki, lbe);
-    double p;
-    if constexpr (kCellEB == 8) {
-        p = fma(re, kCellExpQ3, c_cell[11]);
-        p = fma(p, re, c_cell[10]);
-        p = fma(p, re, c_cell[9]);
-    } else {
-        p = fma(re, kCellExpQ2i, c_cell[10]);
-        p = fma(p, re, c_cell[9]);
-    }
+    double p = fma(re, kCellExpQ3, c_cell[11]);
+    p = fma(p, re, c_cell[10]);
+    p = fma(p, re, c_cell[9]);
     const double qq = p * re;
-    const bool dead = ki < kCellExpLo;
-    const unsigned kc = kFloor ? max(min(ki, kCellExpHi), kCellExpLo) : min(ki, kCellExpHi);
+    const unsigned kc = max(min(ki, kCellExpHi), kCellExpLo);
     const double Ts = __hiloint2double(int(kc * (1048576u >> kCellEB)) + __double2hiint(T), __double2loint(T));
-    return (!kFloor && dead) ? 0.0 : fma(Ts, qq, Ts);
+    return fma(Ts, qq, Ts);
 }
 
 // PREF is used for power-of-two R up to 1024, where the buffer (24 B x R per series) fits
@@ -407,7 +413,11 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     constexpr unsigned kCaBase = kDynBase + bocd_fm_bytes(EC, LB);
     constexpr unsigned kYBase = kCaBase + unsigned(NT * J + NT) * 16u;
     constexpr int TILE = PREF ? kTileP : kTile;
-    using GS = GroupSmem<NT, TILE>;
+    constexpr int IL = series_il(NT, FULL, SPB);  // series interleaved per warp (lane & 1)
+    constexpr int NTEAM = NT * IL;                // threads of one team (IL series)
+    constexpr int W = n_partials(NT, IL);         // per-series partials of a step (one per warp)
+    static_assert(SPB % IL == 0, "series per CTA must be a multiple of the interleave");
+    using GS = GroupSmem<NT, TILE, IL>;
     const int R = FULL ? NT * J : P.R;
     const int RT = table_entries<NT, J, FULL, TAB2>(R);
     // dynamic shared memory: [fast-math tables, cell tables (bocd_fm_bytes)][per-r tables][groups]
@@ -430,11 +440,16 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         for (int k = threadIdx.x; k < (1 << LB); k += blockDim.x) lg[k] = src[k];
     }
     const unsigned lb = 8u * (threadIdx.x & unsigned(EC - 1));  // exp2 table copy of this lane
-    const int g = threadIdx.x / NT;
-    const int i = threadIdx.x % NT;
     const int lane = threadIdx.x & 31;
-    const int w = i >> 5;
-    GS& gs = *reinterpret_cast<GS*>(gbase + size_t(g) * group_bytes<NT, PREF>(R));
+    const int team = threadIdx.x / NTEAM;
+    const int tt = threadIdx.x % NTEAM;
+    // series g of the CTA and the thread's index i within its series (consecutive i = the
+    // lanes of one parity within a warp, then the next warp)
+    const int g = IL == 2 ? team * 2 + (lane & 1) : team;
+    const int i = IL == 2 ? ((tt >> 5) << 4) + (lane >> 1) : tt;
+    const int w = IL == 2 ? (tt >> 5) : (i >> 5);  // this series' partial index
+    const bool red_lane = IL == 2 ? lane < 2 : lane == 0;  // writes the warp's partial of its series
+    GS& gs = *reinterpret_cast<GS*>(gbase + size_t(g) * group_bytes<NT, PREF, IL>(R));
     // PREF: the prefetched next-unit state [mu R][beta R][a R][SeriesScalars], position order
     double* const pf = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(&gs) + sizeof(GS));
     SeriesScalars* const pf_sc = reinterpret_cast<SeriesScalars*>(pf + 3 * size_t(R));
@@ -451,7 +466,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     const bool any_out = P.out_map || P.out_pnew || P.out_logz;  // per-step outputs requested
     // argmax-eligible run lengths: MERGE r <= R-3 (slot R-1 is the bucket), DROP r <= R-2
     const int r_elig = merge ? R - 3 : R - 2;
-    const double ninf = kFloor ? kImpossible : -__longlong_as_double(0x7FF0000000000000ll);
+    const double ninf = kImpossible;
     unsigned xphase = 0u;  // parity of the two x-tile mbarriers (bit b: mbar[b])
     unsigned sphase = 0u;  // parity of the state mbarrier
     auto issue_state = [&](int64_t sn) {  // thread 0 of the group: next unit's state -> pf
@@ -464,17 +479,21 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         tma_load_1d(pf + 2 * size_t(R), P.st_a + sn * R, unsigned(rb), &gs.mbar_st);
         tma_load_1d(pf_sc, P.scal + sn, unsigned(sizeof(SeriesScalars)), &gs.mbar_st);
     };
-    if constexpr (PREF) {
+    if constexpr (PREF) {  // (a series past the end prefetches the last series' rows; see below)
         const int64_t s0 = int64_t(blockIdx.x) * SPB + g;
-        if (i == 0 && P.t0 > 0 && blockIdx.x < nunits && s0 < P.S) issue_state(s0);
+        if (i == 0 && P.t0 > 0 && blockIdx.x < nunits && int64_t(blockIdx.x) * SPB + int64_t(team) * IL < P.S)
+            issue_state(s0 < P.S ? s0 : P.S - 1);
     }
 
     for (int64_t u = blockIdx.x; u < nunits; u += PERSIST ? int64_t(gridDim.x) : nunits) {
-        const int64_t s = u * SPB + g;
-        if (s >= P.S) break;  // group-uniform; later units only have larger s
+        // team-uniform exit: later units only have larger s.  A series past the end in a team
+        // that still has a live one runs on a copy of the last series' rows and writes nothing.
+        if (u * SPB + int64_t(team) * IL >= P.S) break;
+        const bool act = u * SPB + g < P.S;
+        const int64_t s = act ? u * SPB + g : P.S - 1;
         const double* xrow = P.x + s * P.ld;
         // Prefetch tile 0 (TMA) as early as possible.
-        if (i == 0 && ntiles > 0 && tile_tma_ok<TILE>(P, 0)) issue_tile_tma<NT, TILE>(gs, xrow, 0, P.T);
+        if (i == 0 && ntiles > 0 && tile_tma_ok<TILE>(P, 0)) issue_tile_tma<NT, TILE, IL>(gs, xrow, 0, P.T);
 
         // ---- load or initialise the state --------------------------------
         double mu[J], be[J], a[J];
@@ -518,7 +537,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             gs.flags = sc.flags | (ok ? 0 : 2) | (fm_ok ? 0 : 4);
             gs.dc0 = sc.dc;
         }
-        group_sync<NT>(g);
+        team_sync<NTEAM>(team);
         // the prior and the rarely used per-series scalars stay in shared memory (gs) so
         // that the step loop keeps its registers for the cells
         int zexp = ((__double2hiint(gs.zd_prev) >> 20) & 0x7FF) - 1023;  // binary exponent of Zd_{t-1}
@@ -566,10 +585,11 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             if (BUCKET_PRED) L0p = cell_log2<EC, LB>(be[0]);  // = the previous step's lg beta' of slot 0
         }
         if constexpr (PREF) {
-            // pf is free once every thread of the group has read it: prefetch the next unit
-            group_sync<NT>(g);
-            const int64_t sn = s + int64_t(gridDim.x) * SPB;
-            if (i == 0 && P.t0 > 0 && sn < P.S) issue_state(sn);
+            // pf is free once every thread of the team has read it: prefetch the next unit
+            team_sync<NTEAM>(team);
+            const int64_t un = u + int64_t(gridDim.x);
+            const int64_t sn = un * SPB + g;
+            if (i == 0 && P.t0 > 0 && un * SPB + int64_t(team) * IL < P.S) issue_state(sn < P.S ? sn : P.S - 1);
         }
         bool nonfinite = false;
         if (i == 0 && P.out_logz) gs.lzd_prev = fast_log2(gs.zd_prev, kFmBase);
@@ -580,13 +600,13 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             const int buf = k & 1;
             // prefetch the next tile into the other buffer (its previous readers all
             // passed at least one group barrier since their last read)
-            if (i == 0 && k + 1 < ntiles && tile_tma_ok<TILE>(P, k + 1)) issue_tile_tma<NT, TILE>(gs, xrow, k + 1, P.T);
+            if (i == 0 && k + 1 < ntiles && tile_tma_ok<TILE>(P, k + 1)) issue_tile_tma<NT, TILE, IL>(gs, xrow, k + 1, P.T);
             if (tile_tma_ok<TILE>(P, k)) {
                 mbar_wait(&gs.mbar[buf], (xphase >> buf) & 1u);
                 xphase ^= 1u << buf;
             } else {
                 for (int q = i; q < n; q += NT) gs.xbuf[buf][q] = xrow[base + q];
-                group_sync<NT>(g);
+                team_sync<NTEAM>(team);
             }
             // the tile's exponent references K0_t = round(l0_t), spread over the group
             for (int q = i; q < n; q += NT) {
@@ -595,13 +615,12 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 const double l0 = prior_l2(xq, gs.mu0, gs.beta0, gs.aprior, s_ca[0], s_y[0], kFmBase);
                 gs.kbuf[buf][q] = __double2int_rn(fmin(fmax(l0, -kK0Max), kK0Max));
             }
-            group_sync<NT>(g);
+            team_sync<NTEAM>(team);
             // ROT: the tile's steps run in segments that end at a rotation step (iB = NT-1); the
             // slot rotation, the fold of the pending weights and the frame rebase run between
             // segments (register permutations outside the step loop: no copies inside it)
             for (int q = 0; q < n;) {
             const int qe = ROT ? min(n, q + (NT - iB)) : n;
-#pragma unroll kStepUnroll
             for (; q < qe; ++q) {
                 const int tl = base + q;
                 const int64_t t = P.t0 + tl;
@@ -611,7 +630,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 if (!ROT && (unsigned(t) & (kRebase - 1)) == 0u) {  // generic: rebase at t % kRebase == 0
                     const double dcd = double(dc);
 #pragma unroll
-                    for (int j = 0; j < J; ++j) a[j] = kFloor ? fmax(a[j] - dcd, kImpossible) : a[j] - dcd;
+                    for (int j = 0; j < J; ++j) a[j] = fmax(a[j] - dcd, kImpossible);
                     dc = 0;
                 }
                 dc += K0 + zexp;  // Dc_t = Dc_{t-1} + N_t
@@ -688,11 +707,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                                                                  int(tb[kk] & 0x7FF00000u),
                                                              __double2loint(lt[kk].x));
                         rl[kk] = fma(bn[kk], invs, -1.0);
-#if FALCON_BOCD_KT_I2F
-                        kt[kk] = __int2double_rn(int(tb[kk] >> 20) - 1023) + lt[kk].y;
-#else
-                        kt[kk] = (__hiloint2double(0x43300000, int(tb[kk] >> 20)) - 4503599627371519.0) + lt[kk].y;
-#endif
+                        kt[kk] = __int2double_rn(int(tb[kk] >> 20) - 1023) + lt[kk].y;  // I2F.F64: k exact
                     }
                     {
                         constexpr int o = 3 * (LB - 8);
@@ -717,11 +732,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                             }
                         }
                         if constexpr (ROT) {  // lg beta' of slot 0 (and slot 1 of thread 0) for the bucket
-#if FALCON_BOCD_PRED_PUBLISH
                             if (j == 0 && i == iB + 1) gs.l0[par][i] = Ln;  // only the bucket's is read
-#else
-                            if (j == 0) gs.l0[par][i] = Ln;
-#endif
                             if (J > 1 && j == 1 && i == 0) gs.l0[par][NT] = Ln;
                         } else {
                             if (merge && i + NT * j == kA) gs.spec[par][3] = fma(-ca[kk].y, Ln, ca[kk].x);
@@ -739,12 +750,9 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                         Tv[kk] = cell_exp_entry<EC>(ki[kk], lb);
                     }
 #pragma unroll
-                    for (int kk = 0; kk < G; ++kk)
-                        pe[kk] = kCellEB == 8 ? fma(re[kk], kCellExpQ3, c_cell[11]) : fma(re[kk], kCellExpQ2i, c_cell[10]);
-                    if constexpr (kCellEB == 8) {
+                    for (int kk = 0; kk < G; ++kk) pe[kk] = fma(re[kk], kCellExpQ3, c_cell[11]);
 #pragma unroll
-                        for (int kk = 0; kk < G; ++kk) pe[kk] = fma(pe[kk], re[kk], c_cell[10]);
-                    }
+                    for (int kk = 0; kk < G; ++kk) pe[kk] = fma(pe[kk], re[kk], c_cell[10]);
 #pragma unroll
                     for (int kk = 0; kk < G; ++kk) pe[kk] = fma(pe[kk], re[kk], c_cell[9]);
 #pragma unroll
@@ -752,13 +760,12 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                         const int j = j0 + kk;
                         const int p = i + NT * j;
                         const double qq = pe[kk] * re[kk];
-                        // 2^e, e = floor(n/256) for n = ki - 2^31: exactly 0 below 2^-1021, e clamped
-                        // at +1000; hi word = kc * 2^12 + hi(T'_j) (cellmath.cuh)
-                        const bool dead = ki[kk] < kCellExpLo;
-                        const unsigned kc = kFloor ? max(min(ki[kk], kCellExpHi), kCellExpLo) : min(ki[kk], kCellExpHi);
+                        // 2^e, e = floor(n/256) for n = ki - 2^31, floored at 2^-1021 and clamped at
+                        // +1000; hi word = kc * 2^12 + hi(T'_j) (cellmath.cuh)
+                        const unsigned kc = max(min(ki[kk], kCellExpHi), kCellExpLo);
                         const double Ts = __hiloint2double(int(kc * (1048576u >> kCellEB)) + __double2hiint(Tv[kk]),
                                                            __double2loint(Tv[kk]));
-                        double E = (!kFloor && dead) ? 0.0 : fma(Ts, qq, Ts);
+                        double E = fma(Ts, qq, Ts);
                         if (ROT && j == 0) E *= wq;  // slot 0's pending weight (new CP / bucket mass)
                         if (FULL || p < R) {
                             sum += E;
@@ -770,11 +777,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                             }
                             // the tail's cells, published by their owners
                             if constexpr (ROT) {
-#if FALCON_BOCD_PRED_PUBLISH
                                 if (j == 0 && unsigned(i - iB + 1) <= 2u) gs.e0[par][i] = E;  // iB-1 .. iB+1
-#else
-                                if (j == 0) gs.e0[par][i] = E;
-#endif
                                 if (J > 1 && j == 1 && i == 0) gs.e0[par][NT] = E;
                                 if (j == J - 1 && i == NT - 1) gs.e0[par][NT + 1] = E;
                             } else {
@@ -785,28 +788,28 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                         }
                     }
                 }
-                // ---- group sum (and, EAGER, argmax): the step's only barrier ------------
+                // ---- series sum (and, EAGER, argmax): the step's only barrier -----------
+                // (xor butterfly over the series' lanes of the warp, then a fixed-order
+                // pairwise sum of the W per-warp partials: deterministic)
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-                if constexpr (EAGER) key = warp_max_u64(key);
-                if constexpr (NT > 32) {
-                    if (lane == 0) {
+                for (int o = 16; o >= IL; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+                if constexpr (EAGER) key = warp_max_u64<IL>(key);
+                if constexpr (W > 1) {
+                    if (red_lane) {
                         gs.red2[par][w] = sum;
                         if (EAGER) gs.red1[par][w] = key;
                     }
-                    group_sync<NT>(g);
-                    sum = gs.red2[par][0];
-#pragma unroll
-                    for (int ww = 1; ww < NT / 32; ++ww) sum += gs.red2[par][ww];
+                    team_sync<NTEAM>(team);
+                    sum = tree_sum<W>(gs.red2[par]);
                     if constexpr (EAGER) {
 #pragma unroll
-                        for (int ww = 0; ww < NT / 32; ++ww) {
+                        for (int ww = 0; ww < W; ++ww) {
                             const unsigned long long o = gs.red1[par][ww];
                             key = o > key ? o : key;
                         }
                     }
                 } else {
-                    group_sync<NT>(g);
+                    team_sync<NTEAM>(team);
                 }
                 // ---- the scalar tail (A5-A8): group-uniform, no transcendentals -----------
                 const double Z = sum;
@@ -829,7 +832,6 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 // step's critical path), folded into a at the next rotation step.  Generic: one
                 // divergent block for the one or two owner lanes (one shared log2 pass).
                 if constexpr (ROT) {
-#if FALCON_BOCD_OWNER_SELECT
                     const bool ownB = (i == iB);
                     const bool ownA = merge && (i == iB + 1);  // iB = NT-1: thread 0, slot 1 (rotation)
                     const double dcd = double(dc);
@@ -842,23 +844,6 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     be[0] = ownB ? b0 : be[0];
                     a[0] = ownB ? aB : (ownA ? aA : a[0]);
                     wq = ownB ? wB : (ownA ? wA : wq);
-#else
-                    // one short divergent block for the one or two owner lanes (no log: the new
-                    // masses are pending weights), skipped by the other warps of the group
-                    if (unsigned(i - iB) <= (merge ? 1u : 0u)) {  // i == iB (CP) or i == iB + 1 (bucket)
-                        const double dcd = double(dc);
-                        if (i == iB) {
-                            mu[0] = gs.mu0;
-                            be[0] = gs.beta0;
-                            a[0] = gs.aprior + dcd;
-                            wq = P.hr * Z;
-                        } else {  // iB = NT-1: thread 0, slot 1 (rotation block)
-                            const double2 cA = s_ca[R - 2];  // G_{R-1} - alpha_{R-1} lg beta' of cell kA
-                            a[0] = dcd - fma(-cA.y, gs.l0[par][iB + 1], cA.x);
-                            wq = bucket_mass(qA, qB);
-                        }
-                    }
-#endif
                 } else {
                 const bool ownB = (unsigned(kB) % NT) == unsigned(i);
                 const bool ownA = merge && ((unsigned(kA) % NT) == unsigned(i));
@@ -879,7 +864,10 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 if (i == 0) gs.zd_prev = Zd;
                 // ---- rare path (group-uniform): MAP run length r* (A7), events (A8), per-step
                 // outputs ----------------------------------------------------------------
-                if (EAGER || (fl & P.ev_mask) || any_out) {
+                // (team-uniform: the on-demand argmax below synchronises the team; with IL = 2
+                // every warp holds lanes of both series, so a warp vote sees the whole team)
+                const bool ev_team = IL == 2 ? __any_sync(0xffffffffu, (fl & P.ev_mask) != 0u) : (fl & P.ev_mask) != 0u;
+                if (EAGER || ev_team || any_out) {
                     int r_ex = -1;
                     double qex = 0.0;
                     if constexpr (EAGER) {
@@ -887,7 +875,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                             r_ex = key_r(key);
                             qex = key_val(key);
                         }
-                    } else if (fl & P.ev_mask) {  // on demand: an event at this step
+                    } else if (ev_team) {  // on demand: an event at this step (in this team)
                         unsigned long long kb = 0ull;
                         // one cell at a time (runtime slot index, register arrays read by selects):
                         // the recomputation must not raise the register pressure of the step loop
@@ -920,16 +908,16 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                                 }
                             }
                         }
-                        kb = warp_max_u64(kb);
-                        if constexpr (NT > 32) {
-                            if (lane == 0) gs.red3[w] = kb;
-                            group_sync<NT>(g);
+                        kb = warp_max_u64<IL>(kb);
+                        if constexpr (W > 1) {
+                            if (red_lane) gs.red3[w] = kb;
+                            team_sync<NTEAM>(team);
 #pragma unroll
-                            for (int ww = 0; ww < NT / 32; ++ww) {
+                            for (int ww = 0; ww < W; ++ww) {
                                 const unsigned long long o = gs.red3[ww];
                                 kb = o > kb ? o : kb;
                             }
-                            group_sync<NT>(g);  // red3 is reused at the next event step
+                            team_sync<NTEAM>(team);  // red3 is reused at the next event step
                         }
                         if (kb != 0ull) {
                             r_ex = key_r(kb);
@@ -946,9 +934,9 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                         }
                         if (EAGER && t > 0 && rstar < min(map_prev + 1, R - 1)) fl |= 2u;
                         map_prev = rstar;
-                        if (i == 0 && P.out_map) P.out_map[s * P.ld_o + tl] = rstar;
+                        if (i == 0 && act && P.out_map) P.out_map[s * P.ld_o + tl] = rstar;
                         if (fl & P.ev_mask) {
-                            if (i == 0 && ev_count < P.ev_cap) {
+                            if (i == 0 && act && ev_count < P.ev_cap) {
                                 EventRec ev;
                                 ev.t = t;
                                 ev.cp_index = t - rstar + 1;
@@ -960,7 +948,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                             ++ev_count;
                         }
                     }
-                    if (i == 0) {
+                    if (i == 0 && act) {
                         if (P.out_pnew) P.out_pnew[s * P.ld_o + tl] = pnum * fast_rcp(Zp);
                         if (P.out_logz) {  // kept mass (A4)
                             const double lzd = fast_log2(Zd, kFmBase);
@@ -983,7 +971,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 a[0] += safe_log2(wq);
                 wq = 1.0;
 #pragma unroll
-                for (int j = 0; j < J; ++j) a[j] = kFloor ? fmax(a[j] - dcd, kImpossible) : a[j] - dcd;
+                for (int j = 0; j < J; ++j) a[j] = fmax(a[j] - dcd, kImpossible);
                 dc = 0;
                 if (merge && i == 0 && J > 1) {
                     const double2 cA = s_ca[R - 2];
@@ -1009,18 +997,18 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         }
         // ---- spill -----------------------------------------------------------
         if (nonfinite) atomicOr(&gs.flags, 1);
-        group_sync<NT>(g);
+        team_sync<NTEAM>(team);
 #pragma unroll
         for (int j = 0; j < J; ++j) {
             const int p = ROT ? i + NT * ((j + phi) & (J - 1)) : i + NT * j;
-            if (FULL || p < R) {
+            if ((FULL || p < R) && act) {
                 P.st_mu[sbase + p] = mu[j];
                 P.st_beta[sbase + p] = be[j];
                 P.st_a[sbase + p] = a[j];
             }
         }
-        if constexpr (ROT) P.st_w[s * NT + i] = wq;
-        if (i == 0) {
+        if (ROT && act) P.st_w[s * NT + i] = wq;
+        if (i == 0 && act) {
             SeriesScalars sc;
             sc.mu0 = gs.mu0;
             sc.beta0 = gs.beta0;
@@ -1033,7 +1021,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             P.scal[s] = sc;
             if (sc.flags) atomicOr(P.err, unsigned(sc.flags));
         }
-        group_sync<NT>(g);  // gs is reused by the next unit
+        team_sync<NTEAM>(team);  // gs is reused by the next unit
     }
 }
 

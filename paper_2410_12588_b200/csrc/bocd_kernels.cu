@@ -20,8 +20,9 @@ static void make_variant_mode(Variant* out) {
     v.spb = SPB;
     v.full = FULL;
     v.tab2 = TAB2;
-    v.group_smem = sizeof(GroupSmem<NT, kTile>);
-    v.group_smem_p = sizeof(GroupSmem<NT, kPrefOk<NT, J, FULL> ? kTileP : kTile>);  // (+ PREF buffer): group_bytes
+    constexpr int IL = series_il(NT, FULL, SPB);
+    v.group_smem = sizeof(GroupSmem<NT, kTile, IL>);
+    v.group_smem_p = sizeof(GroupSmem<NT, kPrefOk<NT, J, FULL> ? kTileP : kTile, IL>);  // (+ PREF buffer): group_bytes
     *out = v;
 }
 // the truncation mode is a template parameter of the kernels (MERGE / DROP specialised tails)

@@ -685,20 +685,50 @@ int falcon_bocd_update_chunk_host(falcon_bocd_t h, const double* x_host, int64_t
     return FALCON_OK;
 }
 
+// Copies the drained records from the device staging buffer to page-locked host memory as
+// contiguous 8-byte words (coalesced writes over the host link; the gather kernel's
+// per-record 40-byte scatter would be many small host transactions).
+__global__ void drain_copyout_kernel(const unsigned long long* src, unsigned long long* dst, const int64_t* meta) {
+    if (!meta[3]) return;
+    const int64_t n = meta[0] * int64_t(sizeof(falcon_bocd_event) / 8);
+    for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x)
+        dst[k] = src[k];
+}
+
 // Enqueues the two drain kernels (count, then gather into `out` unless out == nullptr);
 // meta (device-accessible int64 [4]) receives {total, overflow, error bits, drained}.
+// host_out: `out` is page-locked host memory, reached through the device staging buffer
+// and drain_copyout_kernel.
 static int enqueue_drain(falcon_bocd_t h, falcon_bocd_event* out, int64_t capacity, int64_t* meta,
-                         cudaStream_t st) {
+                         cudaStream_t st, bool host_out = false) {
     const int64_t S = h->cfg.n_series;
     const int cap = h->cfg.event_capacity;
     const int nblk = int((S + kDrainSpan - 1) / kDrainSpan);
     drain_count_kernel<<<nblk, kDrainThreads, 0, st>>>(h->d_scal, S, cap, h->d_off, h->d_blk, h->d_blkovf);
     CUDA_TRY(h, cudaGetLastError());
     const int64_t threads = S * 32;
+    falcon_bocd_event* dst = out;
+    if (host_out && capacity > 0) {
+        const int64_t need = std::min<int64_t>(capacity, S * int64_t(cap));
+        if (need > h->evout_cap) {
+            CUDA_TRY(h, cudaStreamSynchronize(st));
+            cudaFree(h->d_evout);
+            h->d_evout = nullptr;
+            h->evout_cap = 0;
+            CUDA_TRY(h, cudaMalloc((void**)&h->d_evout, size_t(need) * sizeof(falcon_bocd_event)));
+            h->evout_cap = need;
+        }
+        dst = h->d_evout;
+    }
     drain_gather_kernel<<<unsigned((threads + 255) / 256), 256, 0, st>>>(
-        h->d_scal, h->d_ev, S, cap, h->d_off, h->d_blk, h->d_blkovf, nblk, h->d_err, capacity, out, meta,
+        h->d_scal, h->d_ev, S, cap, h->d_off, h->d_blk, h->d_blkovf, nblk, h->d_err, capacity, dst, meta,
         h->cfg.series_base);
     CUDA_TRY(h, cudaGetLastError());
+    if (host_out && capacity > 0) {
+        drain_copyout_kernel<<<148, 256, 0, st>>>(reinterpret_cast<const unsigned long long*>(dst),
+                                                  reinterpret_cast<unsigned long long*>(out), meta);
+        CUDA_TRY(h, cudaGetLastError());
+    }
     return FALCON_OK;
 }
 
@@ -752,9 +782,20 @@ int falcon_bocd_changepoints(falcon_bocd_t h, falcon_bocd_event* out, int64_t ca
     int rc;
     if ((rc = g.set(h)) != 0) return rc;
     cudaStream_t st = (cudaStream_t)stream;
-    // device memory or pinned host memory: the gather kernel writes there directly (one
-    // synchronisation); pageable host memory: staged through a device buffer
-    const bool direct = capacity > 0 && device_writable(out);
+    // device memory: the gather kernel writes there directly; page-locked host memory: gathered
+    // on the device and copied out by a kernel (one synchronisation either way); pageable host
+    // memory: staged through the device buffer and copied after the count is known
+    cudaPointerAttributes pa;
+    bool dev_out = false, pinned_out = false;
+    if (capacity > 0) {
+        if (cudaPointerGetAttributes(&pa, out) == cudaSuccess) {
+            dev_out = pa.type == cudaMemoryTypeDevice || pa.type == cudaMemoryTypeManaged;
+            pinned_out = pa.type == cudaMemoryTypeHost && pa.devicePointer == out;
+        } else {
+            cudaGetLastError();
+        }
+    }
+    const bool direct = dev_out || pinned_out;
     falcon_bocd_event* dst = out;
     if (capacity > 0 && !direct) {
         const int64_t need = std::min<int64_t>(capacity, h->cfg.n_series * int64_t(h->cfg.event_capacity));
@@ -768,7 +809,7 @@ int falcon_bocd_changepoints(falcon_bocd_t h, falcon_bocd_event* out, int64_t ca
         }
         dst = h->d_evout;
     }
-    if ((rc = enqueue_drain(h, capacity > 0 ? dst : nullptr, capacity, h->h_meta, st)) != 0) return rc;
+    if ((rc = enqueue_drain(h, capacity > 0 ? dst : nullptr, capacity, h->h_meta, st, pinned_out)) != 0) return rc;
     CUDA_TRY(h, cudaStreamSynchronize(st));
     const int64_t total = h->h_meta[0], ovf = h->h_meta[1], err = h->h_meta[2];
     if ((rc = sticky_status(h, err)) != 0) return rc;
@@ -797,7 +838,13 @@ int falcon_bocd_changepoints_async(falcon_bocd_t h, falcon_bocd_event* out, int6
     if ((rc = g.set(h)) != 0) return rc;
     if (!device_writable(meta) || (capacity > 0 && !device_writable(out)))
         return fail(h, FALCON_EINVAL, "out / meta must be device memory or page-locked host memory");
-    return enqueue_drain(h, capacity > 0 ? out : nullptr, capacity, meta, (cudaStream_t)stream);
+    bool host_out = false;
+    if (capacity > 0) {
+        cudaPointerAttributes pa;
+        host_out = cudaPointerGetAttributes(&pa, out) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+        cudaGetLastError();
+    }
+    return enqueue_drain(h, capacity > 0 ? out : nullptr, capacity, meta, (cudaStream_t)stream, host_out);
 }
 
 int falcon_bocd_read_posterior(falcon_bocd_t h, int64_t s0, int64_t count, double* logR_out, double* mu_out,

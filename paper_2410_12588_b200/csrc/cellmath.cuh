@@ -34,11 +34,7 @@ namespace fbocd {
 // reaches 1024-2048 and the log's error, carried along the MERGE bucket's chain of merged
 // masses, would approach the parity budget (measured 6.2e-10 at R = 2048 with LB = 8).
 __host__ __device__ constexpr int cell_logbits(bool full, int r_full) { return (full && r_full <= 1024) ? 8 : 10; }
-#ifndef FALCON_BOCD_EXPBITS
-#define FALCON_BOCD_EXPBITS 8
-#endif
-constexpr int kCellEB = FALCON_BOCD_EXPBITS;  // exp2 table bits: 8 (degree-4 fit) or 9 (degree 3)
-static_assert(kCellEB == 8 || kCellEB == 9, "FALCON_BOCD_EXPBITS: 8 or 9");
+constexpr int kCellEB = 8;  // exp2 table bits (degree-4 fit; 9 bits with degree 3 measured slower)
 constexpr int kCellExpTab = 1 << kCellEB;
 constexpr double kCellExpScale = double(kCellExpTab);          // the rounding grid 2^-EB
 constexpr unsigned kCellExpLo = 0x80000000u - 1021u * kCellExpTab;  // 2^-1021: floor / dead
@@ -77,16 +73,13 @@ static const double kCellConstants[12] = {
     1.4426950408884385, -0.7213475204440444, 0.4808994476545776,   // LB = 8
     1.4426950408889305, -0.7213475204444544, 0.4808986221353932,   // LB = 9
     1.4426950408889614, -0.72134752044448, 0.4808984157560584,     // LB = 10
-    // exp: Q0, Q1, Q2 (EB = 8: + Q3 immediate, max error 4.8e-18; EB = 9: Q2 immediate,
-    // degree 3 on |r| <= 2^-10, 2.2e-15)
-    kCellEB == 8 ? 0.6931471805599428 : 0.6931471805599453, kCellEB == 8 ? 0.24022650695910044 : 0.2402265138385228,
-    0.05550411375117056};
+    // exp: Q0, Q1, Q2 (+ Q3 immediate; max error of r Q(r) 4.8e-18)
+    0.6931471805599428, 0.24022650695910044, 0.05550411375117056};
 // leading coefficients rounded to 20 mantissa bits (DFMA immediates; the rounding is weighted
 // by r^4 <= 2^-36, i.e. below 1e-18)
 template <int LB>
 constexpr double kCellLogP3 = LB == 8 ? -0.3606746196746826 : -0.3606739044189453;
-constexpr double kCellExpQ3 = 0.009618133306503296;  // 0.009618129695226546 (EB = 8)
-constexpr double kCellExpQ2i = 0.05550411343574524;  // 0.05550410961851198 (EB = 9)
+constexpr double kCellExpQ3 = 0.009618133306503296;  // 0.009618129695226546 rounded
 
 constexpr unsigned kCellExpBase = 0x1A00u;
 template <int EC>

@@ -4,7 +4,6 @@
 set -x
 O=gpurun_out/r02b; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
-nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/peaks/smem_probe tools/peaks/smem_probe.cu && ./tools/peaks/smem_probe > $O/smem_probe.jsonl 2>&1
 python tools/peaks/p0.py > $O/p0.json 2> $O/p0.err
 timeout 600 python bench.py --config C5 --steps 5 --warmup 3 > $O/bench_C5.json 2> $O/bench_C5.err
 timeout 600 python bench.py --config C3 --eager --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_C3_eager.json 2> $O/bench_C3_eager.err
