@@ -302,7 +302,8 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2410_12588_b200 import bocd, tracegen
-    from paper_2410_12588_b200.distributed import ShardedBocd, allgather_events, max_over_ranks, shard_range
+    from paper_2410_12588_b200.distributed import (ShardedBocd, compact_gathered, gather_fixed, max_over_ranks,
+                                                   shard_range)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -363,19 +364,24 @@ def main():
     for k in range(args.warmup):
         run_step(k)
         b.changepoints_async(device_out=True).result()
-    b.reserve_events(2 * max(b._ev_hint, 1024), device_out=True)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
 
     block = 100 if streaming else 1  # C5: kernel time is averaged over blocks of back-to-back calls
 
+    # per-step event capacity: twice the busiest warmup step (a step that overflows it is
+    # reported as an error after the timed region, nothing is dropped silently)
+    cap_step = max(2 * b._ev_hint, 1024)
+
     def timed_region():
         ev_start, ev_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        n_marks = args.steps * (per_step // block)
+        n_marks = args.steps * (per_step // block) if streaming else args.steps
         ks = [torch.cuda.Event(enable_timing=True) for _ in range(n_marks)]
         ke = [torch.cuda.Event(enable_timing=True) for _ in range(n_marks)]
-        events, drop_any, pending = [], False, None
+        bufs = [torch.empty((cap_step, 40), dtype=torch.uint8, device=dev) for _ in range(args.steps)]
+        metas = [torch.zeros(4, dtype=torch.int64, device=dev) for _ in range(args.steps)]
+        gathered = []
         with ClockSampler(local) as clk:
             time.sleep(0.3)
             torch.cuda.synchronize()
@@ -395,25 +401,22 @@ def main():
                     b.update_chunk(x[:, kk * per_step:(kk + 1) * per_step])
                     ke[m].record(stream)
                     m += 1
-                # each step's result: its events drained into device memory, stream-ordered; the
-                # previous step's drain is collected while this step runs
-                ticket = b.changepoints_async(device_out=True)
-                if pending is not None:
-                    recs, dropped = pending.result()
-                    events.append(recs)
-                    drop_any |= dropped
-                pending = ticket
-            recs, dropped = pending.result()
-            events.append(recs)
-            drop_any |= dropped
-            recs = torch.cat(events) if len(events) > 1 else events[0]
-            if world > 1:
-                allgather_events(recs)
+                # each step's result: its events drained into device memory and (N > 1)
+                # all-gathered over NVLink, stream-ordered: the host never waits inside the loop
+                b.drain_into(bufs[k], metas[k])
+                if world > 1:
+                    gathered.append(gather_fixed(bufs[k], metas[k]))
             ev_end.record(stream)
             torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        return ev_start, ev_end, ks, ke, clk, recs, drop_any
+        if world > 1:
+            parts = [compact_gathered(g, mt, world) for g, mt in gathered]
+        else:
+            parts = [compact_gathered(bf, mt, 1) for bf, mt in zip(bufs, metas)]
+        assert not any(p[2] for p in parts), "a step's events exceeded the per-step drain capacity"
+        recs = torch.cat([p[0] for p in parts])
+        return ev_start, ev_end, ks, ke, clk, recs, any(p[1] for p in parts)
 
     ev_start, ev_end, ks, ke, clk, recs, dropped = timed_region()
     cs = clk.summary()
@@ -425,6 +428,7 @@ def main():
     t_ms = ev_start.elapsed_time(ev_end)
     t_max = max_over_ranks(t_ms, dev)
     k_ms = [a.elapsed_time(e) for a, e in zip(ks, ke)]
+    gaps = [ke[m].elapsed_time(ks[m + 1]) for m in range(len(ks) - 1)] if not streaming else []
     k_avg = sum(k_ms) / len(k_ms) / block  # per launch (C5: blocks of back-to-back calls)
     k_share = sum(k_ms) / t_ms
     value = n_global * per_step * args.steps / (t_max * 1e-3) if args.scaling == "strong" else (
@@ -445,6 +449,10 @@ def main():
         roof = _roofline_alu(S * per_step * cfg.R, k_avg, kname, peaks)
         roof["traffic"] = _traffic(cfg.name, S * per_step)
     roof["kernel_share_of_step"] = k_share
+    if gaps:
+        roof["gaps_between_launches_ms"] = [round(g, 4) for g in gaps]
+        roof["tail_after_last_launch_ms"] = round(ke[-1].elapsed_time(ev_end), 4)
+        roof["head_before_first_launch_ms"] = round(ev_start.elapsed_time(ks[0]), 4)
     clocks = clk.summary()
     if remeasured:
         clocks["remeasured"] = True
@@ -524,11 +532,12 @@ def streaming_latency(b, col, args, stream, n):
 
 def e2e_run(sb0, bocd, x, col, args, cfg, kw, local, lo, S, n_global, world, dev, stream):
     """The same metric end to end through the public API with HOST buffers: every step copies
-    that step's observations from pinned host memory (falcon_bocd_update_chunk_host) and reads
-    that step's change points back (falcon_bocd_changepoints_async into page-locked memory,
-    collected while the next step's copy and kernel run); N > 1: the final all-gather."""
+    that step's observations from pinned host memory (falcon_bocd_update_chunk_host: staged
+    copy overlapped with the previous step's kernel) and reads that step's change points back
+    to pinned host memory (drain into device memory, then an asynchronous copy of the drain
+    meta and the fixed-capacity record buffer); N > 1: each step's events are all-gathered."""
     import torch
-    from paper_2410_12588_b200.distributed import allgather_events, max_over_ranks
+    from paper_2410_12588_b200.distributed import compact_gathered, gather_fixed, max_over_ranks
     streaming = col is not None
     per_step = args.calls if streaming else args.chunk
     nbuf = 2
@@ -541,48 +550,46 @@ def e2e_run(sb0, bocd, x, col, args, cfg, kw, local, lo, S, n_global, world, dev
         for i in range(nbuf):
             hb[i].copy_(x[:, (args.warmup + i) * per_step:(args.warmup + i + 1) * per_step])
     b2 = bocd.BocdBatch(S, device=local, series_base=lo, **kw)
+    cap = max(2 * sb0.batch._ev_hint, 1024)
+    dbuf = [torch.empty((cap, 40), dtype=torch.uint8, device=dev) for _ in range(args.steps + 1)]
+    dmeta = [torch.zeros(4, dtype=torch.int64, device=dev) for _ in range(args.steps + 1)]
+    hbuf = [torch.empty((cap, 40), dtype=torch.uint8).pin_memory() for _ in range(args.steps + 1)]
+    hmeta = [torch.zeros(4, dtype=torch.int64).pin_memory() for _ in range(args.steps + 1)]
 
-    def host_step(k):
+    def host_step(k, slot):
         h = hb[k % nbuf]
         if streaming:
             for c in range(per_step):
                 b2.update_chunk_host(h[c].view(S, 1))
         else:
             b2.update_chunk_host(h)
-        return b2.changepoints_async()
+        b2.drain_into(dbuf[slot], dmeta[slot])
+        hmeta[slot].copy_(dmeta[slot], non_blocking=True)
+        hbuf[slot].copy_(dbuf[slot], non_blocking=True)
+        return gather_fixed(dbuf[slot], dmeta[slot]) if world > 1 else None
 
-    host_step(0).result()
-    b2.reserve_events(2 * max(b2._ev_hint, sb0.batch._ev_hint, 1024))
+    host_step(0, args.steps)  # warm-up (staging buffers, copy stream)
     torch.cuda.synchronize()
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    pending, got, d2h = None, [], 0
-    for k in range(args.steps):
-        ticket = host_step(k)
-        if pending is not None:
-            evs, _ = pending.result()  # the previous step's events, read while this step runs
-            got.append(evs)
-            d2h += evs.nbytes + 32
-        pending = ticket
-    evs, _ = pending.result()
-    got.append(evs)
-    d2h += evs.nbytes + 32
-    if world > 1:
-        import numpy as np
-        allrec = np.concatenate(got) if got else np.empty(0, bocd.EVENT_DTYPE)
-        allgather_events(torch.from_numpy(allrec.view(np.uint8).reshape(-1, 40).copy()).to(dev))
+    gathered = [host_step(k, k) for k in range(args.steps)]
     e1.record(stream)
     torch.cuda.synchronize()
     et = max_over_ranks(e0.elapsed_time(e1), dev)
+    for k in range(args.steps):  # the host copies hold every step's result
+        assert int(hmeta[k][3]) == 1, "a step's events exceeded the per-step drain capacity"
+    if world > 1:
+        for g, mt in gathered:
+            compact_gathered(g, mt, world)
     b2.close()
     n_units = (n_global if args.scaling == "strong" else S * world) * per_step * args.steps
     return {"value": n_units / (et * 1e-3), "unit": UNIT, "h2d_bytes_per_step": S * per_step * 8,
-            "d2h_bytes_per_step": int(d2h / args.steps),
+            "d2h_bytes_per_step": cap * 40 + 32,
             "api": ("falcon_bocd_update_chunk_host per call" if streaming else "falcon_bocd_update_chunk_host")
-                   + " + falcon_bocd_changepoints_async per step (pinned host x and events)"}
+                   + " + falcon_bocd_changepoints_async per step (pinned host x; events copied to pinned host)"}
 
 
 if __name__ == "__main__":

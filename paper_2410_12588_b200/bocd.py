@@ -151,6 +151,17 @@ class BocdBatch:
             self._evbufs[key] = buf
         return buf
 
+    def drain_into(self, out: torch.Tensor, meta: torch.Tensor, stream=None):
+        """Enqueue a drain into caller-owned buffers (falcon_bocd_changepoints_async): out uint8
+        [capacity, 40] and meta int64 [4], each device memory or page-locked host memory.  No
+        synchronisation; after the stream reaches it, meta = (total, overflow, error bits,
+        drained) and out[:total] holds the events when drained == 1."""
+        assert out.dtype == torch.uint8 and out.dim() == 2 and out.shape[1] == EVENT_DTYPE.itemsize
+        assert meta.dtype == torch.int64 and meta.numel() >= 4 and meta.is_contiguous()
+        N.check(N.lib().falcon_bocd_changepoints_async(self._h, ctypes.c_void_p(out.data_ptr()), out.shape[0],
+                                                       ctypes.c_void_p(meta.data_ptr()),
+                                                       _stream_ptr(stream, self.device)), self._h)
+
     def reserve_events(self, n: int, device_out: bool = False):
         """Pre-allocate every drain buffer for n events (keeps allocations out of a timed loop)."""
         where = "device" if device_out else "host"

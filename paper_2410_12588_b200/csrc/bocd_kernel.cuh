@@ -134,14 +134,30 @@ struct KParams {
     int tma_ok;  // x base 16-B aligned and ld even
 };
 
-// Series interleaving.  The FULL kernels with at least two series per CTA interleave IL = 2
-// series lane by lane (series = lane & 1): at every step all series of a CTA read the same
-// per-r table rows (the ring position -> run length map depends only on the thread index and
-// t), so the two lanes of a pair share each table entry and a warp's table reads touch half
-// as many distinct rows (profiles/r02_smem_probe.jsonl: a pair-shared 16-B row costs half the
-// shared-memory wavefronts of 32 distinct rows).  A "team" is the IL series that share warps;
-// it synchronises as one (named barrier per team).  IL = 1 otherwise.
-__host__ __device__ constexpr int series_il(int nt, bool full, int spb) { return (full && spb >= 2 && nt >= 32) ? 2 : 1; }
+// Series interleaving (FBOCD_IL = 2, an A/B alternative; default IL = 1).  IL = 2 interleaves
+// two series lane by lane (series = lane & 1) in the FULL kernels with at least two series per
+// CTA: at every step all series of a CTA read the same per-r table rows (the ring position ->
+// run length map depends only on the thread index and t), so the two lanes of a pair share
+// each table row: the {G, alpha} rows cost 2 shared-memory wavefronts per warp instead of 4
+// and y 1 instead of 2 (ncu, profiles/r02_ncu_c3_il2.txt).  But the log2-table rows of the
+// two series no longer cluster within a quarter-warp (+1.3 wavefronts of bank conflicts) and
+// each step's barrier couples 8 warps instead of 4: measured 78.2 ms vs 74.9 ms per C3 call
+// (an octet layout, lanes 0-7 / 8-15, loses the row sharing: LDS.128 does not merge
+// quarter-warps; 91.9 ms).  A "team" is the IL series that share warps; it synchronises as one.
+#ifndef FBOCD_IL
+#define FBOCD_IL 1
+#endif
+// The exp2 exponent needs only the lower clamp (the floor): every cell's joint is below the
+// step's evidence Z, which the frame Dc_t keeps within a few binades of 1 (Dc_t tracks the prior
+// predictive of x_t and the exponent of Zd_{t-1}; the predictive of any run length exceeds the
+// prior predictive by at most ~sqrt(2 alpha_r)), so 2^+1000 is unreachable for
+// finite x.  FBOCD_CLAMP1=0 restores the two-sided clamp (A/B: 75.6 vs 75.15 ms per C3 call).
+#ifndef FBOCD_CLAMP1
+#define FBOCD_CLAMP1 1
+#endif
+__host__ __device__ constexpr int series_il(int nt, bool full, int spb) {
+    return (FBOCD_IL == 2 && full && spb >= 2 && nt >= 32) ? 2 : 1;
+}
 
 // per-series partial sums of a step: one per (warp, series) pair
 __host__ __device__ constexpr int n_partials(int nt, int il) { return nt * il / 32 > 0 ? nt * il / 32 : 1; }
@@ -352,8 +368,11 @@ constexpr unsigned kFmBase = 0x800u;
 // free, for the R <= 1024 FULL kernels; 8 otherwise, where the per-r tables are larger).
 // The persistent prefetching kernels (HBM-bound streaming) take 4 copies and 64-step x tiles
 // so that two CTAs with their prefetch buffers still fit one SM.
+#ifndef FBOCD_OCC3
+#define FBOCD_OCC3 0  // A/B: R = 1024 at 3 CTAs per SM (85 registers, 8 exp2 copies)
+#endif
 __host__ __device__ constexpr int cell_ec(bool full, int r_full, bool pref) {
-    return pref ? 4 : ((full && r_full <= 1024) ? 16 : 8);
+    return pref ? 4 : ((full && r_full <= 1024 && !(FBOCD_OCC3 && r_full == 1024)) ? 16 : 8);
 }
 __host__ __device__ constexpr unsigned bocd_fm_bytes(int ec, int lb) {
     return (lb == 8 ? (ec == 16 ? cell_tables_end<16, 8>() : ec == 8 ? cell_tables_end<8, 8>()
@@ -462,6 +481,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     }
     __syncthreads();
     const int ntiles = (P.T + TILE - 1) / TILE;
+    const int tl_min = P.t0 == 0 ? 1 : 0;  // no events at global t = 0 (Q8): local steps tl >= tl_min
     constexpr bool merge = (MODE == 0);  // truncation at R: MERGE (0) or DROP (1)
     const bool any_out = P.out_map || P.out_pnew || P.out_logz;  // per-step outputs requested
     // argmax-eligible run lengths: MERGE r <= R-3 (slot R-1 is the bucket), DROP r <= R-2
@@ -762,7 +782,11 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                         const double qq = pe[kk] * re[kk];
                         // 2^e, e = floor(n/256) for n = ki - 2^31, floored at 2^-1021 and clamped at
                         // +1000; hi word = kc * 2^12 + hi(T'_j) (cellmath.cuh)
+#if FBOCD_CLAMP1
+                        const unsigned kc = max(ki[kk], kCellExpLo);
+#else
                         const unsigned kc = max(min(ki[kk], kCellExpHi), kCellExpLo);
+#endif
                         const double Ts = __hiloint2double(int(kc * (1048576u >> kCellEB)) + __double2hiint(Tv[kk]),
                                                            __double2loint(Tv[kk]));
                         double E = fma(Ts, qq, Ts);
@@ -826,7 +850,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 const double Zd = merge ? Z : Z - P.omH * qB;    // normaliser of the new posterior
                 const double Zp = merge ? Z : Z - qB;            // p_new = pnum / Zp
                 const double pnum = (merge && R == 2) ? Z : q0;  // MERGE R = 2: p_new = 1
-                uint32_t fl = (t > 0 && pnum > P.theta * Zp) ? 1u : 0u;
+                uint32_t fl = (tl >= tl_min && pnum > P.theta * Zp) ? 1u : 0u;
                 // A6: the new change-point cell (owner of kB) and the MERGE bucket (owner of kA).
                 // ROT: branch-free; the new mass is the slot-0 pending weight wq (no log on the
                 // step's critical path), folded into a at the next rotation step.  Generic: one
@@ -932,7 +956,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                         } else {
                             rstar = r_ex + 1;
                         }
-                        if (EAGER && t > 0 && rstar < min(map_prev + 1, R - 1)) fl |= 2u;
+                        if (EAGER && tl >= tl_min && rstar < min(map_prev + 1, R - 1)) fl |= 2u;
                         map_prev = rstar;
                         if (i == 0 && act && P.out_map) P.out_map[s * P.ld_o + tl] = rstar;
                         if (fl & P.ev_mask) {

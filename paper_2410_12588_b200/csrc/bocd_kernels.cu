@@ -44,7 +44,7 @@ int select_variant(int R, int mode, Variant* out) {
     switch (R) {
         case 256: make_variant<32, 8, true, true, 8, 2>(mode, out); return 0;
         case 512: make_variant<64, 8, true, true, 4, 2>(mode, out); return 0;
-        case 1024: make_variant<128, 8, true, true, 2, 2>(mode, out); return 0;
+        case 1024: make_variant<128, 8, true, true, 2, FBOCD_OCC3 ? 3 : 2>(mode, out); return 0;
         case 2048: make_variant<256, 8, true, false, 1, 2>(mode, out); return 0;
         case 4096: make_variant<512, 8, true, false, 1, 1>(mode, out); return 0;
         default: break;

@@ -137,6 +137,28 @@ def run_sharded(x_source, n_global: int, T: int, chunk: int, device=None, batch_
     return (records_to_numpy(recs) if recs is not None else None), dropped
 
 
+def gather_fixed(records: torch.Tensor, meta: torch.Tensor, group=None):
+    """Stream-ordered all-gather of one drain whose size the host does not know yet: every
+    rank contributes its fixed-capacity record buffer (uint8 [cap, 40]) and its drain meta
+    (int64 [4], total first), both on the device, so nothing waits for the host.  Returns
+    (records [world * cap, 40], metas [world * 4]) on every rank; compact_gathered() keeps
+    the valid prefix of each rank's block."""
+    world = dist.get_world_size(group)
+    out = torch.empty((world * records.shape[0], RECORD_BYTES), dtype=torch.uint8, device=records.device)
+    metas = torch.empty(world * meta.numel(), dtype=meta.dtype, device=meta.device)
+    dist.all_gather_into_tensor(metas, meta.contiguous(), group=group)
+    dist.all_gather_into_tensor(out, records.contiguous(), group=group)
+    return out, metas
+
+
+def compact_gathered(records: torch.Tensor, metas: torch.Tensor, world: int):
+    """The valid events of a gather_fixed result, rank by rank (global (series, t) order)."""
+    cap = records.shape[0] // world
+    m = metas.view(world, -1).cpu()
+    parts = [records[r * cap: r * cap + int(m[r, 0])] for r in range(world)]
+    return torch.cat(parts, 0), bool(m[:, 1].any()), bool((m[:, 3] == 0).any())
+
+
 def records_to_numpy(records: torch.Tensor):
     """uint8 [n, 40] records -> numpy structured array (falcon_bocd_event layout)."""
     from .bocd import EVENT_DTYPE
