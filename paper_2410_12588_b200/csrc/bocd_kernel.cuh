@@ -108,6 +108,8 @@ struct KParams {
     double H, omH, hr, theta, alpha0, prior_cov;  // omH = 1-H, hr = H/(1-H)
     double ln_omH;                                // log(1-H)
     double c_bucket, alpha_bucket;                // c_{R-1}/ln2 and alpha_{R-1} (MERGE bucket, FULL)
+    double al2_bucket;                            // 2 alpha_{R-1}
+    int a2p1;                                     // 2 alpha0 + 1 (FULL kernels: 2 alpha0 is an integer)
     int mode;                                     // 0 MERGE, 1 DROP
     int prior_first_obs;
     uint32_t ev_mask;
@@ -301,9 +303,11 @@ __host__ __device__ constexpr size_t group_bytes(int R) {
     return sizeof(GroupSmem<NT, PREF ? kTileP : kTile, IL>) +
            (PREF ? ((3 * size_t(R) * sizeof(double) + sizeof(SeriesScalars) + 15) & ~size_t(15)) : 0);
 }
-// bytes of the per-r tables ({G_{r+1}, alpha_{r+1}} and y_r) for `entries` table rows
-__host__ __device__ constexpr size_t table_bytes(int entries) {
-    return (size_t(entries) * (sizeof(double2) + sizeof(double)) + 15) & ~size_t(15);
+// bytes of the per-r tables for `entries` table rows: generic kernels {G_{r+1}, alpha_{r+1}}
+// and y_r (24 B per row); FULL kernels {G_{r+1}, y_r} (16 B per row: alpha is converted from
+// the integer 2 alpha0 + r + 1)
+__host__ __device__ constexpr size_t table_bytes(int entries, bool full) {
+    return (size_t(entries) * (full ? sizeof(double2) : sizeof(double2) + sizeof(double)) + 15) & ~size_t(15);
 }
 
 // Writes v into register slot j of a (a runtime slot index: a plain jump table).
@@ -429,8 +433,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     constexpr bool BUCKET_PRED = FULL && NT * J >= 2048 && MODE == 0;
     // FULL: absolute shared addresses of the per-r tables (the dynamic window starts at
     // kDynBase, checked at entry with the fast-math tables)
-    constexpr unsigned kCaBase = kDynBase + bocd_fm_bytes(EC, LB);
-    constexpr unsigned kYBase = kCaBase + unsigned(NT * J + NT) * 16u;
+    constexpr unsigned kGyBase = kDynBase + bocd_fm_bytes(EC, LB);  // FULL: {G_{r+1}, y_r} rows
     constexpr int TILE = PREF ? kTileP : kTile;
     constexpr int IL = series_il(NT, FULL, SPB);  // series interleaved per warp (lane & 1)
     constexpr int NTEAM = NT * IL;                // threads of one team (IL series)
@@ -441,21 +444,28 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     const int RT = table_entries<NT, J, FULL, TAB2>(R);
     // dynamic shared memory: [fast-math tables, cell tables (bocd_fm_bytes)][per-r tables][groups]
     unsigned char* const smem = smem_raw;
+    // generic: s_ca = {G_{r+1}, alpha_{r+1}}, s_y = y_r; FULL: s_gy = {G_{r+1}, y_r} (same base)
     double2* s_ca = reinterpret_cast<double2*>(smem + bocd_fm_bytes(EC, LB));
     double* s_y = reinterpret_cast<double*>(s_ca + RT);
-    unsigned char* gbase = smem + bocd_fm_bytes(EC, LB) + table_bytes(RT);
+    double2* s_gy = s_ca;
+    unsigned char* gbase = smem + bocd_fm_bytes(EC, LB) + table_bytes(RT, FULL);
 
     for (int k = threadIdx.x; k < RT; k += blockDim.x) {
         const int r = k < R ? k : k - R;
-        s_ca[k] = P.tab_ca[r];
-        s_y[k] = P.tab_y[r];
+        if constexpr (FULL) {
+            s_gy[k] = make_double2(P.tab_ca[r].x, P.tab_y[r]);
+        } else {
+            s_ca[k] = P.tab_ca[r];
+            s_y[k] = P.tab_y[r];
+        }
     }
     const bool fm_ok = smem_addr(smem_raw) == kDynBase && fm_setup(smem_raw, P.fm) == kFmBase;
     {
         double* ex = reinterpret_cast<double*>(smem_raw + (kCellExpBase - kDynBase));
         for (int k = threadIdx.x; k < kCellExpTab * EC; k += blockDim.x) ex[k] = P.ct->exptab[k / EC];
         double2* lg = reinterpret_cast<double2*>(smem_raw + (cell_log_base<EC>() - kDynBase));
-        const double2* src = LB == 8 ? P.ct->log8 : P.ct->log10;
+        // FULL kernels evaluate the half-log (cellmath.cuh, cell_log2h): halved table values
+        const double2* src = FULL ? (LB == 8 ? P.ct->log8h : P.ct->log10h) : (LB == 8 ? P.ct->log8 : P.ct->log10);
         for (int k = threadIdx.x; k < (1 << LB); k += blockDim.x) lg[k] = src[k];
     }
     const unsigned lb = 8u * (threadIdx.x & unsigned(EC - 1));  // exp2 table copy of this lane
@@ -602,7 +612,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             // before x_0 the cell that step 0 truncates (thread iB's slot 0) is impossible: its
             // continuation weight is 0 (later steps: the bucket the previous step formed)
             else if (BUCKET_PRED && i == iB) wq = 0.0;
-            if (BUCKET_PRED) L0p = cell_log2<EC, LB>(be[0]);  // = the previous step's lg beta' of slot 0
+            if (BUCKET_PRED) L0p = cell_log2h<EC, LB>(be[0]);  // = the previous step's lg beta'/2 of slot 0
         }
         if constexpr (PREF) {
             // pf is free once every thread of the team has read it: prefetch the next unit
@@ -632,7 +642,9 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             for (int q = i; q < n; q += NT) {
                 const double xq = gs.xbuf[buf][q];
                 if (!isfinite(xq)) nonfinite = true;
-                const double l0 = prior_l2(xq, gs.mu0, gs.beta0, gs.aprior, s_ca[0], s_y[0], kFmBase);
+                const double l0 = FULL ? prior_l2(xq, gs.mu0, gs.beta0, gs.aprior, make_double2(s_gy[0].x, P.alpha0 + 0.5),
+                                                  s_gy[0].y, kFmBase)
+                                       : prior_l2(xq, gs.mu0, gs.beta0, gs.aprior, s_ca[0], s_y[0], kFmBase);
                 gs.kbuf[buf][q] = __double2int_rn(fmin(fmax(l0, -kK0Max), kK0Max));
             }
             team_sync<NTEAM>(team);
@@ -675,6 +687,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     k0 = tmod;
                 }
                 const int par = tl & 1;
+                const int mb = FULL ? P.a2p1 + ib : 0;  // 2 alpha0 + 1 + (table index of slot 0)
                 double sum = 0.0;
                 unsigned long long key = 0ull;
 #pragma unroll
@@ -695,8 +708,12 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                         }
                         if (!FULL && p >= R) idx[kk] = 0;  // masked cell: any valid entry
                         if constexpr (FULL) {  // compile-time shared addresses (no generic pointers)
-                            ca[kk] = lds_v2f64(unsigned(idx[kk]) * 16u + kCaBase);
-                            yv[kk] = lds_f64(unsigned(idx[kk]) * 8u + kYBase);
+                            // {G_{r+1}, y_r} and 2 alpha_{r+1} = 2 alpha0 + r + 1 (exact integer, I2F.F64);
+                            // r = idx - R for the one slot whose index wrapped (slot 0)
+                            const double2 gy = lds_v2f64(unsigned(idx[kk]) * 16u + kGyBase);
+                            const int m2 = mb - NT * j - ((j == 0 && idx[kk] >= R) ? R : 0);
+                            ca[kk] = make_double2(gy.x, __int2double_rn(m2));
+                            yv[kk] = gy.y;
                         } else {
                             ca[kk] = s_ca[idx[kk]];
                             yv[kk] = s_y[idx[kk]];
@@ -727,12 +744,15 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                                                                  int(tb[kk] & 0x7FF00000u),
                                                              __double2loint(lt[kk].x));
                         rl[kk] = fma(bn[kk], invs, -1.0);
-                        kt[kk] = __int2double_rn(int(tb[kk] >> 20) - 1023) + lt[kk].y;  // I2F.F64: k exact
+                        // I2F.F64: k exact.  FULL: the half-log (cell_log2h), k/2 + l_i/2
+                        kt[kk] = FULL ? fma(__int2double_rn(int(tb[kk] >> 20) - 1023), 0.5, lt[kk].y)
+                                      : __int2double_rn(int(tb[kk] >> 20) - 1023) + lt[kk].y;
                     }
                     {
-                        constexpr int o = 3 * (LB - 8);
+                        constexpr int o = FULL ? 12 + 3 * (LB - 8) : 3 * (LB - 8);
 #pragma unroll
-                        for (int kk = 0; kk < G; ++kk) pl[kk] = fma(rl[kk], kCellLogP3<LB>, c_cell[o + 2]);
+                        for (int kk = 0; kk < G; ++kk)
+                            pl[kk] = fma(rl[kk], FULL ? kCellLogP3h<LB> : kCellLogP3<LB>, c_cell[o + 2]);
 #pragma unroll
                         for (int kk = 0; kk < G; ++kk) pl[kk] = fma(pl[kk], rl[kk], c_cell[o + 1]);
 #pragma unroll
@@ -742,11 +762,13 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
 #pragma unroll
                     for (int kk = 0; kk < G; ++kk) {
                         const int j = j0 + kk;
+                        // lg beta' (FULL: lg beta' / 2, multiplied by 2 alpha: the same product)
                         const double Ln = fma(rl[kk], pl[kk], kt[kk]);
                         ell[kk] = fma(-ca[kk].y, Ln, a[j] + ca[kk].x);
                         if constexpr (BUCKET_PRED) {
                             if (j == 0) {  // the truncated cell (thread iB): the bucket's continuation
-                                const double lb_ = fma(P.alpha_bucket, L0p - Ln, fma(-0.5, Ln, P.c_bucket));
+                                // alpha (lg beta - lg beta') - lg beta'/2 with half-logs (FULL)
+                                const double lb_ = fma(P.al2_bucket, L0p - Ln, P.c_bucket - Ln);
                                 ell[kk] = (i == iB) ? lb_ : ell[kk];
                                 L0p = Ln;
                             }
@@ -859,8 +881,9 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     const bool ownB = (i == iB);
                     const bool ownA = merge && (i == iB + 1);  // iB = NT-1: thread 0, slot 1 (rotation)
                     const double dcd = double(dc);
-                    const double2 cA = s_ca[R - 2];  // G_{R-1} - alpha_{R-1} lg beta' of cell kA
-                    const double offA = fma(-cA.y, gs.l0[par][iB + 1], cA.x);
+                    // G_{R-1} - alpha_{R-1} lg beta' of cell kA (half-log x 2 alpha_{R-1})
+                    const double GA = lds_v2f64(kGyBase + unsigned(NT * J - 2) * 16u).x;
+                    const double offA = fma(-P.al2_bucket, gs.l0[par][iB + 1], GA);
                     const double m0 = gs.mu0, b0 = gs.beta0;
                     const double aB = gs.aprior + dcd, aA = dcd - offA;
                     const double wB = P.hr * Z, wA = bucket_mass(qA, qB);
@@ -923,8 +946,10 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                                         bj = (jj == j) ? be[jj] : bj;
                                         aj = (jj == j) ? a[jj] : aj;
                                     }
-                                    const double2 c2 = s_ca[id];
-                                    const double Ln = cell_log2<EC, LB>(bj);
+                                    // the loop's arithmetic, one cell (FULL: half-log x 2 alpha)
+                                    const double2 c2 = FULL ? make_double2(s_gy[id].x, __int2double_rn(P.a2p1 + r))
+                                                            : s_ca[id];
+                                    const double Ln = FULL ? cell_log2h<EC, LB>(bj) : cell_log2<EC, LB>(bj);
                                     double E = cell_exp2<EC>(fma(-c2.y, Ln, aj + c2.x), C7, lb);
                                     if (ROT && j == 0) E *= wq;
                                     const unsigned long long kq = argmax_key(E, r);
@@ -998,8 +1023,8 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 for (int j = 0; j < J; ++j) a[j] = fmax(a[j] - dcd, kImpossible);
                 dc = 0;
                 if (merge && i == 0 && J > 1) {
-                    const double2 cA = s_ca[R - 2];
-                    a[1] = -fma(-cA.y, gs.l0[par][NT], cA.x);
+                    const double GA = lds_v2f64(kGyBase + unsigned(NT * J - 2) * 16u).x;
+                    a[1] = -fma(-P.al2_bucket, gs.l0[par][NT], GA);
                     wq = bucket_mass(gs.e0[par][NT], gs.e0[par][NT - 1]);
                 }
                 // rotate slot j <- slot j+1
@@ -1014,7 +1039,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 mu[J - 1] = m0;
                 be[J - 1] = b0;
                 a[J - 1] = a0;
-                if (BUCKET_PRED) L0p = cell_log2<EC, LB>(be[0]);  // slot 0 is a new cell
+                if (BUCKET_PRED) L0p = cell_log2h<EC, LB>(be[0]);  // slot 0 is a new cell
                 iB = 0;
             }
             }

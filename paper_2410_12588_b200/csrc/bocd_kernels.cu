@@ -1,4 +1,5 @@
 // bocd_kernels.cu — instantiations of the resident BOCD kernel and the variant table.
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 
@@ -40,8 +41,13 @@ static void make_variant(int mode, Variant* out) {
 // EAGER-MAP kernel (bocd_kernel.cuh), one-unit and persistent, per truncation mode.
 // (Shapes measured slower for R = 1024 and removed: 128x8 with 3-4 series per CTA, 64x16
 // (J = 16: > 168 registers), 256x4.)
-int select_variant(int R, int mode, Variant* out) {
-    switch (R) {
+int select_variant(int R, int mode, double alpha0, Variant* out) {
+    // FULL kernels form 2 alpha_{r+1} = 2 alpha0 + r + 1 as an exact integer conversion: they
+    // need 2 alpha0 to be an integer (the default alpha0 = 1, and every half-integer); other
+    // priors take the generic kernels (table-driven alpha, masked ring arithmetic)
+    const double a2 = 2.0 * alpha0;
+    const bool full_ok = a2 == std::floor(a2) && a2 >= 1.0 && a2 <= double(1 << 20);
+    switch (full_ok ? R : -1) {
         case 256: make_variant<32, 8, true, true, 8, 2>(mode, out); return 0;
         case 512: make_variant<64, 8, true, true, 4, 2>(mode, out); return 0;
         case 1024: make_variant<128, 8, true, true, 2, FBOCD_OCC3 ? 3 : 2>(mode, out); return 0;
@@ -50,6 +56,15 @@ int select_variant(int R, int mode, Variant* out) {
         default: break;
     }
     if (R < 2 || R > 4096) return -1;
+    if (!full_ok && (R == 256 || R == 512 || R == 1024 || R == 2048 || R == 4096)) {
+        // the generic kernels of the same shape (TAB2 up to 2048)
+        if (R == 256) { make_variant<32, 8, false, true, 8, 2>(mode, out); return 0; }
+        if (R == 512) { make_variant<64, 8, false, true, 4, 2>(mode, out); return 0; }
+        if (R == 1024) { make_variant<128, 8, false, true, 2, 2>(mode, out); return 0; }
+        if (R == 2048) { make_variant<256, 8, false, false, 1, 2>(mode, out); return 0; }
+        make_variant<512, 8, false, false, 1, 1>(mode, out);
+        return 0;
+    }
     if (R <= 32) { make_variant<32, 1, false, true, 8, 2>(mode, out); return 0; }
     if (R <= 256) { make_variant<32, 8, false, true, 8, 2>(mode, out); return 0; }
     if (R <= 512) { make_variant<64, 8, false, true, 4, 2>(mode, out); return 0; }
@@ -64,7 +79,7 @@ size_t variant_smem(const Variant& v, int R, bool persistent) {
     const bool pref = persistent && v.pref;  // only the persistent kernels carry the prefetch buffer
     const size_t grp = (pref ? v.group_smem_p : v.group_smem) +
                        (pref ? ((3 * size_t(R) * sizeof(double) + sizeof(SeriesScalars) + 15) & ~size_t(15)) : 0);
-    return bocd_fm_bytes(cell_ec(v.full, v.nt * v.j, pref), cell_logbits(v.full, v.nt * v.j)) + table_bytes(rows) +
+    return bocd_fm_bytes(cell_ec(v.full, v.nt * v.j, pref), cell_logbits(v.full, v.nt * v.j)) + table_bytes(rows, v.full) +
            size_t(v.spb) * grp;
 }
 

@@ -22,7 +22,7 @@ struct Variant {
     bool pref = false;         // the persistent kernels prefetch the next unit's state (TMA)
 };
 
-int select_variant(int R, int mode, Variant* out);  // mode: FALCON_TRUNC_MERGE / _DROP
+int select_variant(int R, int mode, double alpha0, Variant* out);  // mode: FALCON_TRUNC_MERGE / _DROP
 // dynamic shared memory of one CTA of variant v at ring size R (persistent or one-unit kernels)
 size_t variant_smem(const Variant& v, int R, bool persistent);
 

@@ -404,7 +404,7 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
     h->cfg = c;
     h->cfg.mu0 = nullptr;
     h->cfg.beta0 = nullptr;
-    if (fbocd::select_variant(c.R, c.trunc_mode, &h->var) != 0) {
+    if (fbocd::select_variant(c.R, c.trunc_mode, c.alpha0, &h->var) != 0) {
         delete h;
         return fail(nullptr, FALCON_EINVAL, "no kernel variant for this R");
     }
@@ -543,6 +543,8 @@ static int launch_update(falcon_bocd_t h, const double* x_dev, int64_t ld, int64
         P.ln_omH = log1p(-c.hazard);
         P.c_bucket = h->c_bucket;
         P.alpha_bucket = c.alpha0 + 0.5 * (c.R - 1);
+        P.al2_bucket = 2.0 * c.alpha0 + double(c.R - 1);
+        P.a2p1 = int(2.0 * c.alpha0) + 1;  // used by the FULL kernels only (2 alpha0 integral there)
         P.hr = (double)((long double)c.hazard / (1.0L - (long double)c.hazard));
         P.theta = c.threshold;
         P.alpha0 = c.alpha0;

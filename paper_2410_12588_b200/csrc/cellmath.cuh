@@ -44,6 +44,8 @@ struct CellTables {
     double exptab[kCellExpTab];  // 2^(j/2^EB), high word minus (j << (20 - EB))
     double2 log8[256];           // {invc_i, -log2(invc_i)}, z in [1 + i/2^LB, 1 + (i+1)/2^LB)
     double2 log10[1024];
+    double2 log8h[256];          // {invc_i, -log2(invc_i) / 2}: the FULL kernels' half-log (below)
+    double2 log10h[1024];
 };
 
 inline void fill_cell_tables(CellTables* t) {
@@ -54,31 +56,39 @@ inline void fill_cell_tables(CellTables* t) {
         b -= uint64_t(uint32_t(j) << (20 - kCellEB)) << 32;  // n 2^(20-EB) + hi(T'_j) = (k << 20) + hi(T_j)
         std::memcpy(&t->exptab[j], &b, sizeof(b));
     }
-    auto fill_log = [](double2* tab, int n) {
+    auto fill_log = [](double2* tab, int n, long double scale) {
         for (int i = 0; i < n; ++i) {
             const long double c = 1.0L + ((long double)i + 0.5L) / (long double)n;
             const double invc = (double)(1.0L / c);
             tab[i].x = invc;
-            tab[i].y = (double)(-log2l((long double)invc));
+            tab[i].y = (double)(-log2l((long double)invc) * scale);  // scale 1/2: exactly half
         }
     };
-    fill_log(t->log8, 256);
-    fill_log(t->log10, 1024);
+    fill_log(t->log8, 256, 1.0L);
+    fill_log(t->log10, 1024, 1.0L);
+    fill_log(t->log8h, 256, 0.5L);
+    fill_log(t->log10h, 1024, 0.5L);
 }
 
 // Polynomial coefficients (constant bank; uploaded with the fast-math constants): P0..P2 of
 // the log for LB = 8, 9, 10 at 3 (LB - 8), Q0..Q2 of the exp at 9.
-static __constant__ double c_cell[12];
-static const double kCellConstants[12] = {
+// 12..20: the log coefficients halved (exact), for the half-log lg(b)/2 of the FULL kernels.
+static __constant__ double c_cell[21];
+static const double kCellConstants[21] = {
     1.4426950408884385, -0.7213475204440444, 0.4808994476545776,   // LB = 8
     1.4426950408889305, -0.7213475204444544, 0.4808986221353932,   // LB = 9
     1.4426950408889614, -0.72134752044448, 0.4808984157560584,     // LB = 10
     // exp: Q0, Q1, Q2 (+ Q3 immediate; max error of r Q(r) 4.8e-18)
-    0.6931471805599428, 0.24022650695910044, 0.05550411375117056};
+    0.6931471805599428, 0.24022650695910044, 0.05550411375117056,
+    0.5 * 1.4426950408884385, 0.5 * -0.7213475204440444, 0.5 * 0.4808994476545776,
+    0.5 * 1.4426950408889305, 0.5 * -0.7213475204444544, 0.5 * 0.4808986221353932,
+    0.5 * 1.4426950408889614, 0.5 * -0.72134752044448, 0.5 * 0.4808984157560584};
 // leading coefficients rounded to 20 mantissa bits (DFMA immediates; the rounding is weighted
 // by r^4 <= 2^-36, i.e. below 1e-18)
 template <int LB>
 constexpr double kCellLogP3 = LB == 8 ? -0.3606746196746826 : -0.3606739044189453;
+template <int LB>
+constexpr double kCellLogP3h = 0.5 * kCellLogP3<LB>;
 constexpr double kCellExpQ3 = 0.009618133306503296;  // 0.009618129695226546 rounded
 
 constexpr unsigned kCellExpBase = 0x1A00u;
@@ -106,6 +116,25 @@ __device__ __forceinline__ double cell_log2(double b) {
     const double kt = __int2double_rn(int(tb >> 20) - 1023) + t.y;  // k + l_i (k exact)
     constexpr int o = 3 * (LB - 8);
     double p = fma(r, kCellLogP3<LB>, c_cell[o + 2]);
+    p = fma(p, r, c_cell[o + 1]);
+    p = fma(p, r, c_cell[o]);
+    return fma(r, p, kt);
+}
+
+// Half-log lg(b)/2, bit-for-bit half of cell_log2 (every coefficient and table value is
+// scaled by the exact factor 1/2, so each rounding is the scaled rounding).  The FULL kernels
+// form alpha_r lg beta' as (2 alpha_r)(lg beta'/2) with 2 alpha_r an exactly converted integer
+// (no alpha column in the per-r table); the product, and so every result, is unchanged.
+// The shared-memory log table must hold the halved entries (log8h / log10h).
+template <int EC, int LB>
+__device__ __forceinline__ double cell_log2h(double b) {
+    const unsigned tb = unsigned(__double2hiint(b));
+    const double2 t = cell_log_entry<EC, LB>(tb);
+    const double invs = __hiloint2double(__double2hiint(t.x) + 0x3FF00000 - int(tb & 0x7FF00000u), __double2loint(t.x));
+    const double r = fma(b, invs, -1.0);
+    const double kt = fma(__int2double_rn(int(tb >> 20) - 1023), 0.5, t.y);  // k/2 + l_i/2 (k exact)
+    constexpr int o = 12 + 3 * (LB - 8);
+    double p = fma(r, kCellLogP3h<LB>, c_cell[o + 2]);
     p = fma(p, r, c_cell[o + 1]);
     p = fma(p, r, c_cell[o]);
     return fma(r, p, kt);
