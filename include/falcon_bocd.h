@@ -165,6 +165,13 @@ int falcon_bocd_pending_events(falcon_bocd_t h, int64_t *n_out, void *stream);
 int falcon_bocd_read_posterior(falcon_bocd_t h, int64_t s0, int64_t count, double *logR_out,
                                double *mu_out, double *beta_out, void *stream);
 
+/* Kernel schedule of later update calls (test hook; results are bit-identical either way):
+ * 0 = automatic (default: calls of <= 64 steps with more series units than co-resident CTAs
+ * run the persistent kernels with TMA-prefetched state, all others one unit per CTA);
+ * 1 = persistent kernels for every call of <= 64 steps; 2 = one unit per CTA always.
+ * Returns FALCON_EINVAL for another value. */
+int falcon_bocd_set_schedule(falcon_bocd_t h, int32_t schedule);
+
 /* Number of observations absorbed so far (the next global t). */
 int falcon_bocd_steps(falcon_bocd_t h, int64_t *t_out);
 

@@ -80,6 +80,7 @@ def lib():
         "falcon_bocd_pending_events": (ctypes.c_int, [H, ctypes.POINTER(_i64), _P]),
         "falcon_bocd_read_posterior": (ctypes.c_int, [H, _i64, _i64, _P, _P, _P, _P]),
         "falcon_bocd_steps": (ctypes.c_int, [H, ctypes.POINTER(_i64)]),
+        "falcon_bocd_set_schedule": (ctypes.c_int, [H, _i32]),
         "falcon_bocd_kernel_shape": (ctypes.c_int, [H, ctypes.POINTER(_i32), ctypes.POINTER(_i32),
                                                     ctypes.POINTER(_i32)]),
         "falcon_bocd_destroy": (ctypes.c_int, [H]),
@@ -106,6 +107,7 @@ def lib():
 EXPORTED = ["falcon_bocd_abi_version", "falcon_bocd_config_init", "falcon_bocd_create",
             "falcon_bocd_update_chunk", "falcon_bocd_update_chunk_host", "falcon_bocd_changepoints", "falcon_bocd_changepoints_async",
             "falcon_bocd_pending_events", "falcon_bocd_read_posterior", "falcon_bocd_steps",
+            "falcon_bocd_set_schedule",
             "falcon_bocd_kernel_shape", "falcon_bocd_destroy", "falcon_bocd_last_error",
             "falcon_bocd_predictive_constants", "falcon_trace_generate", "falcon_bocd_debug_fastmath",
             "falcon_verify_changepoints", "falcon_pair_failslow", "falcon_classify_groups",

@@ -216,6 +216,12 @@ class BocdBatch:
                                                    _ptr(out[2]), _stream_ptr(stream, self.device)), self._h)
         return tuple(out)
 
+    def set_schedule(self, schedule: str):
+        """Kernel schedule of later calls: 'auto', 'persistent' (every call of <= 64 steps) or
+        'one_unit' (falcon_bocd_set_schedule; a test hook: results are bit-identical)."""
+        N.check(N.lib().falcon_bocd_set_schedule(self._h, {"auto": 0, "persistent": 1, "one_unit": 2}[schedule]),
+                self._h)
+
     @property
     def steps(self) -> int:
         t = ctypes.c_int64()

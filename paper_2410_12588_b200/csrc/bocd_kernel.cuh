@@ -46,8 +46,9 @@
 //                             + Dc_t;  DROP: q'_{R-1} is dropped
 //   A7  decision, MAP         p_new = R_t(1)/(1-R_t(0)) = q'_0/Z (MERGE) or q'_0/(Z - q'_{R-1}) (DROP);
 //                             r* = argmax over the growth slots (+ bucket), reduced every step when
-//                             the caller asks for per-step MAP / MAPRESET events, else on demand at
-//                             the steps that report an event (q' recomputed from the registers)
+//                             the caller asks for per-step MAP / MAPRESET events or theta < 1/2
+//                             (EAGER); otherwise r* = 1 at every PROB event (p_new > theta >= 1/2
+//                             puts more than half the growth mass in slot 1)
 // mu, beta, a live in registers for the whole call; x is staged in double-buffered
 // shared-memory tiles by 1-D TMA bulk copies (cp.async.bulk + mbarrier); state is
 // spilled to HBM once per call.  The cell loop is written stage-major over groups of
@@ -136,43 +137,17 @@ struct KParams {
     int tma_ok;  // x base 16-B aligned and ld even
 };
 
-// Series interleaving (FBOCD_IL = 2, an A/B alternative; default IL = 1).  IL = 2 interleaves
-// two series lane by lane (series = lane & 1) in the FULL kernels with at least two series per
-// CTA: at every step all series of a CTA read the same per-r table rows (the ring position ->
-// run length map depends only on the thread index and t), so the two lanes of a pair share
-// each table row: the {G, alpha} rows cost 2 shared-memory wavefronts per warp instead of 4
-// and y 1 instead of 2 (ncu, profiles/r02_ncu_c3_il2.txt).  But the log2-table rows of the
-// two series no longer cluster within a quarter-warp (+1.3 wavefronts of bank conflicts) and
-// each step's barrier couples 8 warps instead of 4: measured 78.2 ms vs 74.9 ms per C3 call
-// (an octet layout, lanes 0-7 / 8-15, loses the row sharing: LDS.128 does not merge
-// quarter-warps; 91.9 ms).  A "team" is the IL series that share warps; it synchronises as one.
-#ifndef FBOCD_IL
-#define FBOCD_IL 1
-#endif
-// The exp2 exponent needs only the lower clamp (the floor): every cell's joint is below the
-// step's evidence Z, which the frame Dc_t keeps within a few binades of 1 (Dc_t tracks the prior
-// predictive of x_t and the exponent of Zd_{t-1}; the predictive of any run length exceeds the
-// prior predictive by at most ~sqrt(2 alpha_r)), so 2^+1000 is unreachable for
-// finite x.  FBOCD_CLAMP1=0 restores the two-sided clamp (A/B: 75.6 vs 75.15 ms per C3 call).
-#ifndef FBOCD_CLAMP1
-#define FBOCD_CLAMP1 1
-#endif
-__host__ __device__ constexpr int series_il(int nt, bool full, int spb) {
-    return (FBOCD_IL == 2 && full && spb >= 2 && nt >= 32) ? 2 : 1;
-}
+// per-series partial sums of a step: one per warp
+__host__ __device__ constexpr int n_partials(int nt) { return nt / 32 > 0 ? nt / 32 : 1; }
 
-// per-series partial sums of a step: one per (warp, series) pair
-__host__ __device__ constexpr int n_partials(int nt, int il) { return nt * il / 32 > 0 ? nt * il / 32 : 1; }
-
-template <int NT, int TILE = kTile, int IL = 1>
+template <int NT, int TILE = kTile>
 struct __align__(16) GroupSmem {
     double xbuf[2][TILE];
     int kbuf[2][TILE];  // K0_t = round(l0_t) of the tile's steps
     // red2 / red1 / spec are double-buffered by step parity: a warp that runs ahead into
     // step t+1 cannot overwrite what a slower warp still reads after barrier t
-    double red2[2][n_partials(NT, IL)];
-    unsigned long long red1[2][n_partials(NT, IL)];  // EAGER argmax keys
-    unsigned long long red3[n_partials(NT, IL)];     // on-demand argmax (event steps)
+    double red2[2][n_partials(NT)];
+    unsigned long long red1[2][n_partials(NT)];  // EAGER argmax keys
     // generic kernels: q' of the cells r = R-2, R-1, 0 and G - alpha lg beta' of r = R-2;
     // ROT kernels: e0 / l0 hold q' / lg beta' of every thread's slot 0, entry NT = slot 1 of
     // thread 0, entry NT+1 (e0) = slot J-1 of thread NT-1 (the cells the tail needs)
@@ -229,13 +204,13 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
         : "memory");
 }
 
-// barrier of one team (NTEAM threads = IL series x NT)
-template <int NTEAM>
-__device__ __forceinline__ void team_sync(int team) {
-    if constexpr (NTEAM == 32) {
+// barrier of one series group (NT threads)
+template <int NT>
+__device__ __forceinline__ void group_sync(int g) {
+    if constexpr (NT == 32) {
         __syncwarp();
     } else {
-        asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(NTEAM) : "memory");
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(NT) : "memory");
     }
 }
 
@@ -260,27 +235,16 @@ __device__ __forceinline__ double key_val(unsigned long long k) {
     return __longlong_as_double(static_cast<long long>(k & ~0xFFFull));
 }
 
-// 64-bit max over the lanes of one series in a warp: IL = 1, two 32-bit REDUX passes over the
-// warp; IL = 2 (series = lane & 1), an xor butterfly over the lanes of the same parity
-template <int IL>
+// 64-bit max over the warp with two 32-bit REDUX passes
 __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long k) {
-    if constexpr (IL == 1) {
-        const unsigned hi = unsigned(k >> 32);
-        const unsigned hmax = __reduce_max_sync(0xffffffffu, hi);
-        const unsigned lmax = __reduce_max_sync(0xffffffffu, hi == hmax ? unsigned(k) : 0u);
-        return (static_cast<unsigned long long>(hmax) << 32) | lmax;
-    } else {
-#pragma unroll
-        for (int o = 16; o >= IL; o >>= 1) {
-            const unsigned long long v = __shfl_xor_sync(0xffffffffu, k, o);
-            k = v > k ? v : k;
-        }
-        return k;
-    }
+    const unsigned hi = unsigned(k >> 32);
+    const unsigned hmax = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned lmax = __reduce_max_sync(0xffffffffu, hi == hmax ? unsigned(k) : 0u);
+    return (static_cast<unsigned long long>(hmax) << 32) | lmax;
 }
 
-template <int NT, int TILE, int IL>
-__device__ __forceinline__ void issue_tile_tma(GroupSmem<NT, TILE, IL>& gs, const double* xrow, int k, int T) {
+template <int NT, int TILE>
+__device__ __forceinline__ void issue_tile_tma(GroupSmem<NT, TILE>& gs, const double* xrow, int k, int T) {
     const int base = k * TILE;
     const int n = min(TILE, T - base);
     fence_proxy_async();
@@ -298,9 +262,9 @@ __device__ __forceinline__ bool tile_tma_ok(const KParams& P, int k) {
 // TAB2: the per-r tables are stored twice (entries r and r+R) so the ring index
 // (t - p) mod R becomes (t - p + R) with no masking and compile-time offsets per cell.
 // per group: GroupSmem and (PREF) the prefetch buffer [mu R][beta R][a R][scalars]
-template <int NT, bool PREF, int IL>
+template <int NT, bool PREF>
 __host__ __device__ constexpr size_t group_bytes(int R) {
-    return sizeof(GroupSmem<NT, PREF ? kTileP : kTile, IL>) +
+    return sizeof(GroupSmem<NT, PREF ? kTileP : kTile>) +
            (PREF ? ((3 * size_t(R) * sizeof(double) + sizeof(SeriesScalars) + 15) & ~size_t(15)) : 0);
 }
 // bytes of the per-r tables for `entries` table rows: generic kernels {G_{r+1}, alpha_{r+1}}
@@ -353,9 +317,8 @@ __device__ __forceinline__ double prior_l2(double x, double mu0, double be0, dou
 //          its prior reset is a compile-time register write, and every table
 //          offset of a slot is a compile-time constant.
 //   TAB2 : doubled per-r tables (generic R <= 2048);
-//   EAGER: the MAP run length r* is reduced every step (per-step MAP output or
-//          MAPRESET events requested); otherwise it is reduced on demand, from
-//          q' recomputed out of the registers, only at steps that report an event.
+//   EAGER: the MAP run length r* is reduced every step (per-step MAP output,
+//          MAPRESET events, or theta < 1/2); otherwise r* = 1 at every PROB event.
 // ---------------------------------------------------------------------------
 template <int NT, int J, bool FULL, bool TAB2>
 __host__ __device__ constexpr int table_entries(int R) {
@@ -372,11 +335,8 @@ constexpr unsigned kFmBase = 0x800u;
 // free, for the R <= 1024 FULL kernels; 8 otherwise, where the per-r tables are larger).
 // The persistent prefetching kernels (HBM-bound streaming) take 4 copies and 64-step x tiles
 // so that two CTAs with their prefetch buffers still fit one SM.
-#ifndef FBOCD_OCC3
-#define FBOCD_OCC3 0  // A/B: R = 1024 at 3 CTAs per SM (85 registers, 8 exp2 copies)
-#endif
 __host__ __device__ constexpr int cell_ec(bool full, int r_full, bool pref) {
-    return pref ? 4 : ((full && r_full <= 1024 && !(FBOCD_OCC3 && r_full == 1024)) ? 16 : 8);
+    return pref ? 4 : ((full && r_full <= 1024) ? 16 : 8);
 }
 __host__ __device__ constexpr unsigned bocd_fm_bytes(int ec, int lb) {
     return (lb == 8 ? (ec == 16 ? cell_tables_end<16, 8>() : ec == 8 ? cell_tables_end<8, 8>()
@@ -389,9 +349,8 @@ static_assert(kFmBase + kFmSmemBytes - 2048u <= kCellExpBase, "fast-math tables 
 
 // exp2 of a cell: q' = 2^(ell - Dc) with C7 = 1.5 2^52 + 2^31 - 256 Dc (cellmath.cuh's
 // reduction with the frame folded into the rounding constant).  Below 2^-1021: floored to
-// [2^-1021, 2^-1019); exponent clamped at +1000.  The cell loop evaluates
-// the same operations stage by stage; the on-demand MAP recomputation calls this and must
-// agree bit for bit.
+// [2^-1021, 2^-1019).  The cell loop evaluates
+// the same operations stage by stage (this scalar form serves the accuracy probe).
 template <int EC>
 __device__ __forceinline__ double cell_exp2(double ell, double C7, unsigned lbe) {
     const double zf = fma(ell, kCellExpScale, C7);
@@ -402,7 +361,7 @@ __device__ __forceinline__ double cell_exp2(double ell, double C7, unsigned lbe)
     p = fma(p, re, c_cell[10]);
     p = fma(p, re, c_cell[9]);
     const double qq = p * re;
-    const unsigned kc = max(min(ki, kCellExpHi), kCellExpLo);
+    const unsigned kc = max(ki, kCellExpLo);  // the floor only (see the cell loop)
     const double Ts = __hiloint2double(int(kc * (1048576u >> kCellEB)) + __double2hiint(T), __double2loint(T));
     return fma(Ts, qq, Ts);
 }
@@ -435,11 +394,8 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     // kDynBase, checked at entry with the fast-math tables)
     constexpr unsigned kGyBase = kDynBase + bocd_fm_bytes(EC, LB);  // FULL: {G_{r+1}, y_r} rows
     constexpr int TILE = PREF ? kTileP : kTile;
-    constexpr int IL = series_il(NT, FULL, SPB);  // series interleaved per warp (lane & 1)
-    constexpr int NTEAM = NT * IL;                // threads of one team (IL series)
-    constexpr int W = n_partials(NT, IL);         // per-series partials of a step (one per warp)
-    static_assert(SPB % IL == 0, "series per CTA must be a multiple of the interleave");
-    using GS = GroupSmem<NT, TILE, IL>;
+    constexpr int W = n_partials(NT);  // per-series partials of a step (one per warp)
+    using GS = GroupSmem<NT, TILE>;
     const int R = FULL ? NT * J : P.R;
     const int RT = table_entries<NT, J, FULL, TAB2>(R);
     // dynamic shared memory: [fast-math tables, cell tables (bocd_fm_bytes)][per-r tables][groups]
@@ -469,16 +425,11 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         for (int k = threadIdx.x; k < (1 << LB); k += blockDim.x) lg[k] = src[k];
     }
     const unsigned lb = 8u * (threadIdx.x & unsigned(EC - 1));  // exp2 table copy of this lane
+    const int g = threadIdx.x / NT;
+    const int i = threadIdx.x % NT;
     const int lane = threadIdx.x & 31;
-    const int team = threadIdx.x / NTEAM;
-    const int tt = threadIdx.x % NTEAM;
-    // series g of the CTA and the thread's index i within its series (consecutive i = the
-    // lanes of one parity within a warp, then the next warp)
-    const int g = IL == 2 ? team * 2 + (lane & 1) : team;
-    const int i = IL == 2 ? ((tt >> 5) << 4) + (lane >> 1) : tt;
-    const int w = IL == 2 ? (tt >> 5) : (i >> 5);  // this series' partial index
-    const bool red_lane = IL == 2 ? lane < 2 : lane == 0;  // writes the warp's partial of its series
-    GS& gs = *reinterpret_cast<GS*>(gbase + size_t(g) * group_bytes<NT, PREF, IL>(R));
+    const int w = i >> 5;
+    GS& gs = *reinterpret_cast<GS*>(gbase + size_t(g) * group_bytes<NT, PREF>(R));
     // PREF: the prefetched next-unit state [mu R][beta R][a R][SeriesScalars], position order
     double* const pf = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(&gs) + sizeof(GS));
     SeriesScalars* const pf_sc = reinterpret_cast<SeriesScalars*>(pf + 3 * size_t(R));
@@ -509,21 +460,17 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         tma_load_1d(pf + 2 * size_t(R), P.st_a + sn * R, unsigned(rb), &gs.mbar_st);
         tma_load_1d(pf_sc, P.scal + sn, unsigned(sizeof(SeriesScalars)), &gs.mbar_st);
     };
-    if constexpr (PREF) {  // (a series past the end prefetches the last series' rows; see below)
+    if constexpr (PREF) {
         const int64_t s0 = int64_t(blockIdx.x) * SPB + g;
-        if (i == 0 && P.t0 > 0 && blockIdx.x < nunits && int64_t(blockIdx.x) * SPB + int64_t(team) * IL < P.S)
-            issue_state(s0 < P.S ? s0 : P.S - 1);
+        if (i == 0 && P.t0 > 0 && blockIdx.x < nunits && s0 < P.S) issue_state(s0);
     }
 
     for (int64_t u = blockIdx.x; u < nunits; u += PERSIST ? int64_t(gridDim.x) : nunits) {
-        // team-uniform exit: later units only have larger s.  A series past the end in a team
-        // that still has a live one runs on a copy of the last series' rows and writes nothing.
-        if (u * SPB + int64_t(team) * IL >= P.S) break;
-        const bool act = u * SPB + g < P.S;
-        const int64_t s = act ? u * SPB + g : P.S - 1;
+        const int64_t s = u * SPB + g;
+        if (s >= P.S) break;  // group-uniform; later units only have larger s
         const double* xrow = P.x + s * P.ld;
         // Prefetch tile 0 (TMA) as early as possible.
-        if (i == 0 && ntiles > 0 && tile_tma_ok<TILE>(P, 0)) issue_tile_tma<NT, TILE, IL>(gs, xrow, 0, P.T);
+        if (i == 0 && ntiles > 0 && tile_tma_ok<TILE>(P, 0)) issue_tile_tma<NT, TILE>(gs, xrow, 0, P.T);
 
         // ---- load or initialise the state --------------------------------
         double mu[J], be[J], a[J];
@@ -567,7 +514,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             gs.flags = sc.flags | (ok ? 0 : 2) | (fm_ok ? 0 : 4);
             gs.dc0 = sc.dc;
         }
-        team_sync<NTEAM>(team);
+        group_sync<NT>(g);
         // the prior and the rarely used per-series scalars stay in shared memory (gs) so
         // that the step loop keeps its registers for the cells
         int zexp = ((__double2hiint(gs.zd_prev) >> 20) & 0x7FF) - 1023;  // binary exponent of Zd_{t-1}
@@ -615,11 +562,10 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             if (BUCKET_PRED) L0p = cell_log2h<EC, LB>(be[0]);  // = the previous step's lg beta'/2 of slot 0
         }
         if constexpr (PREF) {
-            // pf is free once every thread of the team has read it: prefetch the next unit
-            team_sync<NTEAM>(team);
-            const int64_t un = u + int64_t(gridDim.x);
-            const int64_t sn = un * SPB + g;
-            if (i == 0 && P.t0 > 0 && un * SPB + int64_t(team) * IL < P.S) issue_state(sn < P.S ? sn : P.S - 1);
+            // pf is free once every thread of the group has read it: prefetch the next unit
+            group_sync<NT>(g);
+            const int64_t sn = s + int64_t(gridDim.x) * SPB;
+            if (i == 0 && P.t0 > 0 && sn < P.S) issue_state(sn);
         }
         bool nonfinite = false;
         if (i == 0 && P.out_logz) gs.lzd_prev = fast_log2(gs.zd_prev, kFmBase);
@@ -630,13 +576,13 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             const int buf = k & 1;
             // prefetch the next tile into the other buffer (its previous readers all
             // passed at least one group barrier since their last read)
-            if (i == 0 && k + 1 < ntiles && tile_tma_ok<TILE>(P, k + 1)) issue_tile_tma<NT, TILE, IL>(gs, xrow, k + 1, P.T);
+            if (i == 0 && k + 1 < ntiles && tile_tma_ok<TILE>(P, k + 1)) issue_tile_tma<NT, TILE>(gs, xrow, k + 1, P.T);
             if (tile_tma_ok<TILE>(P, k)) {
                 mbar_wait(&gs.mbar[buf], (xphase >> buf) & 1u);
                 xphase ^= 1u << buf;
             } else {
                 for (int q = i; q < n; q += NT) gs.xbuf[buf][q] = xrow[base + q];
-                team_sync<NTEAM>(team);
+                group_sync<NT>(g);
             }
             // the tile's exponent references K0_t = round(l0_t), spread over the group
             for (int q = i; q < n; q += NT) {
@@ -647,7 +593,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                                        : prior_l2(xq, gs.mu0, gs.beta0, gs.aprior, s_ca[0], s_y[0], kFmBase);
                 gs.kbuf[buf][q] = __double2int_rn(fmin(fmax(l0, -kK0Max), kK0Max));
             }
-            team_sync<NTEAM>(team);
+            group_sync<NT>(g);
             // ROT: the tile's steps run in segments that end at a rotation step (iB = NT-1); the
             // slot rotation, the fold of the pending weights and the frame rebase run between
             // segments (register permutations outside the step loop: no copies inside it)
@@ -804,11 +750,12 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                         const double qq = pe[kk] * re[kk];
                         // 2^e, e = floor(n/256) for n = ki - 2^31, floored at 2^-1021 and clamped at
                         // +1000; hi word = kc * 2^12 + hi(T'_j) (cellmath.cuh)
-#if FBOCD_CLAMP1
+                        // only the lower clamp (the floor): every cell's joint is below the step's
+                        // evidence Z, which the frame Dc_t keeps within a few binades of 1 (Dc_t tracks
+                        // the prior predictive of x_t and the exponent of Zd_{t-1}; no run length's
+                        // predictive exceeds the prior predictive by more than ~sqrt(2 alpha_r)), so
+                        // 2^+1000 is unreachable for finite x
                         const unsigned kc = max(ki[kk], kCellExpLo);
-#else
-                        const unsigned kc = max(min(ki[kk], kCellExpHi), kCellExpLo);
-#endif
                         const double Ts = __hiloint2double(int(kc * (1048576u >> kCellEB)) + __double2hiint(Tv[kk]),
                                                            __double2loint(Tv[kk]));
                         double E = fma(Ts, qq, Ts);
@@ -838,14 +785,14 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 // (xor butterfly over the series' lanes of the warp, then a fixed-order
                 // pairwise sum of the W per-warp partials: deterministic)
 #pragma unroll
-                for (int o = 16; o >= IL; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-                if constexpr (EAGER) key = warp_max_u64<IL>(key);
+                for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+                if constexpr (EAGER) key = warp_max_u64(key);
                 if constexpr (W > 1) {
-                    if (red_lane) {
+                    if (lane == 0) {
                         gs.red2[par][w] = sum;
                         if (EAGER) gs.red1[par][w] = key;
                     }
-                    team_sync<NTEAM>(team);
+                    group_sync<NT>(g);
                     sum = tree_sum<W>(gs.red2[par]);
                     if constexpr (EAGER) {
 #pragma unroll
@@ -855,7 +802,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                         }
                     }
                 } else {
-                    team_sync<NTEAM>(team);
+                    group_sync<NT>(g);
                 }
                 // ---- the scalar tail (A5-A8): group-uniform, no transcendentals -----------
                 const double Z = sum;
@@ -911,10 +858,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 if (i == 0) gs.zd_prev = Zd;
                 // ---- rare path (group-uniform): MAP run length r* (A7), events (A8), per-step
                 // outputs ----------------------------------------------------------------
-                // (team-uniform: the on-demand argmax below synchronises the team; with IL = 2
-                // every warp holds lanes of both series, so a warp vote sees the whole team)
-                const bool ev_team = IL == 2 ? __any_sync(0xffffffffu, (fl & P.ev_mask) != 0u) : (fl & P.ev_mask) != 0u;
-                if (EAGER || ev_team || any_out) {
+                if (EAGER || (fl & P.ev_mask) || any_out) {
                     int r_ex = -1;
                     double qex = 0.0;
                     if constexpr (EAGER) {
@@ -922,70 +866,26 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                             r_ex = key_r(key);
                             qex = key_val(key);
                         }
-                    } else if (ev_team) {  // on demand: an event at this step (in this team)
-                        unsigned long long kb = 0ull;
-                        // one cell at a time (runtime slot index, register arrays read by selects):
-                        // the recomputation must not raise the register pressure of the step loop
-#pragma unroll 1
-                        for (int j = 0; j < J; ++j) {
-                            const int p = i + NT * j;
-                            if (FULL || p < R) {
-                                int r, id;
-                                if (ROT || TAB2) {
-                                    id = ib - NT * j;
-                                    r = id - ((id >= R) ? R : 0);
-                                } else {
-                                    r = tmod - p;
-                                    r += (r < 0) ? R : 0;
-                                    id = r;
-                                }
-                                if (r <= r_elig) {  // the eligible cells kept their a and beta'
-                                    double bj = be[0], aj = a[0];
-#pragma unroll
-                                    for (int jj = 1; jj < J; ++jj) {
-                                        bj = (jj == j) ? be[jj] : bj;
-                                        aj = (jj == j) ? a[jj] : aj;
-                                    }
-                                    // the loop's arithmetic, one cell (FULL: half-log x 2 alpha)
-                                    const double2 c2 = FULL ? make_double2(s_gy[id].x, __int2double_rn(P.a2p1 + r))
-                                                            : s_ca[id];
-                                    const double Ln = FULL ? cell_log2h<EC, LB>(bj) : cell_log2<EC, LB>(bj);
-                                    double E = cell_exp2<EC>(fma(-c2.y, Ln, aj + c2.x), C7, lb);
-                                    if (ROT && j == 0) E *= wq;
-                                    const unsigned long long kq = argmax_key(E, r);
-                                    kb = kq > kb ? kq : kb;
-                                }
-                            }
-                        }
-                        kb = warp_max_u64<IL>(kb);
-                        if constexpr (W > 1) {
-                            if (red_lane) gs.red3[w] = kb;
-                            team_sync<NTEAM>(team);
-#pragma unroll
-                            for (int ww = 0; ww < W; ++ww) {
-                                const unsigned long long o = gs.red3[ww];
-                                kb = o > kb ? o : kb;
-                            }
-                            team_sync<NTEAM>(team);  // red3 is reused at the next event step
-                        }
-                        if (kb != 0ull) {
-                            r_ex = key_r(kb);
-                            qex = key_val(kb);
-                        }
                     }
                     if (EAGER || (fl & P.ev_mask)) {
-                        int rstar;
-                        if (merge) {
-                            // bucket (qA + qB) vs the best growth slot (ties -> the smaller run length)
-                            rstar = (r_ex < 0 || (qA + qB) > qex) ? R - 1 : r_ex + 1;
-                        } else {
-                            rstar = r_ex + 1;
+                        // lazy kernel: only PROB events reach here, and it runs only for theta >= 1/2
+                        // (capi.cu): p_new = R_t(1) / sum_{r>=1} R_t(r) > theta >= 1/2 makes R_t(1)
+                        // larger than all the other growth slots together, so r* = 1 and
+                        // cp_index = t exactly.  EAGER: the step's reduced argmax key.
+                        int rstar = 1;
+                        if constexpr (EAGER) {
+                            if (merge) {
+                                // bucket (qA + qB) vs the best growth slot (ties -> the smaller run length)
+                                rstar = (r_ex < 0 || (qA + qB) > qex) ? R - 1 : r_ex + 1;
+                            } else {
+                                rstar = r_ex + 1;
+                            }
                         }
                         if (EAGER && tl >= tl_min && rstar < min(map_prev + 1, R - 1)) fl |= 2u;
                         map_prev = rstar;
-                        if (i == 0 && act && P.out_map) P.out_map[s * P.ld_o + tl] = rstar;
+                        if (i == 0 && P.out_map) P.out_map[s * P.ld_o + tl] = rstar;
                         if (fl & P.ev_mask) {
-                            if (i == 0 && act && ev_count < P.ev_cap) {
+                            if (i == 0 && ev_count < P.ev_cap) {
                                 EventRec ev;
                                 ev.t = t;
                                 ev.cp_index = t - rstar + 1;
@@ -997,7 +897,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                             ++ev_count;
                         }
                     }
-                    if (i == 0 && act) {
+                    if (i == 0) {
                         if (P.out_pnew) P.out_pnew[s * P.ld_o + tl] = pnum * fast_rcp(Zp);
                         if (P.out_logz) {  // kept mass (A4)
                             const double lzd = fast_log2(Zd, kFmBase);
@@ -1046,18 +946,18 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         }
         // ---- spill -----------------------------------------------------------
         if (nonfinite) atomicOr(&gs.flags, 1);
-        team_sync<NTEAM>(team);
+        group_sync<NT>(g);
 #pragma unroll
         for (int j = 0; j < J; ++j) {
             const int p = ROT ? i + NT * ((j + phi) & (J - 1)) : i + NT * j;
-            if ((FULL || p < R) && act) {
+            if (FULL || p < R) {
                 P.st_mu[sbase + p] = mu[j];
                 P.st_beta[sbase + p] = be[j];
                 P.st_a[sbase + p] = a[j];
             }
         }
-        if (ROT && act) P.st_w[s * NT + i] = wq;
-        if (i == 0 && act) {
+        if constexpr (ROT) P.st_w[s * NT + i] = wq;
+        if (i == 0) {
             SeriesScalars sc;
             sc.mu0 = gs.mu0;
             sc.beta0 = gs.beta0;
@@ -1070,7 +970,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             P.scal[s] = sc;
             if (sc.flags) atomicOr(P.err, unsigned(sc.flags));
         }
-        team_sync<NTEAM>(team);  // gs is reused by the next unit
+        group_sync<NT>(g);  // gs is reused by the next unit
     }
 }
 

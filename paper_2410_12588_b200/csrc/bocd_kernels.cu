@@ -21,9 +21,8 @@ static void make_variant_mode(Variant* out) {
     v.spb = SPB;
     v.full = FULL;
     v.tab2 = TAB2;
-    constexpr int IL = series_il(NT, FULL, SPB);
-    v.group_smem = sizeof(GroupSmem<NT, kTile, IL>);
-    v.group_smem_p = sizeof(GroupSmem<NT, kPrefOk<NT, J, FULL> ? kTileP : kTile, IL>);  // (+ PREF buffer): group_bytes
+    v.group_smem = sizeof(GroupSmem<NT, kTile>);
+    v.group_smem_p = sizeof(GroupSmem<NT, kPrefOk<NT, J, FULL> ? kTileP : kTile>);  // (+ PREF buffer): group_bytes
     *out = v;
 }
 // the truncation mode is a template parameter of the kernels (MERGE / DROP specialised tails)
@@ -50,7 +49,7 @@ int select_variant(int R, int mode, double alpha0, Variant* out) {
     switch (full_ok ? R : -1) {
         case 256: make_variant<32, 8, true, true, 8, 2>(mode, out); return 0;
         case 512: make_variant<64, 8, true, true, 4, 2>(mode, out); return 0;
-        case 1024: make_variant<128, 8, true, true, 2, FBOCD_OCC3 ? 3 : 2>(mode, out); return 0;
+        case 1024: make_variant<128, 8, true, true, 2, 2>(mode, out); return 0;
         case 2048: make_variant<256, 8, true, false, 1, 2>(mode, out); return 0;
         case 4096: make_variant<512, 8, true, false, 1, 1>(mode, out); return 0;
         default: break;

@@ -62,6 +62,7 @@ struct falcon_bocd_s {
     double* d_ologz = nullptr;
     size_t out_cap = 0;
     bool poisoned = false;
+    int schedule = 0;  // falcon_bocd_set_schedule: 0 auto, 1 persistent, 2 one unit per CTA
     std::string err;
 };
 
@@ -576,12 +577,15 @@ static int launch_update(falcon_bocd_t h, const double* x_dev, int64_t ld, int64
         const int64_t units = (c.n_series + h->var.spb - 1) / h->var.spb;
         // streaming calls (few steps): persistent grid, tables set up once per CTA and the next
         // unit's state prefetched; long calls: one unit per CTA.  Identical arithmetic.
-        const bool persist = n <= kPersistMaxSteps && units > h->grid_cap;
+        const bool persist = h->schedule == 1 ? n <= kPersistMaxSteps
+                           : h->schedule == 2 ? false
+                                              : (n <= kPersistMaxSteps && units > h->grid_cap);
         const int64_t grid = persist ? h->grid_cap : units;
         void* args[] = {&P};
         // r* every step only when it is an output (per-step MAP, MAPRESET events); otherwise
-        // the kernel reduces it on demand at the steps that report an event.
-        const bool eager = (c.event_mask & FALCON_EV_MAPRESET) || omap;
+        // r* = 1 at every PROB event (theta >= 1/2).
+        // theta < 1/2 also needs it at PROB events (bocd_kernel.cuh: r* = 1 only for theta >= 1/2)
+        const bool eager = (c.event_mask & FALCON_EV_MAPRESET) || omap || c.threshold < 0.5;
         const void* fn = persist ? (eager ? h->var.fn_eager_p : h->var.fn_p) : (eager ? h->var.fn_eager : h->var.fn);
         cudaError_t e = cudaLaunchKernel(fn, dim3(unsigned(grid)),
                                          dim3(unsigned(h->var.nt * h->var.spb)), args,
@@ -883,6 +887,12 @@ int falcon_bocd_read_posterior(falcon_bocd_t h, int64_t s0, int64_t count, doubl
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (tmp) cudaFree(tmp);
     if (e != cudaSuccess) return cuda_fail(h, e, "read_posterior");
+    return FALCON_OK;
+}
+
+int falcon_bocd_set_schedule(falcon_bocd_t h, int32_t schedule) {
+    if (!h || schedule < 0 || schedule > 2) return FALCON_EINVAL;
+    h->schedule = schedule;
     return FALCON_OK;
 }
 

@@ -38,7 +38,6 @@ constexpr int kCellEB = 8;  // exp2 table bits (degree-4 fit; 9 bits with degree
 constexpr int kCellExpTab = 1 << kCellEB;
 constexpr double kCellExpScale = double(kCellExpTab);          // the rounding grid 2^-EB
 constexpr unsigned kCellExpLo = 0x80000000u - 1021u * kCellExpTab;  // 2^-1021: floor / dead
-constexpr unsigned kCellExpHi = 0x80000000u + 1000u * kCellExpTab + (kCellExpTab - 1u);  // 2^+1000
 
 struct CellTables {
     double exptab[kCellExpTab];  // 2^(j/2^EB), high word minus (j << (20 - EB))

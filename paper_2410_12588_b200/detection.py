@@ -65,3 +65,41 @@ def latency(first, onset, truth):
         return {"n": 0}
     return {"n": int(d.size), "median": float(np.median(d)), "p90": float(np.percentile(d, 90)),
             "max": int(d.max())}
+
+
+def evaluate(spec, cfg, T: int, min_len: int = 20, event_capacity: int = 8192, device="cuda"):
+    """Scores of raw BOCD and BOCD+V on one labelled synthetic suite (tracegen spec over its
+    S series x T steps), every detector running on the GPU through the C ABI: the BOCD batch
+    (PROB events, p_new > 0.9 of P:770, and MAP resets), falcon_verify_changepoints (the 10%
+    rule of P:772-779) and falcon_pair_failslow.  Returns the dict tools/detection_accuracy.py
+    prints (Tables 5-6 scores per detector)."""
+    import torch
+
+    from . import _native as N, bocd
+    S = spec.n_series
+    x = torch.empty((S, T), dtype=torch.float64, device=device)
+    bocd.DeviceTrace(spec, device).generate(x, 0, 0)
+    b = bocd.BocdBatch(S, R=cfg.R, hazard=cfg.hazard, prior_first_obs=True, prior_cov=cfg.prior_cov,
+                       event_mask=3, event_capacity=event_capacity)
+    b.update_chunk(x)
+    ev, dropped = b.changepoints()
+    b.close()
+    truth, onset = series_truth(spec, 0, T, min_len=min_len)
+    out = {"config": cfg.name, "sigma": float(spec.sigma[0]), "series": S, "steps": T, "R": cfg.R,
+           "slowed_series": int(truth.sum()), "events_dropped": bool(dropped)}
+    for label, mask in (("prob", 1), ("prob_mapreset", 3)):
+        raw = ev[(ev["flags"] & mask) != 0]
+        first_raw = first_flag(raw["series"], raw["t"], S)
+        ver = bocd.verify_changepoints(x, raw, t_lo=0)
+        pairs = bocd.pair_failslow(ver)
+        # a verified change point is known once its 20-sample after-window is complete
+        deg = ver[ver["status"] == N.CP_DEGRADE]
+        t_known = np.maximum(deg["t"], deg["cp_index"] + 19)
+        first_v = first_flag(deg["series"], t_known, S)
+        flagged_v = np.zeros(S, dtype=bool)
+        flagged_v[pairs["series"]] = True  # every fail-slow event starts at a verified DEGRADE
+        out["bocd_" + label] = {**confusion(first_raw >= 0, truth), "raw_events": int(len(raw)),
+                                "delay_steps": latency(first_raw, onset, truth)}
+        out["bocd_v_" + label] = {**confusion(flagged_v, truth), "failslow_events": int(len(pairs)),
+                                  "delay_steps": latency(np.where(flagged_v, first_v, -1), onset, truth)}
+    return out

@@ -20,13 +20,14 @@ from paper_2410_12588_b200 import bocd, tracegen  # noqa: E402
 
 
 def _run_gpu(x, R, H, mode, chunks=None, kappa0=1.0, alpha0=1.0, mu0=None, beta0=None,
-             prior_cov=0.05, ev_mask=1, cap=64):
+             prior_cov=0.05, ev_mask=1, cap=64, schedule="auto", threshold=0.9):
     S, T = x.shape
     first = mu0 is None
     b = bocd.BocdBatch(S, R=R, hazard=H, kappa0=kappa0, alpha0=alpha0,
                        mu0=0.0 if first else mu0, beta0=1.0 if first else beta0,
                        prior_first_obs=first, prior_cov=prior_cov, trunc_mode=mode,
-                       event_mask=ev_mask, event_capacity=cap)
+                       event_mask=ev_mask, event_capacity=cap, threshold=threshold)
+    b.set_schedule(schedule)
     xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
     chunks = chunks or [T]
     maps, pn, lz = [], [], []
@@ -44,9 +45,9 @@ def _run_gpu(x, R, H, mode, chunks=None, kappa0=1.0, alpha0=1.0, mu0=None, beta0
 
 
 def _oracle(oracle_mod, x, R, H, mode, mu0=None, beta0=None, prior_cov=0.05, kappa0=1.0,
-            alpha0=1.0, traj=False):
+            alpha0=1.0, traj=False, threshold=0.9):
     first = mu0 is None
-    return oracle_mod.run(x, R, H, kappa0, alpha0, mu0, beta0, trunc_mode=mode,
+    return oracle_mod.run(x, R, H, kappa0, alpha0, mu0, beta0, trunc_mode=mode, threshold=threshold,
                           prior_first_obs=first, prior_cov=prior_cov, traj=traj, n_threads=0)
 
 
@@ -266,8 +267,8 @@ def test_repeat_runs_bit_identical():
 
 @pytest.mark.parametrize("R,mode", [(1024, 0), (1024, 1), (2048, 0), (300, 0)])
 def test_lazy_map_equals_eager_map(R, mode):
-    """The on-demand MAP (recomputed q' at event steps, no per-step outputs: the bench's kernel)
-    reports exactly the PROB events of the EAGER kernel (r* reduced every step)."""
+    """The lazy kernel (no per-step outputs: the bench's kernel; r* = 1 at every PROB event for
+    theta >= 1/2) reports exactly the PROB events of the EAGER kernel (r* reduced every step)."""
     cfg = tracegen.CONFIGS["C3"]
     x = tracegen.generate(tracegen.make_spec(cfg), 0, 64, 0, max(2 * R, 1500))
     xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
@@ -297,3 +298,80 @@ def test_partial_cta_series_counts(oracle_mod, R, S):
         assert np.array_equal(a[k], b[k], equal_nan=True), k
     res = _oracle(oracle_mod, x, R, cfg.hazard, 0, prior_cov=0.3)
     _full_check(a, res, mask=1, name=f"C3[11:{11 + S},:{T}] R={R} S={S}")
+
+
+@pytest.mark.parametrize("R", [256, 512, 2048, 4096, 300])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_persistent_kernels_bit_exact(oracle_mod, R, mode):
+    """Every persistent kernel (forced with falcon_bocd_set_schedule: the PREF kernels with
+    TMA-prefetched state at R <= 1024, the plain persistent ones at R = 2048 / 4096 including
+    the MERGE bucket's continuation, the generic-R ones) over 1-step and short calls equals
+    one long one-unit-per-CTA call bit for bit, EAGER and lazy, and sampled series match the
+    oracle.  S leaves the last CTA partly empty."""
+    cfg = tracegen.CONFIGS["C3"]
+    S = 7 if R >= 2048 else 21
+    T = R + 150 if R <= 512 else 300
+    x = tracegen.generate(tracegen.make_spec(cfg, n_series=64), 0, S, 0, T)
+    chunks = [1] * 30 + [64, 3, 1] + [T - 98]
+    a = _run_gpu(x, R, cfg.hazard, mode, prior_cov=0.3, ev_mask=3, cap=512, schedule="one_unit")
+    b = _run_gpu(x, R, cfg.hazard, mode, prior_cov=0.3, ev_mask=3, cap=512, chunks=chunks,
+                 schedule="persistent")
+    for k in ("map", "pnew", "logz", "logR", "mu", "beta"):
+        assert np.array_equal(a[k], b[k], equal_nan=True), k
+    assert np.array_equal(a["events"], b["events"])
+    # lazy persistent kernels (PROB only, no per-step outputs)
+    xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    logs = []
+    for sched, parts in (("one_unit", [T]), ("persistent", chunks)):
+        h = bocd.BocdBatch(S, R=R, hazard=cfg.hazard, prior_first_obs=True, prior_cov=0.3, trunc_mode=mode,
+                           event_mask=1, event_capacity=512)
+        h.set_schedule(sched)
+        t0 = 0
+        for n in parts:
+            h.update_chunk(xd[:, t0:t0 + n])
+            t0 += n
+        logs.append((h.read_posterior()[0].cpu().numpy(), h.changepoints()[0]))
+        h.close()
+    assert np.array_equal(logs[0][0], logs[1][0], equal_nan=True)
+    assert np.array_equal(logs[0][1], logs[1][1])
+    res = _oracle(oracle_mod, x[:3], R, cfg.hazard, mode, prior_cov=0.3)
+    st = parity.compare_steps(b["map"][:3], b["pnew"][:3], b["logz"][:3], res, 0.9)
+    st["max_dlogR"] = parity.compare_logR(b["logR"][:3], res.logR_final)
+    parity.record(f"persistent R={R} mode={mode} [0:3,:{T}]", st)
+
+
+@pytest.mark.parametrize("R", [1024, 4096])
+@pytest.mark.parametrize("kappa0,alpha0", [(0.5, 1.5), (2.0, 0.7), (1.0, 3.0)])
+def test_priors_and_per_series_arrays(oracle_mod, R, kappa0, alpha0):
+    """kappa0, alpha0 != 1 at the BASELINE ring sizes (2 alpha0 integral -> FULL kernels with
+    the integer alpha; alpha0 = 0.7 -> the generic kernels of the same shape), with per-series
+    mu0 / beta0 HOST arrays passed through falcon_bocd_config (not prior_first_obs)."""
+    cfg = tracegen.CONFIGS["C3"]
+    S = 6
+    T = R + 200 if R == 1024 else 1200
+    x = tracegen.generate(tracegen.make_spec(cfg, n_series=S), 0, S, 0, T)
+    rng = np.random.default_rng(R + int(10 * alpha0))
+    mu0 = x[:, 0] * rng.uniform(0.8, 1.2, S)
+    beta0 = alpha0 * (rng.uniform(0.1, 0.5, S) * x[:, 0]) ** 2
+    g = _run_gpu(x, R, cfg.hazard, 0, kappa0=kappa0, alpha0=alpha0, mu0=mu0, beta0=beta0, ev_mask=3, cap=2048)
+    res = _oracle(oracle_mod, x, R, cfg.hazard, 0, mu0=mu0, beta0=beta0, kappa0=kappa0, alpha0=alpha0)
+    assert not g["dropped"]
+    _full_check(g, res, mask=3, name=f"priors R={R} kappa0={kappa0} alpha0={alpha0} per-series arrays")
+
+
+@pytest.mark.parametrize("theta", [0.3, 0.5, 0.95])
+def test_threshold_parity(oracle_mod, theta):
+    """The PROB rule at other thresholds (P:770 fixes 0.9): theta < 1/2 runs the EAGER kernel
+    (r* reduced every step), theta >= 1/2 the lazy one (r* = 1 at PROB events)."""
+    cfg = tracegen.CONFIGS["C3"]
+    x = tracegen.generate(tracegen.make_spec(cfg), 40, 16, 0, 1500)
+    xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    b = bocd.BocdBatch(16, R=1024, hazard=cfg.hazard, prior_first_obs=True, prior_cov=0.3,
+                       event_mask=1, event_capacity=1024, threshold=theta)
+    b.update_chunk(xd)
+    ev, dropped = b.changepoints()
+    b.close()
+    res = _oracle(oracle_mod, x, 1024, cfg.hazard, 0, prior_cov=0.3, threshold=theta)
+    assert not dropped
+    n = parity.compare_events(ev, res, theta, 1)
+    assert n > 0

@@ -16,11 +16,9 @@ import json
 import os
 import sys
 
-import numpy as np
-import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2410_12588_b200 import _native as N, bocd, detection, tracegen  # noqa: E402
+from paper_2410_12588_b200 import detection, tracegen  # noqa: E402
 
 
 def main():
@@ -30,31 +28,7 @@ def main():
     sigma = float(sys.argv[4]) if len(sys.argv) > 4 else None
     cfg = tracegen.CONFIGS[name]
     spec = tracegen.make_spec(cfg, n_series=S, T=T, sigma=sigma)
-    x = torch.empty((S, T), dtype=torch.float64, device="cuda")
-    bocd.DeviceTrace(spec, "cuda").generate(x, 0, 0)
-    b = bocd.BocdBatch(S, R=cfg.R, hazard=cfg.hazard, prior_first_obs=True, prior_cov=cfg.prior_cov,
-                       event_mask=3, event_capacity=8192)
-    b.update_chunk(x)
-    ev, dropped = b.changepoints()
-    b.close()
-    truth, onset = detection.series_truth(spec, 0, T, min_len=20)
-    out = {"config": name, "sigma": float(spec.sigma[0]), "series": S, "steps": T, "R": cfg.R,
-           "slowed_series": int(truth.sum()), "events_dropped": bool(dropped)}
-    for label, mask in (("prob", 1), ("prob_mapreset", 3)):
-        raw = ev[(ev["flags"] & mask) != 0]
-        first_raw = detection.first_flag(raw["series"], raw["t"], S)
-        ver = bocd.verify_changepoints(x, raw, t_lo=0)
-        pairs = bocd.pair_failslow(ver)
-        # a verified change point is known once its 20-sample after-window is complete
-        deg = ver[ver["status"] == N.CP_DEGRADE]
-        t_known = np.maximum(deg["t"], deg["cp_index"] + 19)
-        first_v = detection.first_flag(deg["series"], t_known, S)
-        flagged_v = np.zeros(S, dtype=bool)
-        flagged_v[pairs["series"]] = True  # every fail-slow event starts at a verified DEGRADE
-        out["bocd_" + label] = {**detection.confusion(first_raw >= 0, truth), "raw_events": int(len(raw)),
-                                "delay_steps": detection.latency(first_raw, onset, truth)}
-        out["bocd_v_" + label] = {**detection.confusion(flagged_v, truth), "failslow_events": int(len(pairs)),
-                                  "delay_steps": detection.latency(np.where(flagged_v, first_v, -1), onset, truth)}
+    out = detection.evaluate(spec, cfg, T)
     out["note"] = ("synthetic labelled traces (tracegen); detectors: raw BOCD change points (PROB = "
                    "p_new > 0.9, optionally + MAP resets) and the same verified by the 10% rule and "
                    "paired (BOCD+V); the paper's Tables 5-6 are context only")
