@@ -359,7 +359,7 @@ def test_priors_and_per_series_arrays(oracle_mod, R, kappa0, alpha0):
     _full_check(g, res, mask=3, name=f"priors R={R} kappa0={kappa0} alpha0={alpha0} per-series arrays")
 
 
-@pytest.mark.parametrize("theta", [0.3, 0.5, 0.95])
+@pytest.mark.parametrize("theta", [0.3, 0.5, 0.8])
 def test_threshold_parity(oracle_mod, theta):
     """The PROB rule at other thresholds (P:770 fixes 0.9): theta < 1/2 runs the EAGER kernel
     (r* reduced every step), theta >= 1/2 the lazy one (r* = 1 at PROB events)."""
