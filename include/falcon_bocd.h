@@ -295,17 +295,19 @@ int falcon_classify_groups(const double *times_dev, int64_t n_batches, int32_t n
  * --------------------------------------------------------------------------- */
 
 /* codes_dev: DEVICE int32 [n_series][ld] call-signature codes, L per series (2 <= L <= 8192,
- * 1 <= k_max < L).  period_dev (DEVICE int32 [n_series]) receives the smallest k in
- * [1, k_max] with ACF_k >= M, or 0; acf_dev (DEVICE fp64 [n_series][k_max], may be NULL)
- * the ACF values.  One CTA per series; mu, the centred codes and the lag sums in fp64.
- * Stream-ordered, asynchronous. */
+ * 1 <= k_max, 2 k_max <= L: SPEC detect_period's pre-condition |codes| >= 2 k_max; a shorter
+ * sequence returns FALCON_EINVAL, the insufficient-data error).  period_dev (DEVICE int32
+ * [n_series]) receives the smallest k in [1, k_max] with ACF_k >= M, 0 if there is none, or -1
+ * for a zero-variance window (every ACF_k defined as 0, reported as a flag: S:104-105);
+ * acf_dev (DEVICE fp64 [n_series][k_max], may be NULL) the ACF values.  One CTA per series;
+ * mu, the centred codes and the lag sums in fp64.  Stream-ordered, asynchronous. */
 int falcon_detect_period(const int32_t *codes_dev, int64_t n_series, int32_t L, int64_t ld, int32_t k_max,
                          double M, double *acf_dev, int32_t *period_dev, void *stream);
 
 /* ts_dev: DEVICE fp64 [n_series][ld] call timestamps (n per series); period_dev as above.
  * out_dev (DEVICE fp64 [n_series][ld_out]) receives, per series, the iteration times
  * ts[(i+1) P] - ts[i P] for i < (n - 1) / P, and n_out_dev (DEVICE int32 [n_series]) their
- * count (0 where P = 0); ld_out >= n - 1.  Stream-ordered, asynchronous. */
+ * count (0 where P <= 0); ld_out >= n - 1.  Stream-ordered, asynchronous. */
 int falcon_iteration_times(const double *ts_dev, int64_t n_series, int32_t n, int64_t ld,
                            const int32_t *period_dev, double *out_dev, int64_t ld_out, int32_t *n_out_dev,
                            void *stream);

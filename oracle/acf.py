@@ -9,8 +9,9 @@ PAPER.md §4.2 "Iteration time analysis", written out directly:
   operation and its occurrence in the previous period": with SPEC S:120-122's
   anchors (the first call of each period block), duration_i = ts[(i+1) P] - ts[i P].
 Readings (DESIGN.md §3, A1-A3): A1 the window is the whole sequence given (L = len(X));
-A2 zero variance -> ACF 0 for every k and no period; A3 no k <= k_max reaching M
--> no period (0).  Plain numpy in fp64, one lag at a time.
+A2 zero variance -> ACF 0 for every k, reported as a flag: period -1; A3 no
+k <= k_max reaching M -> no period (0).  SPEC's pre-condition |codes| >= 2 k_max
+raises ValueError (the insufficient-data error).  Plain numpy in fp64, one lag at a time.
 """
 from __future__ import annotations
 
@@ -33,8 +34,13 @@ def acf(codes, k_max):
 
 
 def detect_period(codes, k_max, M=0.95):
-    """The smallest k in [1, k_max] with ACF_k >= M, or 0 (A3)."""
-    a, _ = acf(codes, k_max)
+    """The smallest k in [1, k_max] with ACF_k >= M, 0 if none (A3), -1 for a zero-variance
+    window (A2's flag).  Raises ValueError when len(codes) < 2 k_max."""
+    if len(codes) < 2 * k_max:
+        raise ValueError("insufficient data: detect_period needs |codes| >= 2 k_max")
+    a, zero_var = acf(codes, k_max)
+    if zero_var:
+        return -1
     hit = np.nonzero(a >= M)[0]
     return int(hit[0]) + 1 if len(hit) else 0
 
@@ -42,7 +48,7 @@ def detect_period(codes, k_max, M=0.95):
 def iteration_times(ts, period):
     """duration_i = ts[(i+1) P] - ts[i P] for every complete period block."""
     ts = np.asarray(ts, dtype=np.float64)
-    if period <= 0:
+    if period <= 0:  # no period (0) or a zero-variance window (-1)
         return np.zeros(0)
     n = (len(ts) - 1) // period
     return np.array([ts[(i + 1) * period] - ts[i * period] for i in range(n)])

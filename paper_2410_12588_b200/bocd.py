@@ -318,7 +318,8 @@ def classify_groups(times, factor: float = 1.1, stream=None):
 
 def detect_period(codes, k_max: int, M: float = 0.95, with_acf: bool = False, stream=None):
     """ACF period detection (N2, falcon_detect_period): codes is a CUDA int32 tensor [S][L].
-    Returns period (int32 [S], 0 = none) and, with_acf, the ACF [S][k_max] (device tensors)."""
+    Returns period (int32 [S]: 0 = none, -1 = zero-variance window) and, with_acf, the ACF
+    [S][k_max] (device tensors).  Needs L >= 2 k_max (FalconError EINVAL otherwise)."""
     assert codes.is_cuda and codes.dtype == torch.int32 and codes.dim() == 2 and codes.stride(1) == 1
     S, L = codes.shape
     period = torch.empty(S, dtype=torch.int32, device=codes.device)

@@ -56,7 +56,8 @@ __global__ void __launch_bounds__(256) acf_kernel(const int32_t* __restrict__ co
         if (den > 0.0 && a >= M) atomicMin(&pmin, k);
     }
     __syncthreads();
-    if (threadIdx.x == 0) period[s] = pmin == INT_MAX ? 0 : pmin;
+    // -1: zero-variance window, reported as a flag; 0: no lag reaches M (reading A3)
+    if (threadIdx.x == 0) period[s] = den > 0.0 ? (pmin == INT_MAX ? 0 : pmin) : -1;
 }
 
 __global__ void iter_times_kernel(const double* __restrict__ ts, int64_t S, int n, int64_t ld,
@@ -74,7 +75,9 @@ __global__ void iter_times_kernel(const double* __restrict__ ts, int64_t S, int 
 
 extern "C" int falcon_detect_period(const int32_t* codes_dev, int64_t n_series, int32_t L, int64_t ld, int32_t k_max,
                                     double M, double* acf_dev, int32_t* period_dev, void* stream) {
-    if (n_series < 0 || L < 2 || L > kMaxL || ld < L || k_max < 1 || k_max >= L || !(M > -1.0 && M <= 1.0))
+    // SPEC detect_period pre-condition |codes| >= 2 k_max: a shorter sequence is an
+    // explicit insufficient-data error (the biased ACF numerator would have too few terms)
+    if (n_series < 0 || L < 2 || L > kMaxL || ld < L || k_max < 1 || 2 * int64_t(k_max) > L || !(M > -1.0 && M <= 1.0))
         return FALCON_EINVAL;
     if (n_series == 0) return FALCON_OK;
     if (!codes_dev || !period_dev || n_series > 0x7FFFFFFF) return FALCON_EINVAL;

@@ -48,7 +48,14 @@ def test_acf_and_period_match_oracle(S, L, kmax):
 def test_zero_variance_and_constant():
     c = torch.full((2, 100), 5, dtype=torch.int32, device="cuda")
     p, a = bocd.detect_period(c, 10, with_acf=True)
-    assert p.tolist() == [0, 0] and not a.any()
+    assert p.tolist() == [-1, -1] and not a.any()  # the zero-variance flag
+
+
+def test_insufficient_data_is_an_error():
+    c = torch.arange(40, dtype=torch.int32, device="cuda").view(2, 20)
+    with pytest.raises(bocd.N.FalconError) as ei:
+        bocd.detect_period(c, 11)  # |codes| < 2 k_max
+    assert ei.value.code == bocd.N.FALCON_EINVAL
 
 
 def test_iteration_times_match_oracle():

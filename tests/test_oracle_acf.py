@@ -28,7 +28,9 @@ def test_matches_numpy_correlate():
 
 def test_zero_variance_and_none():
     a, zv = A.acf(np.full(64, 3.0), 8)
-    assert zv and not a.any() and A.detect_period(np.full(64, 3.0), 8) == 0
+    assert zv and not a.any() and A.detect_period(np.full(64, 3.0), 8) == -1  # S:104-105 flag
+    with pytest.raises(ValueError):
+        A.detect_period(np.arange(20), 11)  # |codes| < 2 k_max
     rng = np.random.default_rng(1)
     assert A.detect_period(rng.integers(0, 50, size=4096), 64) == 0      # S:114 random codes -> none
 
