@@ -224,6 +224,21 @@ __device__ __forceinline__ double tree_sum(const double* p) {
     }
 }
 
+// The sum of the W per-warp partials, known to every lane: for W >= 16 each lane loads one
+// partial (lane mod W) and an xor butterfly adds them (fixed order: deterministic; one shared
+// load instead of W/2 16-byte loads and W - 1 serial-ish adds); smaller W: tree_sum.
+template <int W>
+__device__ __forceinline__ double partials_sum(const double* p, int lane) {
+    if constexpr (W >= 16) {
+        double v = p[lane & (W - 1)];
+#pragma unroll
+        for (int o = W / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        return v;
+    } else {
+        return tree_sum<W>(p);
+    }
+}
+
 // Argmax key of a non-negative double q at run length r: the bit pattern of q is
 // order-preserving; its low 12 mantissa bits are replaced by (4095 - r) so the max
 // key is the max q and, among (near-)ties (< 2^-40 relative), the smallest r.
@@ -464,6 +479,15 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
         const int64_t s0 = int64_t(blockIdx.x) * SPB + g;
         if (i == 0 && P.t0 > 0 && blockIdx.x < nunits && s0 < P.S) issue_state(s0);
     }
+    // PREF streaming calls whose x rows are not TMA-able (T = 1: one 8-byte value per series):
+    // thread i holds x[s][i] of its unit in a register, loaded during the previous unit, so the
+    // global-load latency is off each unit's critical path
+    const bool xreg = PREF && P.T <= NT && !tile_tma_ok<TILE>(P, 0);
+    double xv = 0.0;
+    if (xreg) {
+        const int64_t s0 = int64_t(blockIdx.x) * SPB + g;
+        if (i < P.T && s0 < P.S) xv = P.x[s0 * P.ld + i];
+    }
 
     for (int64_t u = blockIdx.x; u < nunits; u += PERSIST ? int64_t(gridDim.x) : nunits) {
         const int64_t s = u * SPB + g;
@@ -580,6 +604,11 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
             if (tile_tma_ok<TILE>(P, k)) {
                 mbar_wait(&gs.mbar[buf], (xphase >> buf) & 1u);
                 xphase ^= 1u << buf;
+            } else if (xreg) {  // (one tile, n = T <= NT)
+                if (i < n) gs.xbuf[buf][i] = xv;
+                group_sync<NT>(g);
+                const int64_t sn = s + int64_t(gridDim.x) * SPB;  // the next unit's x, in flight now
+                if (i < n && sn < P.S) xv = P.x[sn * P.ld + i];
             } else {
                 for (int q = i; q < n; q += NT) gs.xbuf[buf][q] = xrow[base + q];
                 group_sync<NT>(g);
@@ -793,7 +822,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                         if (EAGER) gs.red1[par][w] = key;
                     }
                     group_sync<NT>(g);
-                    sum = tree_sum<W>(gs.red2[par]);
+                    sum = partials_sum<W>(gs.red2[par], lane);
                     if constexpr (EAGER) {
 #pragma unroll
                         for (int ww = 0; ww < W; ++ww) {
