@@ -108,7 +108,7 @@ struct KParams {
     int64_t S;
     double H, omH, hr, theta, alpha0, prior_cov;  // omH = 1-H, hr = H/(1-H)
     double ln_omH;                                // log(1-H)
-    double c_bucket, alpha_bucket;                // c_{R-1}/ln2 and alpha_{R-1} (MERGE bucket, FULL)
+    double c_bucket;                              // c_{R-1}/ln2 (MERGE bucket, FULL)
     double al2_bucket;                            // 2 alpha_{R-1}
     int a2p1;                                     // 2 alpha0 + 1 (FULL kernels: 2 alpha0 is an integer)
     int mode;                                     // 0 MERGE, 1 DROP
@@ -665,6 +665,11 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 const int mb = FULL ? P.a2p1 + ib : 0;  // 2 alpha0 + 1 + (table index of slot 0)
                 double sum = 0.0;
                 unsigned long long key = 0ull;
+                // EAGER, ROT: this step's argmax codes and the two ineligible growth candidates
+                const unsigned kcb = unsigned(i) | 0xFFFFF000u;
+                const unsigned kc0 = kcb | ((ROT && ib >= R) ? unsigned(R) : 0u);
+                const bool elig0 = !(i == iB || (merge && i == iB + 1));
+                const bool elig1 = !(merge && iB == NT - 1 && i == 0);
 #pragma unroll
                 for (int j0 = 0; j0 < J; j0 += kG) {
                     constexpr int G = (J < kG) ? J : kG;
@@ -792,10 +797,26 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                         if (FULL || p < R) {
                             sum += E;
                             if constexpr (EAGER) {
-                                int r = idx[kk];
-                                r -= (r >= R) ? R : 0;
-                                const unsigned long long kq = argmax_key(E, r);
-                                key = (r <= r_elig && kq > key) ? kq : key;
+                                if constexpr (ROT) {
+                                    // key = E's bits with the low 12 replaced by the cell's code
+                                    // i + NT j (+ R for the wrapped slot 0): r = R + iB - 1 - code for
+                                    // every cell, so the larger code is the smaller run length (ties ->
+                                    // smaller r).  One LOP3: (lo & b & c) | (b ^ c), b = code bits
+                                    // of the thread (| 0xFFFFF000), c = NT j | 0xFFFFF000 (disjoint low bits)
+                                    const unsigned bc = j == 0 ? kc0 : kcb;
+                                    const unsigned cc = 0xFFFFF000u | unsigned(NT * j);
+                                    const unsigned lo = (unsigned(__double2loint(E)) & bc & cc) | (bc ^ cc);
+                                    unsigned long long kq =
+                                        (static_cast<unsigned long long>(unsigned(__double2hiint(E))) << 32) | lo;
+                                    if (j == 0 && !elig0) kq = 0ull;  // kB (r = R-1) / MERGE kA (r = R-2)
+                                    if (J > 1 && j == 1 && !elig1) kq = 0ull;
+                                    key = kq > key ? kq : key;
+                                } else {
+                                    int r = idx[kk];
+                                    r -= (r >= R) ? R : 0;
+                                    const unsigned long long kq = argmax_key(E, r);
+                                    key = (r <= r_elig && kq > key) ? kq : key;
+                                }
                             }
                             // the tail's cells, published by their owners
                             if constexpr (ROT) {
@@ -892,7 +913,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     double qex = 0.0;
                     if constexpr (EAGER) {
                         if (key != 0ull) {
-                            r_ex = key_r(key);
+                            r_ex = ROT ? R + iB - 1 - int(key & 0xFFFull) : key_r(key);
                             qex = key_val(key);
                         }
                     }

@@ -543,7 +543,6 @@ static int launch_update(falcon_bocd_t h, const double* x_dev, int64_t ld, int64
         P.omH = 1.0 - c.hazard;
         P.ln_omH = log1p(-c.hazard);
         P.c_bucket = h->c_bucket;
-        P.alpha_bucket = c.alpha0 + 0.5 * (c.R - 1);
         P.al2_bucket = 2.0 * c.alpha0 + double(c.R - 1);
         P.a2p1 = int(2.0 * c.alpha0) + 1;  // used by the FULL kernels only (2 alpha0 integral there)
         P.hr = (double)((long double)c.hazard / (1.0L - (long double)c.hazard));

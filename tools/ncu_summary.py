@@ -34,6 +34,17 @@ KEYS = ["gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_second", "launch__
 
 
 def ncu_csv(rep, *args):
+    """ncu -i rep ... --csv; or, for a capture exported on the GPU box (tools/gpu/r02_ncu.sh),
+    rep = the path stem and the CSV files <stem>.raw.csv / <stem>.src.csv(.gz)."""
+    if not rep.endswith(".ncu-rep"):
+        import gzip
+        page = "raw" if "raw" in args else "src"
+        path = f"{rep}.{page}.csv"
+        if not os.path.exists(path):
+            path += ".gz"
+        opener = gzip.open if path.endswith(".gz") else open
+        with opener(path, "rt") as f:
+            return list(csv.reader(f))
     out = subprocess.run(["ncu", "-i", rep, *args, "--csv"], capture_output=True, text=True, check=True).stdout
     return list(csv.reader(io.StringIO(out)))
 
