@@ -665,8 +665,11 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 const int mb = FULL ? P.a2p1 + ib : 0;  // 2 alpha0 + 1 + (table index of slot 0)
                 double sum = 0.0;
                 unsigned long long key = 0ull;
-                // EAGER, ROT: this step's argmax codes and the two ineligible growth candidates
-                const unsigned kcb = unsigned(i) | 0xFFFFF000u;
+                // EAGER, ROT: this step's argmax codes (below R + NT: 12 bits up to R = 2048, 13 at
+                // R = 4096) and the two ineligible growth candidates
+                constexpr unsigned kKeyBits = (ROT && NT * J + NT > 4096) ? 13u : 12u;
+                constexpr unsigned kKeyHi = ~((1u << kKeyBits) - 1u);
+                const unsigned kcb = unsigned(i) | kKeyHi;
                 const unsigned kc0 = kcb | ((ROT && ib >= R) ? unsigned(R) : 0u);
                 const bool elig0 = !(i == iB || (merge && i == iB + 1));
                 const bool elig1 = !(merge && iB == NT - 1 && i == 0);
@@ -798,13 +801,13 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                             sum += E;
                             if constexpr (EAGER) {
                                 if constexpr (ROT) {
-                                    // key = E's bits with the low 12 replaced by the cell's code
+                                    // key = E's bits with the low 12 (13) replaced by the cell's code
                                     // i + NT j (+ R for the wrapped slot 0): r = R + iB - 1 - code for
                                     // every cell, so the larger code is the smaller run length (ties ->
                                     // smaller r).  One LOP3: (lo & b & c) | (b ^ c), b = code bits
-                                    // of the thread (| 0xFFFFF000), c = NT j | 0xFFFFF000 (disjoint low bits)
+                                    // of the thread (| kKeyHi), c = NT j | kKeyHi (disjoint low bits)
                                     const unsigned bc = j == 0 ? kc0 : kcb;
-                                    const unsigned cc = 0xFFFFF000u | unsigned(NT * j);
+                                    const unsigned cc = kKeyHi | unsigned(NT * j);
                                     const unsigned lo = (unsigned(__double2loint(E)) & bc & cc) | (bc ^ cc);
                                     unsigned long long kq =
                                         (static_cast<unsigned long long>(unsigned(__double2hiint(E))) << 32) | lo;
@@ -913,8 +916,14 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     double qex = 0.0;
                     if constexpr (EAGER) {
                         if (key != 0ull) {
-                            r_ex = ROT ? R + iB - 1 - int(key & 0xFFFull) : key_r(key);
-                            qex = key_val(key);
+                            if constexpr (ROT) {
+                                constexpr unsigned long long kLow = (NT * J + NT > 4096) ? 0x1FFFull : 0xFFFull;
+                                r_ex = R + iB - 1 - int(key & kLow);
+                                qex = __longlong_as_double(static_cast<long long>(key & ~kLow));
+                            } else {
+                                r_ex = key_r(key);
+                                qex = key_val(key);
+                            }
                         }
                     }
                     if (EAGER || (fl & P.ev_mask)) {
