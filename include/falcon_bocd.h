@@ -167,8 +167,11 @@ int falcon_bocd_read_posterior(falcon_bocd_t h, int64_t s0, int64_t count, doubl
 
 /* Kernel schedule of later update calls (test hook; results are bit-identical either way):
  * 0 = automatic (default: calls of <= 64 steps with more series units than co-resident CTAs
- * run the persistent kernels with TMA-prefetched state, all others one unit per CTA);
- * 1 = persistent kernels for every call of <= 64 steps; 2 = one unit per CTA always.
+ * run the persistent kernels with TMA-prefetched state, all others one unit per CTA, where
+ * a batch that fits one wave of CTAs but would load some SMs with more series than
+ * ceil(S / #SM) runs as one balanced CTA per SM, R = 512 and 1024);
+ * 1 = persistent kernels for every call of <= 64 steps; 2 = one unit per CTA always (balanced
+ * as in 0); 3 = one unit per CTA, never balanced.
  * Returns FALCON_EINVAL for another value. */
 int falcon_bocd_set_schedule(falcon_bocd_t h, int32_t schedule);
 

@@ -217,10 +217,11 @@ class BocdBatch:
         return tuple(out)
 
     def set_schedule(self, schedule: str):
-        """Kernel schedule of later calls: 'auto', 'persistent' (every call of <= 64 steps) or
-        'one_unit' (falcon_bocd_set_schedule; a test hook: results are bit-identical)."""
-        N.check(N.lib().falcon_bocd_set_schedule(self._h, {"auto": 0, "persistent": 1, "one_unit": 2}[schedule]),
-                self._h)
+        """Kernel schedule of later calls: 'auto', 'persistent' (every call of <= 64 steps),
+        'one_unit' or 'one_unit_packed' (never the balanced one-CTA-per-SM wave)
+        (falcon_bocd_set_schedule; a test hook: results are bit-identical)."""
+        code = {"auto": 0, "persistent": 1, "one_unit": 2, "one_unit_packed": 3}[schedule]
+        N.check(N.lib().falcon_bocd_set_schedule(self._h, code), self._h)
 
     @property
     def steps(self) -> int:

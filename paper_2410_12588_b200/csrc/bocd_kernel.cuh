@@ -448,7 +448,11 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     // PREF: the prefetched next-unit state [mu R][beta R][a R][SeriesScalars], position order
     double* const pf = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(&gs) + sizeof(GS));
     SeriesScalars* const pf_sc = reinterpret_cast<SeriesScalars*>(pf + 3 * size_t(R));
-    const int64_t nunits = (P.S + SPB - 1) / SPB;
+    // balanced (the one-CTA-per-SM twins, MINB = 1 with several groups: one wave, grid = #SM):
+    // every CTA takes floor or ceil of S / grid series, so no SM carries more than
+    // ceil(S / #SM); the host launches them only for S <= #SM * SPB (32-bit arithmetic)
+    constexpr bool bal = !PERSIST && MINB == 1 && SPB > 1;
+    const int64_t nunits = bal ? int64_t(gridDim.x) : (P.S + SPB - 1) / SPB;
     if (i == 0) {
         mbar_init(&gs.mbar[0], 1);
         mbar_init(&gs.mbar[1], 1);
@@ -490,8 +494,8 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     }
 
     for (int64_t u = blockIdx.x; u < nunits; u += PERSIST ? int64_t(gridDim.x) : nunits) {
-        const int64_t s = u * SPB + g;
-        if (s >= P.S) break;  // group-uniform; later units only have larger s
+        const int64_t s = bal ? int64_t(unsigned(u) * unsigned(P.S) / gridDim.x) + g : u * SPB + g;
+        if (s >= (bal ? int64_t(unsigned(u + 1) * unsigned(P.S) / gridDim.x) : P.S)) break;  // group-uniform
         const double* xrow = P.x + s * P.ld;
         // Prefetch tile 0 (TMA) as early as possible.
         if (i == 0 && ntiles > 0 && tile_tma_ok<TILE>(P, 0)) issue_tile_tma<NT, TILE>(gs, xrow, 0, P.T);

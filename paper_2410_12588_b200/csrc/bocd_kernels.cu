@@ -33,6 +33,22 @@ static void make_variant(int mode, Variant* out) {
     else
         make_variant_mode<NT, J, FULL, TAB2, SPB, MINB, 1>(out);
 }
+// + the one-CTA-per-SM twins (SPB * MINB groups, MINB = 1) of the one-unit kernels, for a
+// batch that fits one wave unevenly (C2: 1,024 series of R = 512 on 148 SMs are 8 on most SMs
+// in CTAs of 4, at most 7 in balanced CTAs of 8)
+template <int NT, int J, bool FULL, bool TAB2, int SPB, int MINB>
+static void make_variant_w(int mode, Variant* out) {
+    make_variant<NT, J, FULL, TAB2, SPB, MINB>(mode, out);
+    constexpr int W = SPB * MINB;
+    if (mode == 0) {
+        out->fn_w = reinterpret_cast<const void*>(&bocd_update_kernel<NT, J, FULL, TAB2, false, W, 1, false, 0>);
+        out->fn_eager_w = reinterpret_cast<const void*>(&bocd_update_kernel<NT, J, FULL, TAB2, true, W, 1, false, 0>);
+    } else {
+        out->fn_w = reinterpret_cast<const void*>(&bocd_update_kernel<NT, J, FULL, TAB2, false, W, 1, false, 1>);
+        out->fn_eager_w = reinterpret_cast<const void*>(&bocd_update_kernel<NT, J, FULL, TAB2, true, W, 1, false, 1>);
+    }
+    out->spb_w = W;
+}
 
 // Variant choice: FULL kernels (R = NT*J, compile-time ring arithmetic) for the
 // power-of-two R of the BASELINE configs; generic kernels (runtime R, masked
@@ -48,8 +64,8 @@ int select_variant(int R, int mode, double alpha0, Variant* out) {
     const bool full_ok = a2 == std::floor(a2) && a2 >= 1.0 && a2 <= double(1 << 20);
     switch (full_ok ? R : -1) {
         case 256: make_variant<32, 8, true, true, 8, 2>(mode, out); return 0;
-        case 512: make_variant<64, 8, true, true, 4, 2>(mode, out); return 0;
-        case 1024: make_variant<128, 8, true, true, 2, 2>(mode, out); return 0;
+        case 512: make_variant_w<64, 8, true, true, 4, 2>(mode, out); return 0;
+        case 1024: make_variant_w<128, 8, true, true, 2, 2>(mode, out); return 0;
         case 2048: make_variant<256, 8, true, false, 1, 2>(mode, out); return 0;
         case 4096: make_variant<512, 8, true, false, 1, 1>(mode, out); return 0;
         default: break;
@@ -80,6 +96,12 @@ size_t variant_smem(const Variant& v, int R, bool persistent) {
                        (pref ? ((3 * size_t(R) * sizeof(double) + sizeof(SeriesScalars) + 15) & ~size_t(15)) : 0);
     return bocd_fm_bytes(cell_ec(v.full, v.nt * v.j, pref), cell_logbits(v.full, v.nt * v.j)) + table_bytes(rows, v.full) +
            size_t(v.spb) * grp;
+}
+
+size_t variant_smem_wide(const Variant& v, int R) {
+    Variant w = v;
+    w.spb = v.spb_w;
+    return variant_smem(w, R, false);
 }
 
 // Test hook: elementwise fast_log2 / fast_exp2 (which 0 / 1) and the cell loop's cell_log2 /

@@ -20,11 +20,17 @@ struct Variant {
     size_t group_smem = 0;     // bytes of GroupSmem (one-unit kernels)
     size_t group_smem_p = 0;   // of the persistent kernels' GroupSmem (64-step tiles); + PREF buffer
     bool pref = false;         // the persistent kernels prefetch the next unit's state (TMA)
+    // one-CTA-per-SM twins of the one-unit kernels (spb_w = spb * MINB series groups per CTA,
+    // launched as one balanced wave when the batch fits one wave unevenly); null if none
+    const void* fn_w = nullptr;
+    const void* fn_eager_w = nullptr;
+    int spb_w = 0;
 };
 
 int select_variant(int R, int mode, double alpha0, Variant* out);  // mode: FALCON_TRUNC_MERGE / _DROP
 // dynamic shared memory of one CTA of variant v at ring size R (persistent or one-unit kernels)
 size_t variant_smem(const Variant& v, int R, bool persistent);
+size_t variant_smem_wide(const Variant& v, int R);  // of the fn_w / fn_eager_w kernels
 
 struct FastMathTables;
 struct CellTables;

@@ -30,6 +30,9 @@ struct falcon_bocd_s {
     size_t smem = 0;    // dynamic shared memory of the one-unit-per-CTA kernels
     size_t smem_p = 0;  // of the persistent kernels (+ the state prefetch buffers)
     int64_t grid_cap = 0;  // co-resident CTAs (persistent grid)
+    size_t smem_w = 0;     // of the one-CTA-per-SM twins (var.fn_w), if any
+    int n_sm = 0;          // multiprocessors of the device
+    int per_sm = 0;        // co-resident one-unit CTAs per SM (regular kernels)
     int64_t t = 0;  // observations absorbed
     double c_bucket = 0.0;  // c_{R-1} / ln2 (the MERGE bucket's predictive constant)
     double2* d_ca = nullptr;
@@ -62,7 +65,7 @@ struct falcon_bocd_s {
     double* d_ologz = nullptr;
     size_t out_cap = 0;
     bool poisoned = false;
-    int schedule = 0;  // falcon_bocd_set_schedule: 0 auto, 1 persistent, 2 one unit per CTA
+    int schedule = 0;  // falcon_bocd_set_schedule: 0 auto, 1 persistent, 2 one unit per CTA, 3 = 2 unbalanced
     std::string err;
 };
 
@@ -433,9 +436,28 @@ int falcon_bocd_create(const falcon_bocd_config* cfg, falcon_bocd_t* out) {
         h->err = "cudaMemcpyToSymbol(c_fm) failed";
         return bail(FALCON_ECUDA);
     }
+    h->n_sm = prop.multiProcessorCount;
     for (const void* fn : {h->var.fn, h->var.fn_eager}) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(h->smem));
         if (e != cudaSuccess) return bail(cuda_fail(h, e, "cudaFuncSetAttribute"));
+        int per_sm = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, h->var.nt * h->var.spb, h->smem);
+        if (e != cudaSuccess || per_sm < 1) return bail(cuda_fail(h, e != cudaSuccess ? e : cudaErrorInvalidConfiguration,
+                                                               "occupancy query"));
+        h->per_sm = h->per_sm ? std::min(h->per_sm, per_sm) : per_sm;
+    }
+    if (h->var.fn_w) {
+        // the balanced wave assumes exactly one CTA per SM (registers: NT * spb_w threads x up
+        // to 128 fill the register file); otherwise the twins are not used
+        h->smem_w = fbocd::variant_smem_wide(h->var, c.R);
+        for (const void* fn : {h->var.fn_w, h->var.fn_eager_w}) {
+            cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(h->smem_w));
+            if (e != cudaSuccess) return bail(cuda_fail(h, e, "cudaFuncSetAttribute"));
+            int per_sm = 0;
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, h->var.nt * h->var.spb_w, h->smem_w);
+            if (e != cudaSuccess) return bail(cuda_fail(h, e, "occupancy query"));
+            if (per_sm != 1) h->var.fn_w = h->var.fn_eager_w = nullptr;
+        }
     }
     for (const void* fn : {h->var.fn_p, h->var.fn_eager_p}) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(h->smem_p));
@@ -577,18 +599,26 @@ static int launch_update(falcon_bocd_t h, const double* x_dev, int64_t ld, int64
         // streaming calls (few steps): persistent grid, tables set up once per CTA and the next
         // unit's state prefetched; long calls: one unit per CTA.  Identical arithmetic.
         const bool persist = h->schedule == 1 ? n <= kPersistMaxSteps
-                           : h->schedule == 2 ? false
+                           : h->schedule >= 2 ? false
                                               : (n <= kPersistMaxSteps && units > h->grid_cap);
-        const int64_t grid = persist ? h->grid_cap : units;
+        // one wave that would load SMs unevenly (at most spb * ceil(units / #SM) series per SM
+        // in CTAs of spb): one balanced CTA per SM instead, ceil(S / #SM) series at most
+        const int64_t S = c.n_series, nsm = h->n_sm;
+        const bool wide = !persist && h->var.fn_w && h->schedule != 3 && units <= nsm * h->per_sm &&
+                          S <= nsm * h->var.spb_w &&
+                          (S + nsm - 1) / nsm < int64_t(h->var.spb) * ((units + nsm - 1) / nsm);
+        const int64_t grid = persist ? h->grid_cap : wide ? nsm : units;
         void* args[] = {&P};
         // r* every step only when it is an output (per-step MAP, MAPRESET events); otherwise
         // r* = 1 at every PROB event (theta >= 1/2).
         // theta < 1/2 also needs it at PROB events (bocd_kernel.cuh: r* = 1 only for theta >= 1/2)
         const bool eager = (c.event_mask & FALCON_EV_MAPRESET) || omap || c.threshold < 0.5;
-        const void* fn = persist ? (eager ? h->var.fn_eager_p : h->var.fn_p) : (eager ? h->var.fn_eager : h->var.fn);
+        const void* fn = persist ? (eager ? h->var.fn_eager_p : h->var.fn_p)
+                       : wide    ? (eager ? h->var.fn_eager_w : h->var.fn_w)
+                                 : (eager ? h->var.fn_eager : h->var.fn);
         cudaError_t e = cudaLaunchKernel(fn, dim3(unsigned(grid)),
-                                         dim3(unsigned(h->var.nt * h->var.spb)), args,
-                                         persist ? h->smem_p : h->smem, st);
+                                         dim3(unsigned(h->var.nt * (wide ? h->var.spb_w : h->var.spb))), args,
+                                         persist ? h->smem_p : wide ? h->smem_w : h->smem, st);
         if (e != cudaSuccess) return cuda_fail(h, e, "bocd_update_kernel launch");
         h->t += n;
         done += n;
@@ -890,7 +920,7 @@ int falcon_bocd_read_posterior(falcon_bocd_t h, int64_t s0, int64_t count, doubl
 }
 
 int falcon_bocd_set_schedule(falcon_bocd_t h, int32_t schedule) {
-    if (!h || schedule < 0 || schedule > 2) return FALCON_EINVAL;
+    if (!h || schedule < 0 || schedule > 3) return FALCON_EINVAL;
     h->schedule = schedule;
     return FALCON_OK;
 }

@@ -340,6 +340,39 @@ def test_persistent_kernels_bit_exact(oracle_mod, R, mode):
     parity.record(f"persistent R={R} mode={mode} [0:3,:{T}]", st)
 
 
+@pytest.mark.parametrize("R,S", [(512, 1024), (512, 700), (1024, 400)])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_balanced_wave_bit_exact(oracle_mod, R, S, mode):
+    """A batch that fits one wave of CTAs unevenly (C2: 1,024 series of R = 512 in CTAs of 4,
+    two per SM) runs as one balanced CTA per SM (capi.cu launch_update; the MINB = 1 twins of bocd_kernel.cuh):
+    bit-identical to the packed one-unit launch ('one_unit_packed'), EAGER and lazy, and the
+    first, a middle and the last series match the oracle."""
+    cfg = tracegen.CONFIGS["C2"] if R == 512 else tracegen.CONFIGS["C3"]
+    T = 300
+    x = tracegen.generate(tracegen.make_spec(cfg, n_series=S), 0, S, 0, T)
+    a = _run_gpu(x, R, cfg.hazard, mode, prior_cov=0.3, ev_mask=3, cap=512, schedule="auto")
+    b = _run_gpu(x, R, cfg.hazard, mode, prior_cov=0.3, ev_mask=3, cap=512, schedule="one_unit_packed")
+    for k in ("map", "pnew", "logz", "logR", "mu", "beta"):
+        assert np.array_equal(a[k], b[k], equal_nan=True), k
+    assert np.array_equal(a["events"], b["events"])
+    xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    logs = []
+    for sched in ("auto", "one_unit_packed"):  # lazy kernels (PROB only)
+        h = bocd.BocdBatch(S, R=R, hazard=cfg.hazard, prior_first_obs=True, prior_cov=0.3, trunc_mode=mode,
+                           event_mask=1, event_capacity=512)
+        h.set_schedule(sched)
+        h.update_chunk(xd)
+        logs.append((h.read_posterior()[0].cpu().numpy(), h.changepoints()[0]))
+        h.close()
+    assert np.array_equal(logs[0][0], logs[1][0], equal_nan=True)
+    assert np.array_equal(logs[0][1], logs[1][1])
+    rows = [0, S // 2, S - 1]
+    res = _oracle(oracle_mod, x[rows], R, cfg.hazard, mode, prior_cov=0.3)
+    st = parity.compare_steps(a["map"][rows], a["pnew"][rows], a["logz"][rows], res, 0.9)
+    st["max_dlogR"] = parity.compare_logR(a["logR"][rows], res.logR_final)
+    parity.record(f"balanced R={R} S={S} mode={mode}", st)
+
+
 @pytest.mark.parametrize("R", [1024, 4096])
 @pytest.mark.parametrize("kappa0,alpha0", [(0.5, 1.5), (2.0, 0.7), (1.0, 3.0)])
 def test_priors_and_per_series_arrays(oracle_mod, R, kappa0, alpha0):
