@@ -9,4 +9,3 @@ for c in C2 C4 C5; do timeout 900 python bench.py --config $c --steps 5 --warmup
 timeout 900 python bench.py --eager --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_C3_eager.json 2> $O/bench_C3_eager.err
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_reference.json 2> $O/bench_reference.err
 ls -la $O
-rm -f gpurun_out/ab/ab_C3.txt; VARIANTS="psum eag2" BENCH_ARGS=--eager bash tools/gpu/ab_c3.sh > $O/ab_eager.txt 2>&1
