@@ -34,7 +34,7 @@ namespace fbocd {
 // reaches 1024-2048 and the log's error, carried along the MERGE bucket's chain of merged
 // masses, would approach the parity budget (measured 6.2e-10 at R = 2048 with LB = 8).
 __host__ __device__ constexpr int cell_logbits(bool full, int r_full) { return (full && r_full <= 1024) ? 8 : 10; }
-constexpr int kCellEB = 8;  // exp2 table bits (degree-4 fit; 9 bits with degree 3 measured slower)
+constexpr int kCellEB = 8;  // exp2 table bits (degree-4 / degree-3 fits; 9 bits measured slower)
 constexpr int kCellExpTab = 1 << kCellEB;
 constexpr double kCellExpScale = double(kCellExpTab);          // the rounding grid 2^-EB
 constexpr unsigned kCellExpLo = 0x80000000u - 1021u * kCellExpTab;  // 2^-1021: floor / dead
@@ -72,8 +72,8 @@ inline void fill_cell_tables(CellTables* t) {
 // Polynomial coefficients (constant bank; uploaded with the fast-math constants): P0..P2 of
 // the log for LB = 8, 9, 10 at 3 (LB - 8), Q0..Q2 of the exp at 9.
 // 12..20: the log coefficients halved (exact), for the half-log lg(b)/2 of the FULL kernels.
-static __constant__ double c_cell[21];
-static const double kCellConstants[21] = {
+static __constant__ double c_cell[23];
+static const double kCellConstants[23] = {
     1.4426950408884385, -0.7213475204440444, 0.4808994476545776,   // LB = 8
     1.4426950408889305, -0.7213475204444544, 0.4808986221353932,   // LB = 9
     1.4426950408889614, -0.72134752044448, 0.4808984157560584,     // LB = 10
@@ -81,7 +81,10 @@ static const double kCellConstants[21] = {
     0.6931471805599428, 0.24022650695910044, 0.05550411375117056,
     0.5 * 1.4426950408884385, 0.5 * -0.7213475204440444, 0.5 * 0.4808994476545776,
     0.5 * 1.4426950408889305, 0.5 * -0.7213475204444544, 0.5 * 0.4808986221353932,
-    0.5 * 1.4426950408889614, 0.5 * -0.72134752044448, 0.5 * 0.4808984157560584};
+    0.5 * 1.4426950408889614, 0.5 * -0.72134752044448, 0.5 * 0.4808984157560584,
+    // 21, 22: exp Q0, Q1 of the degree-3 fit (+ kCellExpQ2c immediate; max error of
+    // 1 + r Q(r) vs 2^r 2.4e-14 relative, |r| <= 2^-9), for the cells that feed no chain
+    0.6931471805600506, 0.24022653734438304};
 // leading coefficients rounded to 20 mantissa bits (DFMA immediates; the rounding is weighted
 // by r^4 <= 2^-36, i.e. below 1e-18)
 template <int LB>
@@ -89,6 +92,7 @@ constexpr double kCellLogP3 = LB == 8 ? -0.3606746196746826 : -0.360673904418945
 template <int LB>
 constexpr double kCellLogP3h = 0.5 * kCellLogP3<LB>;
 constexpr double kCellExpQ3 = 0.009618133306503296;  // 0.009618129695226546 rounded
+constexpr double kCellExpQ2c = 0.05550408363342285;  // 0.055504081729180456 rounded (degree 3)
 
 constexpr unsigned kCellExpBase = 0x1A00u;
 template <int EC>
