@@ -799,7 +799,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     for (int kk = 0; kk < G; ++kk) {
                         const int j = j0 + kk;
                         const int p = i + NT * j;
-                        const double qq = pe[kk] * re[kk];
+                        const double qq = ROT ? 0.0 : pe[kk] * re[kk];
                         // 2^e, e = floor(n/256) for n = ki - 2^31, floored at 2^-1021 and clamped at
                         // +1000; hi word = kc * 2^12 + hi(T'_j) (cellmath.cuh)
                         // only the lower clamp (the floor): every cell's joint is below the step's
@@ -810,10 +810,20 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                         const unsigned kc = max(ki[kk], kCellExpLo);
                         const double Ts = __hiloint2double(int(kc * (1048576u >> kCellEB)) + __double2hiint(Tv[kk]),
                                                            __double2loint(Tv[kk]));
-                        double E = fma(Ts, qq, Ts);
-                        if (ROT && j == 0) E *= wq;  // slot 0's pending weight (new CP / bucket mass)
+                        double E;
+                        if constexpr (ROT) {
+                            // q' = Tw u with u = 2^re = 1 + re Q(re) and Tw = 2^(n/256) (x slot 0's
+                            // pending weight: new CP / bucket mass); the sum takes Tw u fused, and
+                            // q' itself is formed only where it is read (EAGER keys, published cells)
+                            const double u = fma(pe[kk], re[kk], 1.0);
+                            const double Tw = j == 0 ? Ts * wq : Ts;
+                            sum = fma(Tw, u, sum);
+                            E = (EAGER || j == 0 || (J > 1 && j == 1) || j == J - 1) ? Tw * u : 0.0;
+                        } else {
+                            E = fma(Ts, qq, Ts);
+                            if (FULL || p < R) sum += E;
+                        }
                         if (FULL || p < R) {
-                            sum += E;
                             if constexpr (EAGER) {
                                 if constexpr (ROT) {
                                     // key = E's bits with the low 12 (13) replaced by the cell's code
