@@ -54,8 +54,8 @@ UNIT = "series*steps/s"
 #   folded into its rounding constant), joint + evidence sum 2  =  26.  Fixed across kernel
 #   formulations (comparable between rounds).  The kernel evaluates the same recursion in
 #   the log-joint form (bocd_kernel.cuh: the predictive ratio telescopes into the NIG marginal
-#   likelihood) with 21 FP64-pipe instructions per cell: "frac_executed" reports the fraction
-#   on that basis.  Per-step work (group reduction, scalar tail, the tile's prior references)
+#   likelihood) with 21 FP64-pipe instructions per cell (19.5 in the lazy FULL kernels: the
+#   degree-3 exp2 and the fused sum): "frac_executed" reports the fraction on the 21 basis.  Per-step work (group reduction, scalar tail, the tile's prior references)
 #   is counted in neither.
 FP64_INSTR_PER_CELL = 26
 FP64_INSTR_PER_CELL_EXECUTED = 21

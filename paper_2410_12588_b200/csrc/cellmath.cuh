@@ -12,7 +12,10 @@
 //              1.0e-15 (LB = 8), 9.9e-19 (LB = 10).  7 FP64 ops.
 //   cell_exp2: d = (256 k + j)/256 + r exactly (|r| <= 2^-9), 2^d = 2^k T_j (1 + r Q(r)),
 //              T_j = 2^(j/256) from a 256-entry table, Q the degree-3 Chebyshev interpolant
-//              of (2^r - 1)/r (max |error| of r Q(r) 4.8e-18).  8 FP64 ops.
+//              of (2^r - 1)/r (max |error| of r Q(r) 4.8e-18).  8 FP64 ops.  A degree-2 Q
+//              (minimax of the relative error, 2.4e-14; c_cell[21..22] + kCellExpQ2c) serves
+//              the FULL kernels' slots >= 1, whose masses are never carried forward
+//              (bocd_kernel.cuh, EXP3).
 // The coefficients were fitted with 60-digit mpmath (Chebyshev nodes on the reduced
 // interval) and rounded to double; the leading ones are DFMA immediates.  Tables are
 // computed on the host in long double.  Accuracy: tests/test_gpu_fastmath.py.
