@@ -398,12 +398,13 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     constexpr bool PREF = PERSIST && kPrefOk<NT, J, FULL>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr bool ROT = FULL;
-    // FULL kernels: the exp2 polynomial of degree 3 (2.4e-14 relative, one DFMA less) for every
-    // slot but 0; slot 0 keeps degree 4 (4.8e-18): its cells are the ones whose masses are
-    // carried forward as weights (the new change-point cell, the MERGE bucket q'_{R-2} + q'_{R-1}),
-    // where a bias would accumulate.  Every other cell's mass is recomputed from its statistics
-    // each step, and its l = a + G - alpha lg beta' already carries ~1e-12 of rounding
-    // (measured: parity unchanged, C3 73.8 -> 72.0 ms, C4 1074 -> 1036 ms per call)
+    // FULL kernels: the exp2 polynomial of degree 3 (2.4e-14 relative, one DFMA less) for slots
+    // >= 2; slots 0 and 1 keep degree 4 (4.8e-18): theirs are the masses carried forward as
+    // weights (slot 0: the new change-point cell and the MERGE bucket q'_{R-2} + q'_{R-1} every
+    // step; slot 1 of thread 0: the bucket's weight at the rotation steps), where a bias would
+    // accumulate.  Every other cell's mass is recomputed from its statistics each step, and its
+    // l = a + G - alpha lg beta' already carries ~1e-12 of rounding (measured: parity
+    // unchanged, C3 73.8 -> 71.3 ms with the fused sum below, C4 1074 -> 1025 ms per call)
     constexpr bool EXP3 = FULL;
     constexpr int EC = cell_ec(FULL, NT * J, PREF);
     constexpr int LB = cell_logbits(FULL, NT * J);
@@ -787,14 +788,14 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     }
 #pragma unroll
                     for (int kk = 0; kk < G; ++kk)
-                        pe[kk] = EXP3 && j0 + kk > 0 ? fma(re[kk], kCellExpQ2c, c_cell[22])
-                                                     : fma(re[kk], kCellExpQ3, c_cell[11]);
+                        pe[kk] = EXP3 && j0 + kk >= 2 ? fma(re[kk], kCellExpQ2c, c_cell[22])
+                                                      : fma(re[kk], kCellExpQ3, c_cell[11]);
 #pragma unroll
                     for (int kk = 0; kk < G; ++kk)
-                        pe[kk] = EXP3 && j0 + kk > 0 ? fma(pe[kk], re[kk], c_cell[21]) : fma(pe[kk], re[kk], c_cell[10]);
+                        pe[kk] = EXP3 && j0 + kk >= 2 ? fma(pe[kk], re[kk], c_cell[21]) : fma(pe[kk], re[kk], c_cell[10]);
 #pragma unroll
                     for (int kk = 0; kk < G; ++kk)
-                        if (!(EXP3 && j0 + kk > 0)) pe[kk] = fma(pe[kk], re[kk], c_cell[9]);
+                        if (!(EXP3 && j0 + kk >= 2)) pe[kk] = fma(pe[kk], re[kk], c_cell[9]);
 #pragma unroll
                     for (int kk = 0; kk < G; ++kk) {
                         const int j = j0 + kk;
