@@ -607,7 +607,7 @@ static int launch_update(falcon_bocd_t h, const double* x_dev, int64_t ld, int64
         const bool wide = !persist && h->var.fn_w && h->schedule != 3 && units <= nsm * h->per_sm &&
                           S <= nsm * h->var.spb_w &&
                           (S + nsm - 1) / nsm < int64_t(h->var.spb) * ((units + nsm - 1) / nsm);
-        const int64_t grid = persist ? h->grid_cap : wide ? nsm : units;
+        const int64_t grid = persist ? h->grid_cap : wide ? std::min(nsm, S) : units;
         void* args[] = {&P};
         // r* every step only when it is an output (per-step MAP, MAPRESET events); otherwise
         // r* = 1 at every PROB event (theta >= 1/2).
