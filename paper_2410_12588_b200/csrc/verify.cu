@@ -8,8 +8,8 @@
 // Both steps are tiny next to the BOCD recursion (a few thousand events per C3 chunk):
 // one thread per event for the verification (<= 2 x window fp64 loads, sums in index
 // order so the means are bit-identical to the oracle's), one thread per series segment
-// for the pairing state machine, then a single-CTA scan + gather that compacts the
-// events in (series, onset) order.
+// for the pairing state machine, then a tiled scan + gather that compacts the events in
+// (series, onset) order.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -98,31 +98,68 @@ __global__ void pair_segments_kernel(const falcon_verified_cp* __restrict__ v, i
     }
 }
 
-// Exclusive scan of cnt[0..n) into off (single CTA, blocked), total into *total.
-__global__ void scan_counts_kernel(const int64_t* __restrict__ cnt, int64_t n, int64_t* __restrict__ off,
-                                   int64_t* __restrict__ total) {
-    __shared__ int64_t part[1024];
-    const int64_t per = (n + blockDim.x - 1) / blockDim.x;
-    const int64_t lo = int64_t(threadIdx.x) * per, hi = (lo + per < n) ? lo + per : n;
-    int64_t acc = 0;
-    for (int64_t k = lo; k < hi; ++k) acc += cnt[k];
-    part[threadIdx.x] = acc;
+// Exclusive scan of cnt[0..n) into off, total into *total: tiles of kScanTile counts (one
+// per thread), per-tile sums (scan_tiles_kernel, pass 0), their exclusive scan in one CTA
+// (scan_sums_kernel), then every tile rescanned with its offset (scan_tiles_kernel, pass 1).
+constexpr int kScanTile = 1024;
+
+// block-wide inclusive scan of one int64 per thread (1024 threads); returns the inclusive
+// prefix, *tile_total = the tile's sum
+__device__ int64_t block_scan_incl(int64_t v, int64_t* warp_sums, int64_t* tile_total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+    }
+    if (lane == 31) warp_sums[w] = v;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        int64_t run = 0;
-        for (unsigned w = 0; w < blockDim.x; ++w) {
-            const int64_t c = part[w];
-            part[w] = run;
-            run += c;
+    if (w == 0) {
+        int64_t s = warp_sums[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t u = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += u;
         }
-        *total = run;
+        warp_sums[lane] = s;  // inclusive over warps
     }
     __syncthreads();
-    int64_t run = part[threadIdx.x];
-    for (int64_t k = lo; k < hi; ++k) {
-        off[k] = run;
-        run += cnt[k];
+    const int64_t r = v + (w > 0 ? warp_sums[w - 1] : 0);
+    *tile_total = warp_sums[31];
+    return r;
+}
+
+__global__ void __launch_bounds__(kScanTile) scan_tiles_kernel(const int64_t* __restrict__ cnt, int64_t n,
+                                                                int64_t* __restrict__ tile_sum,
+                                                                const int64_t* __restrict__ tile_off,
+                                                                int64_t* __restrict__ off, int pass) {
+    __shared__ int64_t ws[32];
+    const int64_t k = int64_t(blockIdx.x) * kScanTile + threadIdx.x;
+    const int64_t c = k < n ? cnt[k] : 0;
+    int64_t tot;
+    const int64_t incl = block_scan_incl(c, ws, &tot);
+    if (pass == 0) {
+        if (threadIdx.x == 0) tile_sum[blockIdx.x] = tot;
+    } else if (k < n) {
+        off[k] = tile_off[blockIdx.x] + incl - c;
     }
+}
+
+// exclusive scan of the nt tile sums in place (one CTA, kScanTile at a time), total -> *total
+__global__ void __launch_bounds__(kScanTile) scan_sums_kernel(int64_t* __restrict__ s, int64_t nt,
+                                                               int64_t* __restrict__ total) {
+    __shared__ int64_t ws[32];
+    int64_t carry = 0;
+    for (int64_t base = 0; base < nt; base += kScanTile) {
+        const int64_t k = base + threadIdx.x;
+        const int64_t c = k < nt ? s[k] : 0;
+        int64_t tot;
+        const int64_t incl = block_scan_incl(c, ws, &tot);
+        if (k < nt) s[k] = carry + incl - c;
+        carry += tot;
+        __syncthreads();  // ws is reused by the next tile
+    }
+    if (threadIdx.x == 0) *total = carry;
 }
 
 __global__ void gather_kernel(const falcon_failslow_event* __restrict__ tmp, const int64_t* __restrict__ cnt,
@@ -159,16 +196,18 @@ extern "C" int falcon_pair_failslow(const falcon_verified_cp* v_dev, int64_t n, 
     if (n == 0) return FALCON_OK;
     if (!v_dev) return FALCON_EINVAL;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    // workspace: tmp [n] events, cnt [n], off [n], total, bad flag
+    // workspace: tmp [n] events, cnt [n], off [n], tile sums [nt], total, bad flag
     char* ws = nullptr;
+    const int64_t nt = (n + kScanTile - 1) / kScanTile;
     const size_t b_tmp = size_t(n) * sizeof(falcon_failslow_event);
     const size_t b_i64 = size_t(n) * sizeof(int64_t);
-    const size_t bytes = b_tmp + 2 * b_i64 + 2 * sizeof(int64_t);
+    const size_t bytes = b_tmp + 2 * b_i64 + size_t(nt) * sizeof(int64_t) + 2 * sizeof(int64_t);
     if (cudaMallocAsync(reinterpret_cast<void**>(&ws), bytes, st) != cudaSuccess) return FALCON_ENOMEM;
     auto* tmp = reinterpret_cast<falcon_failslow_event*>(ws);
     auto* cnt = reinterpret_cast<int64_t*>(ws + b_tmp);
     auto* off = reinterpret_cast<int64_t*>(ws + b_tmp + b_i64);
-    auto* total = reinterpret_cast<int64_t*>(ws + b_tmp + 2 * b_i64);
+    auto* tsum = reinterpret_cast<int64_t*>(ws + b_tmp + 2 * b_i64);
+    auto* total = tsum + nt;
     auto* bad = reinterpret_cast<int*>(total + 1);
     int rc = FALCON_OK;
     int64_t h_total = 0;
@@ -176,7 +215,9 @@ extern "C" int falcon_pair_failslow(const falcon_verified_cp* v_dev, int64_t n, 
     cudaError_t e = cudaMemsetAsync(bad, 0, sizeof(int), st);
     if (e == cudaSuccess) {
         pair_segments_kernel<<<grid_of(n), 256, 0, st>>>(v_dev, n, tmp, cnt, bad);
-        scan_counts_kernel<<<1, 1024, 0, st>>>(cnt, n, off, total);
+        scan_tiles_kernel<<<unsigned(nt), kScanTile, 0, st>>>(cnt, n, tsum, tsum, off, 0);
+        scan_sums_kernel<<<1, kScanTile, 0, st>>>(tsum, nt, total);
+        scan_tiles_kernel<<<unsigned(nt), kScanTile, 0, st>>>(cnt, n, tsum, tsum, off, 1);
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaMemcpyAsync(&h_total, total, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
