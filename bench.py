@@ -476,7 +476,9 @@ def main():
         v, dt = cpu_baseline_run(cfg, spec, n_s, T_s)
         cpu = {"value": v, "unit": UNIT, "cores": host_cores(), "kind": "oracle",
                "sample": _sample_text(cfg, n_s, T_s, dt)}
-    launches = args.steps * (per_step + 2)  # update kernels + the two drain kernels (device out) per step
+    # per step: the update launches (one per update_chunk call: C5 calls per step, one 1,000-step
+    # launch otherwise) + the two drain kernels (count/scan, gather into device memory)
+    launches = args.steps * ((per_step if streaming else 1) + 2)
     n_events = int(recs.shape[0])
     sb.close()
     if rank == 0:
