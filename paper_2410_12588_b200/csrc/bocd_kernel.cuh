@@ -406,6 +406,10 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     // l = a + G - alpha lg beta' already carries ~1e-12 of rounding (measured: parity
     // unchanged, C3 73.8 -> 71.3 ms with the fused sum below, C4 1074 -> 1025 ms per call)
     constexpr bool EXP3 = FULL;
+    // the owner updates of the scalar tail only in the (one or two) warps holding an owner lane
+    // for groups of >= 8 warps (R = 2048 / 4096: C4 1026 -> 994 ms per call); for 4 warps
+    // (R = 1024) the branch costs more than the skipped selects (71.25 vs 71.53 ms)
+    constexpr bool OWNW = NT >= 256;
     constexpr int EC = cell_ec(FULL, NT * J, PREF);
     constexpr int LB = cell_logbits(FULL, NT * J);
     // the MERGE bucket's multiplicative continuation (below) for R >= 2048, where the log-joint's
@@ -903,7 +907,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 // ROT: branch-free; the new mass is the slot-0 pending weight wq (no log on the
                 // step's critical path), folded into a at the next rotation step.  Generic: one
                 // divergent block for the one or two owner lanes (one shared log2 pass).
-                if constexpr (ROT) {
+                if (ROT && (!OWNW || w == (iB >> 5) || w == ((iB + 1) >> 5))) {  // warps holding an owner
                     const bool ownB = (i == iB);
                     const bool ownA = merge && (i == iB + 1);  // iB = NT-1: thread 0, slot 1 (rotation)
                     const double dcd = double(dc);
@@ -917,7 +921,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     be[0] = ownB ? b0 : be[0];
                     a[0] = ownB ? aB : (ownA ? aA : a[0]);
                     wq = ownB ? wB : (ownA ? wA : wq);
-                } else {
+                } else if constexpr (!ROT) {
                 const bool ownB = (unsigned(kB) % NT) == unsigned(i);
                 const bool ownA = merge && ((unsigned(kA) % NT) == unsigned(i));
                 if (ownB || ownA) {
