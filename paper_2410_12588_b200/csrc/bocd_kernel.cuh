@@ -941,7 +941,10 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                 if (i == 0) gs.zd_prev = Zd;
                 // ---- rare path (group-uniform): MAP run length r* (A7), events (A8), per-step
                 // outputs ----------------------------------------------------------------
-                if (EAGER || (fl & P.ev_mask) || any_out) {
+                // (OWNW: warp 0 only — thread 0 alone writes events and outputs and keeps r*_{t-1}
+                // and the event count; the other warps skip the EAGER per-step work: C4 EAGER
+                // 1326 -> 1293 ms; with 4 warps the branch costs more, 85.0 vs 85.3 for C3)
+                if ((EAGER || (fl & P.ev_mask) || any_out) && (!OWNW || w == 0)) {
                     int r_ex = -1;
                     double qex = 0.0;
                     if constexpr (EAGER) {
