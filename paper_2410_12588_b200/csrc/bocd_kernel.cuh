@@ -877,7 +877,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                     }
                     group_sync<NT>(g);
                     sum = partials_sum<W>(gs.red2[par], lane);
-                    if constexpr (EAGER) {
+                    if (EAGER && (!OWNW || w == 0)) {  // OWNW: only warp 0 reads the argmax
 #pragma unroll
                         for (int ww = 0; ww < W; ++ww) {
                             const unsigned long long o = gs.red1[par][ww];
