@@ -541,7 +541,8 @@ def e2e_run(sb0, bocd, x, col, args, cfg, kw, local, lo, S, n_global, world, dev
     that step's observations from pinned host memory (falcon_bocd_update_chunk_host: staged
     copy overlapped with the previous step's kernel) and reads that step's change points back
     to pinned host memory (drain into device memory, then an asynchronous copy of the drain
-    meta and the fixed-capacity record buffer); N > 1: each step's events are all-gathered."""
+    meta and the fixed-capacity record buffer on a side stream); N > 1: each step's events are
+    all-gathered."""
     import torch
     from paper_2410_12588_b200.distributed import compact_gathered, gather_fixed, max_over_ranks
     streaming = col is not None
@@ -562,6 +563,11 @@ def e2e_run(sb0, bocd, x, col, args, cfg, kw, local, lo, S, n_global, world, dev
     hbuf = [torch.empty((cap, 40), dtype=torch.uint8).pin_memory() for _ in range(args.steps + 1)]
     hmeta = [torch.zeros(4, dtype=torch.int64).pin_memory() for _ in range(args.steps + 1)]
 
+    # the read-back of each step's events runs on a side stream behind an event, so the
+    # device-to-host copy overlaps the next step's update instead of sitting between kernels
+    d2h = torch.cuda.Stream(device=dev)
+    done = [torch.cuda.Event() for _ in range(args.steps + 1)]
+
     def host_step(k, slot):
         h = hb[k % nbuf]
         if streaming:
@@ -570,8 +576,11 @@ def e2e_run(sb0, bocd, x, col, args, cfg, kw, local, lo, S, n_global, world, dev
         else:
             b2.update_chunk_host(h)
         b2.drain_into(dbuf[slot], dmeta[slot])
-        hmeta[slot].copy_(dmeta[slot], non_blocking=True)
-        hbuf[slot].copy_(dbuf[slot], non_blocking=True)
+        done[slot].record(stream)
+        d2h.wait_event(done[slot])
+        with torch.cuda.stream(d2h):
+            hmeta[slot].copy_(dmeta[slot], non_blocking=True)
+            hbuf[slot].copy_(dbuf[slot], non_blocking=True)
         return gather_fixed(dbuf[slot], dmeta[slot]) if world > 1 else None
 
     host_step(0, args.steps)  # warm-up (staging buffers, copy stream)
@@ -582,6 +591,7 @@ def e2e_run(sb0, bocd, x, col, args, cfg, kw, local, lo, S, n_global, world, dev
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     gathered = [host_step(k, k) for k in range(args.steps)]
+    stream.wait_stream(d2h)  # the timed region ends when every step's events are on the host
     e1.record(stream)
     torch.cuda.synchronize()
     et = max_over_ranks(e0.elapsed_time(e1), dev)
