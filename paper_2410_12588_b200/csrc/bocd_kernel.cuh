@@ -110,7 +110,8 @@ struct KParams {
     double ln_omH;                                // log(1-H)
     double c_bucket;                              // c_{R-1}/ln2 (MERGE bucket, FULL)
     double al2_bucket;                            // 2 alpha_{R-1}
-    int a2p1;                                     // 2 alpha0 + 1 (FULL kernels: 2 alpha0 is an integer)
+    int a2p1;                                     // floor(2 alpha0) + 1 (FULL kernels)
+    double f2;                                    // 2 alpha0 - floor(2 alpha0) (FULL kernels, MODE bit 1)
     int mode;                                     // 0 MERGE, 1 DROP
     int prior_first_obs;
     uint32_t ev_mask;
@@ -416,7 +417,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     // larger terms (alpha to 2048, frames of up to 512 steps) would carry ~1e-12 per step of
     // rounding along the bucket's chain (6.3e-10 measured at R = 2048 after 5,120 steps); at
     // R <= 1024 the plain form measures 6.2e-11 after the full 100,000 C3 steps
-    constexpr bool BUCKET_PRED = FULL && NT * J >= 2048 && MODE == 0;
+    constexpr bool BUCKET_PRED = FULL && NT * J >= 2048 && (MODE & 1) == 0;
     // FULL: absolute shared addresses of the per-r tables (the dynamic window starts at
     // kDynBase, checked at entry with the fast-math tables)
     constexpr unsigned kGyBase = kDynBase + bocd_fm_bytes(EC, LB);  // FULL: {G_{r+1}, y_r} rows
@@ -474,7 +475,8 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
     __syncthreads();
     const int ntiles = (P.T + TILE - 1) / TILE;
     const int tl_min = P.t0 == 0 ? 1 : 0;  // no events at global t = 0 (Q8): local steps tl >= tl_min
-    constexpr bool merge = (MODE == 0);  // truncation at R: MERGE (0) or DROP (1)
+    constexpr bool merge = (MODE & 1) == 0;  // truncation at R: MERGE (0) or DROP (1)
+    constexpr bool FRAC = FULL && (MODE & 2);  // 2 alpha0 not an integer: + f2 per cell
     const bool any_out = P.out_map || P.out_pnew || P.out_logz;  // per-step outputs requested
     // argmax-eligible run lengths: MERGE r <= R-3 (slot R-1 is the bucket), DROP r <= R-2
     const int r_elig = merge ? R - 3 : R - 2;
@@ -711,7 +713,7 @@ __global__ void __launch_bounds__(NT* SPB, MINB) bocd_update_kernel(const KParam
                             // r = idx - R for the one slot whose index wrapped (slot 0)
                             const double2 gy = lds_v2f64(unsigned(idx[kk]) * 16u + kGyBase);
                             const int m2 = mb - NT * j - ((j == 0 && idx[kk] >= R) ? R : 0);
-                            ca[kk] = make_double2(gy.x, __int2double_rn(m2));
+                            ca[kk] = make_double2(gy.x, FRAC ? __int2double_rn(m2) + P.f2 : __int2double_rn(m2));
                             yv[kk] = gy.y;
                         } else {
                             ca[kk] = s_ca[idx[kk]];

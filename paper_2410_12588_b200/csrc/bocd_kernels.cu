@@ -25,9 +25,20 @@ static void make_variant_mode(Variant* out) {
     v.group_smem_p = sizeof(GroupSmem<NT, kPrefOk<NT, J, FULL> ? kTileP : kTile>);  // (+ PREF buffer): group_bytes
     *out = v;
 }
-// the truncation mode is a template parameter of the kernels (MERGE / DROP specialised tails)
+// the truncation mode is a template parameter of the kernels (MERGE / DROP specialised tails);
+// MODE bit 1 (FULL kernels only): 2 alpha0 has a fractional part f2, added to the exact
+// integer conversion of 2 alpha0 + r + 1 - f2 (one DADD per cell)
 template <int NT, int J, bool FULL, bool TAB2, int SPB, int MINB>
-static void make_variant(int mode, Variant* out) {
+static void make_variant(int mode, Variant* out, bool frac = false) {
+    if constexpr (FULL) {
+        if (frac) {
+            if (mode == 0)
+                make_variant_mode<NT, J, FULL, TAB2, SPB, MINB, 2>(out);
+            else
+                make_variant_mode<NT, J, FULL, TAB2, SPB, MINB, 3>(out);
+            return;
+        }
+    }
     if (mode == 0)
         make_variant_mode<NT, J, FULL, TAB2, SPB, MINB, 0>(out);
     else
@@ -36,18 +47,21 @@ static void make_variant(int mode, Variant* out) {
 // + the one-CTA-per-SM twins (SPB * MINB groups, MINB = 1) of the one-unit kernels, for a
 // batch that fits one wave unevenly (C2: 1,024 series of R = 512 on 148 SMs are 8 on most SMs
 // in CTAs of 4, at most 7 in balanced CTAs of 8)
-template <int NT, int J, bool FULL, bool TAB2, int SPB, int MINB>
-static void make_variant_w(int mode, Variant* out) {
-    make_variant<NT, J, FULL, TAB2, SPB, MINB>(mode, out);
+template <int NT, int J, bool FULL, bool TAB2, int SPB, int MINB, int MODE>
+static void set_wide(Variant* out) {
     constexpr int W = SPB * MINB;
-    if (mode == 0) {
-        out->fn_w = reinterpret_cast<const void*>(&bocd_update_kernel<NT, J, FULL, TAB2, false, W, 1, false, 0>);
-        out->fn_eager_w = reinterpret_cast<const void*>(&bocd_update_kernel<NT, J, FULL, TAB2, true, W, 1, false, 0>);
-    } else {
-        out->fn_w = reinterpret_cast<const void*>(&bocd_update_kernel<NT, J, FULL, TAB2, false, W, 1, false, 1>);
-        out->fn_eager_w = reinterpret_cast<const void*>(&bocd_update_kernel<NT, J, FULL, TAB2, true, W, 1, false, 1>);
-    }
+    out->fn_w = reinterpret_cast<const void*>(&bocd_update_kernel<NT, J, FULL, TAB2, false, W, 1, false, MODE>);
+    out->fn_eager_w = reinterpret_cast<const void*>(&bocd_update_kernel<NT, J, FULL, TAB2, true, W, 1, false, MODE>);
     out->spb_w = W;
+}
+template <int NT, int J, bool FULL, bool TAB2, int SPB, int MINB>
+static void make_variant_w(int mode, Variant* out, bool frac = false) {
+    make_variant<NT, J, FULL, TAB2, SPB, MINB>(mode, out, frac);
+    const int m = mode + (FULL && frac ? 2 : 0);
+    if (m == 0) set_wide<NT, J, FULL, TAB2, SPB, MINB, 0>(out);
+    else if (m == 1) set_wide<NT, J, FULL, TAB2, SPB, MINB, 1>(out);
+    else if (m == 2) set_wide<NT, J, FULL, TAB2, SPB, MINB, 2>(out);
+    else set_wide<NT, J, FULL, TAB2, SPB, MINB, 3>(out);
 }
 
 // Variant choice: FULL kernels (R = NT*J, compile-time ring arithmetic) for the
@@ -57,17 +71,18 @@ static void make_variant_w(int mode, Variant* out) {
 // (Shapes measured slower for R = 1024 and removed: 128x8 with 3-4 series per CTA, 64x16
 // (J = 16: > 168 registers), 256x4.)
 int select_variant(int R, int mode, double alpha0, Variant* out) {
-    // FULL kernels form 2 alpha_{r+1} = 2 alpha0 + r + 1 as an exact integer conversion: they
-    // need 2 alpha0 to be an integer (the default alpha0 = 1, and every half-integer); other
-    // priors take the generic kernels (table-driven alpha, masked ring arithmetic)
+    // FULL kernels form 2 alpha_{r+1} = 2 alpha0 + r + 1 as the exact integer conversion of
+    // floor(2 alpha0) + 1 + r, plus the fractional part of 2 alpha0 when it has one (MODE bit
+    // 1: one DADD per cell; the default alpha0 = 1 and every half-integer need none)
     const double a2 = 2.0 * alpha0;
-    const bool full_ok = a2 == std::floor(a2) && a2 >= 1.0 && a2 <= double(1 << 20);
+    const bool full_ok = a2 > 0.0 && a2 <= double(1 << 20);
+    const bool frac = a2 != std::floor(a2);
     switch (full_ok ? R : -1) {
-        case 256: make_variant<32, 8, true, true, 8, 2>(mode, out); return 0;
-        case 512: make_variant_w<64, 8, true, true, 4, 2>(mode, out); return 0;
-        case 1024: make_variant_w<128, 8, true, true, 2, 2>(mode, out); return 0;
-        case 2048: make_variant<256, 8, true, false, 1, 2>(mode, out); return 0;
-        case 4096: make_variant<512, 8, true, false, 1, 1>(mode, out); return 0;
+        case 256: make_variant<32, 8, true, true, 8, 2>(mode, out, frac); return 0;
+        case 512: make_variant_w<64, 8, true, true, 4, 2>(mode, out, frac); return 0;
+        case 1024: make_variant_w<128, 8, true, true, 2, 2>(mode, out, frac); return 0;
+        case 2048: make_variant<256, 8, true, false, 1, 2>(mode, out, frac); return 0;
+        case 4096: make_variant<512, 8, true, false, 1, 1>(mode, out, frac); return 0;
         default: break;
     }
     if (R < 2 || R > 4096) return -1;

@@ -566,7 +566,8 @@ static int launch_update(falcon_bocd_t h, const double* x_dev, int64_t ld, int64
         P.ln_omH = log1p(-c.hazard);
         P.c_bucket = h->c_bucket;
         P.al2_bucket = 2.0 * c.alpha0 + double(c.R - 1);
-        P.a2p1 = int(2.0 * c.alpha0) + 1;  // used by the FULL kernels only (2 alpha0 integral there)
+        P.a2p1 = int(std::floor(2.0 * c.alpha0)) + 1;  // FULL kernels: 2 alpha_{r+1} = (a2p1 + r) + f2
+        P.f2 = 2.0 * c.alpha0 - std::floor(2.0 * c.alpha0);
         P.hr = (double)((long double)c.hazard / (1.0L - (long double)c.hazard));
         P.theta = c.threshold;
         P.alpha0 = c.alpha0;

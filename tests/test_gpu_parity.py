@@ -373,15 +373,16 @@ def test_balanced_wave_bit_exact(oracle_mod, R, S, mode):
     parity.record(f"balanced R={R} S={S} mode={mode}", st)
 
 
-@pytest.mark.parametrize("R", [1024, 4096])
-@pytest.mark.parametrize("kappa0,alpha0", [(0.5, 1.5), (2.0, 0.7), (1.0, 3.0)])
+@pytest.mark.parametrize("R", [1024, 4096, 1000])
+@pytest.mark.parametrize("kappa0,alpha0", [(0.5, 1.5), (2.0, 0.7), (1.0, 3.0), (1.0, 0.3)])
 def test_priors_and_per_series_arrays(oracle_mod, R, kappa0, alpha0):
-    """kappa0, alpha0 != 1 at the BASELINE ring sizes (2 alpha0 integral -> FULL kernels with
-    the integer alpha; alpha0 = 0.7 -> the generic kernels of the same shape), with per-series
-    mu0 / beta0 HOST arrays passed through falcon_bocd_config (not prior_first_obs)."""
+    """kappa0, alpha0 != 1 at the BASELINE ring sizes (FULL kernels: 2 alpha_{r+1} as the exact
+    integer conversion of floor(2 alpha0) + 1 + r, plus the fractional part of 2 alpha0 for
+    alpha0 = 0.7 / 0.3) and at R = 1000 (the generic kernels: table-driven alpha), with
+    per-series mu0 / beta0 HOST arrays passed through falcon_bocd_config (not prior_first_obs)."""
     cfg = tracegen.CONFIGS["C3"]
     S = 6
-    T = R + 200 if R == 1024 else 1200
+    T = R + 200 if R <= 1024 else 1200
     x = tracegen.generate(tracegen.make_spec(cfg, n_series=S), 0, S, 0, T)
     rng = np.random.default_rng(R + int(10 * alpha0))
     mu0 = x[:, 0] * rng.uniform(0.8, 1.2, S)

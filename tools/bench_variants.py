@@ -1,6 +1,6 @@
 """Kernel time of one 1,000-step update_chunk for the kernel variants a user can land on:
-the FULL kernels (power-of-two R = NT x J, 2 alpha0 integral) and the generic ones (any other
-R, or a prior with 2 alpha0 not an integer), C3-recipe data, device-resident, CUDA events.
+the FULL kernels (power-of-two R = NT x J; a fractional 2 alpha0 adds one DADD per cell) and the
+generic ones (any other R), C3-recipe data, device-resident, CUDA events.
 One JSON line per case.
 
     python tools/bench_variants.py
@@ -41,7 +41,7 @@ def run(R, alpha0, S, T=1000, reps=3):
     nt, j, spb = b.kernel_shape()
     b.changepoints()
     b.close()
-    full = (R == nt * j) and float(2 * alpha0).is_integer()
+    full = R == nt * j
     cells = S * T * R
     return {"R": R, "alpha0": alpha0, "series": S, "steps": T, "kernel": "FULL" if full else "generic",
             "shape": [nt, j, spb], "ms": ms, "ns_per_kcells": ms * 1e6 / (cells / 1e3),
