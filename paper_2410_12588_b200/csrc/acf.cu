@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(kAcfThreads) acf_kernel(const int32_t* __restr
         double acc[kLagBlk], win[kLagBlk];
 #pragma unroll
         for (int m = 0; m < kLagBlk; ++m) acc[m] = 0.0;
-        if (seg < nseg) {
+        if (seg < nseg && t0 < t1) {  // (the last segments may be empty for short L)
 #pragma unroll
             for (int m = 0; m < kLagBlk - 1; ++m) win[m] = y[pad_idx(t0 + k0 + m)];
             for (int t = t0; t < t1; ++t) {
